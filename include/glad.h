@@ -1,0 +1,208 @@
+/*
+ * glad.h — C ABI of libglad: B200 (sm_100a) decode attention for Grouped
+ * Latent Attention (GLA), Grouped-Tied Attention (GTA) and an MLA baseline,
+ * over a paged cache, with split-KV and a log-sum-exp merge.
+ *
+ * Paper: arXiv 2505.21487, "Hardware-Efficient Attention for Fast Decoding".
+ * Citation key: P:n = line n of the paper text; readings of silent
+ * passages are numbered R1..R16 in DESIGN.md ("Readings").
+ *
+ * Conventions common to every call
+ *  - Pointers are DEVICE pointers unless stated.  The caller owns all memory;
+ *    the library never allocates on the hot path and never synchronises the
+ *    host.  Every kernel-launching call is asynchronous on `stream`
+ *    (cudaStream_t passed as void*; NULL = legacy default stream).
+ *  - Element types: bf16 for q, cache, out; fp32 for lse and partials;
+ *    int32 for block tables and lengths.  All tensors are dense row-major.
+ *  - Errors: host-checkable violations return GLAD_ERR_INVALID_ARG (bad
+ *    shape/dim/alignment), GLAD_ERR_UNSUPPORTED (valid but no kernel built
+ *    for this shape), GLAD_ERR_WORKSPACE (workspace too small) before any
+ *    launch; launch failures return GLAD_ERR_CUDA.  glad_last_error() gives a
+ *    thread-local message naming the offending argument.  Device-side contract
+ *    breaches (page id out of range, seqlens[b] > pages*page_size, a block
+ *    table entry < 0 for a page in use) are undefined behaviour.
+ *  - Calls are stateless and reentrant.  Concurrent append and decode on the
+ *    same pool are forbidden by contract.
+ */
+#ifndef GLAD_H_
+#define GLAD_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define GLAD_API __attribute__((visibility("default")))
+#else
+#define GLAD_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  GLAD_OK = 0,
+  GLAD_ERR_INVALID_ARG = 1,
+  GLAD_ERR_UNSUPPORTED = 2,
+  GLAD_ERR_WORKSPACE = 3,
+  GLAD_ERR_CUDA = 4
+} glad_status;
+
+/* Thread-local description of the last error (never NULL). */
+GLAD_API const char* glad_last_error(void);
+/* Library version string and the compiled target ("sm_100a"). */
+GLAD_API const char* glad_version(void);
+
+/*
+ * Paged cache layout (one per rank).  P:304 paged KV; P:240 latent heads
+ * c_i^KV; P:48 one decoupled RoPE key per token; P:205-213 GTA tied KV +
+ * single-head K_RoPE.
+ *
+ * Row of one token = [head_0 (d_head) | ... | head_{n-1} (d_head) | rope (d_rope) | pad]
+ * (reading R6, pinned by the byte counts P:627).
+ * Pool = [num_pages][page_size][row_stride] bf16, contiguous.
+ *   GLA/MLA: n_heads_kv = latent heads on this rank (h_c / N), d_head = d_c,
+ *            d_rope = d_R.   GTA: n_heads_kv = tied KV heads, d_head = d_h,
+ *            d_rope = d_h/2 (the K_RoPE half).
+ * Requirements: page_size >= 1 (a power of two; page 1 must work),
+ * row_stride >= n_heads_kv*d_head + d_rope and a multiple of 8 (16 B),
+ * pool 16-byte aligned.
+ */
+typedef struct {
+  int32_t num_pages;
+  int32_t page_size;
+  int32_t n_heads_kv;
+  int32_t d_head;
+  int32_t d_rope;
+  int32_t _reserved;
+  int64_t row_stride;
+} glad_cache_layout;
+
+/* Bytes of the pool described by `layout` (host-only, pure). */
+GLAD_API size_t glad_pool_bytes(const glad_cache_layout* layout);
+
+/*
+ * Paged-cache append.  For b < B and i < n_new, token
+ * position p = seqlens_before[b] + i is written to pool row
+ *   block_table[b*bt_stride + p/page_size]*page_size + p%page_size
+ * with the first n_heads_kv*d_head + d_rope elements of row (b, i) of
+ * `rows` [B, n_new, n_heads_kv*d_head + d_rope] bf16 (RoPE part already
+ * rotated by the caller).  Padding columns are not touched.  Bit-exact copy.
+ * block_table: [B, bt_stride] int32 (device).  seqlens_before: [B] int32
+ * (device).  The caller must have allocated the pages.
+ */
+GLAD_API glad_status glad_cache_append(const glad_cache_layout* layout, void* pool, const int32_t* block_table,
+                              int32_t bt_stride, const int32_t* seqlens_before, const void* rows, int32_t B,
+                              int32_t n_new, void* stream);
+
+/*
+ * Debug/test gather through the same paging arithmetic as the decode
+ * producer: dense_out [B, max_len, n_heads_kv*d_head + d_rope] bf16 receives
+ * the logical rows 0..seqlens[b]-1 of each sequence; rows >= seqlens[b] are
+ * zero.  Bit-exact.
+ */
+GLAD_API glad_status glad_paged_gather(const glad_cache_layout* layout, const void* pool, const int32_t* block_table,
+                              int32_t bt_stride, const int32_t* seqlens, int32_t B, int32_t max_len,
+                              void* dense_out, void* stream);
+
+/*
+ * Workspace for split-KV partials: max_splits * B*Lq*H * (d_v + 1) * 4 bytes
+ * (+ alignment).  Zero if max_splits <= 1.
+ */
+GLAD_API size_t glad_decode_workspace_bytes(int32_t B, int32_t Lq, int32_t H, int32_t d_v, int32_t max_splits);
+
+/*
+ * Number of KV splits the heuristic would use (num_splits argument 0), given
+ * only host-known quantities (max KV length bound = bt_stride*page_size).
+ */
+GLAD_API int32_t glad_decode_num_splits(const glad_cache_layout* layout, int32_t B, int32_t Lq, int32_t H,
+                               int32_t bt_stride, int32_t variant);
+
+/*
+ * GLA decode (per rank: O_i = softmax(Q_i (c_i^KV)^T) c_i^KV,
+ * with the decoupled-RoPE score term of P:48 added).
+ *
+ *  q       [B, Lq, H, d_head + d_rope] bf16: absorbed q_nope (d_head = d_c)
+ *          || rotated q_rope (d_rope).  Head h attends to latent head
+ *          h / (H / n_heads_kv) (contiguous groups).
+ *  pool    paged latent cache (layout above).
+ *  seqlens [B] int32: KV length of each sequence INCLUDING the Lq new tokens
+ *          (already appended).  Lq > 1 is speculative decoding.
+ *  causal  1: query t sees keys j <= seqlens[b] - Lq + t (R2); 0: all keys.
+ *  softmax_scale  multiplies q.k (the paper writes no scale, R1).
+ *  out     [B, Lq, H, d_head] bf16 = sum_j p_j c_j (latent space).
+ *  lse     [B, Lq, H] fp32 natural-log LSE (R3); -inf and out = 0 when a
+ *          query has no visible key.
+ *  workspace / ws_bytes  split-KV partials (glad_decode_workspace_bytes with
+ *          the num_splits actually used); may be NULL when that is 1.
+ *  num_splits  0 = heuristic (glad_decode_num_splits); else the requested
+ *          number of KV splits (>= 1).
+ * Requirements: H % n_heads_kv == 0; (d_head, d_rope) in {(128, 32),
+ * (128, 64), (256, 32), (256, 64), (512, 64)}; Lq >= 1; q and out 16-byte
+ * aligned.  Other shapes return GLAD_ERR_UNSUPPORTED.
+ */
+GLAD_API glad_status glad_gla_decode(const void* q, const void* pool, const glad_cache_layout* layout,
+                            const int32_t* block_table, int32_t bt_stride, const int32_t* seqlens, int32_t B,
+                            int32_t Lq, int32_t H, float softmax_scale, int32_t causal, void* out, float* lse,
+                            void* workspace, size_t ws_bytes, int32_t num_splits, void* stream);
+
+/* MLA baseline: GLA with a single latent head (n_heads_kv == 1). */
+GLAD_API glad_status glad_mla_decode(const void* q, const void* pool, const glad_cache_layout* layout,
+                            const int32_t* block_table, int32_t bt_stride, const int32_t* seqlens, int32_t B,
+                            int32_t Lq, int32_t H, float softmax_scale, int32_t causal, void* out, float* lse,
+                            void* workspace, size_t ws_bytes, int32_t num_splits, void* stream);
+
+/*
+ * GTA decode.  q [B, Lq, H, d_head] bf16 = [q_nope (d_head/2) ||
+ * rotated q_rope (d_head/2)] (R4).  Pool rows: n_heads_kv tied states of
+ * d_head + one rotated K_RoPE of d_rope = d_head/2.  Key of group g =
+ * concat(KV_g[:d_head/2], K_RoPE) (tied half never rotated); value = KV_g.
+ * out [B, Lq, H, d_head].  Other arguments as glad_gla_decode.
+ * Requirements: d_head == 128, d_rope == 64.
+ */
+GLAD_API glad_status glad_gta_decode(const void* q, const void* pool, const glad_cache_layout* layout,
+                            const int32_t* block_table, int32_t bt_stride, const int32_t* seqlens, int32_t B,
+                            int32_t Lq, int32_t H, float softmax_scale, int32_t causal, void* out, float* lse,
+                            void* workspace, size_t ws_bytes, int32_t num_splits, void* stream);
+
+/*
+ * Split-KV LSE merge (not in the paper; BASELINE north_star):
+ *   lse = ln sum_s exp(lse_s),  out = sum_s exp(lse_s - lse) * o_s
+ * o_part [S, B, Lq, H, d_v] fp32 (normalised per split), lse_part
+ * [S, B, Lq, H] fp32 (-inf for an empty split).  out [B, Lq, H, d_v] bf16,
+ * lse [B, Lq, H] fp32.  d_v % 8 == 0.
+ */
+GLAD_API glad_status glad_splitkv_combine(const float* o_part, const float* lse_part, int32_t S, int32_t B, int32_t Lq,
+                                 int32_t H, int32_t d_v, void* out, float* lse, void* stream);
+
+/* ---- tp_shard helpers: host-only, pure (no CUDA) ---- */
+
+/* D = ceil(N * g_q / h_q).  Returns -1 on invalid input. */
+GLAD_API int32_t glad_tp_duplication(int32_t N, int32_t g_q, int32_t h_q);
+
+/*
+ * Contiguous ownership for rank `rank` of N: KV/latent heads
+ * [kv_begin, kv_end) and query heads [q_begin, q_end).  When
+ * n_kv_heads < N each KV head is duplicated D = N / n_kv_heads times and its
+ * query heads are split across the replicas.  Output pointers are HOST.
+ */
+GLAD_API glad_status glad_tp_shard(int32_t h_q, int32_t n_kv_heads, int32_t N, int32_t rank, int32_t* kv_begin,
+                          int32_t* kv_end, int32_t* q_begin, int32_t* q_end);
+
+/* Variants for glad_kv_bytes_per_token_per_device. */
+enum { GLAD_MHA = 0, GLAD_MQA = 1, GLAD_GQA = 2, GLAD_GTA = 3, GLAD_GLA = 4, GLAD_MLA = 5 };
+
+/*
+ * KV-cache bytes per token per device for one layer (P:123-131 extended
+ * with the replicated single RoPE head; reproduces P:624-628, P:1000-1004,
+ * P:1299-1305).  n_kv_heads: h_q (MHA), 1 (MQA/MLA), h_kv
+ * (GQA/GTA), h_c (GLA); d_head: d_h or d_c; d_rope: d_h/2 (GTA) or d_R
+ * (GLA/MLA).  Returns -1 on invalid input.
+ */
+GLAD_API int64_t glad_kv_bytes_per_token_per_device(int32_t variant, int32_t n_kv_heads, int32_t d_head, int32_t d_rope,
+                                           int32_t N, int32_t dtype_bytes);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GLAD_H_ */

@@ -1,0 +1,353 @@
+// C ABI of libglad (include/glad.h): argument validation, TMA descriptor
+// encoding, split planning and launches.  Host-only logic; every step of the
+// compute path runs in the kernels of decode.cuh / aux_kernels.cu.
+#include <cudaTypedefs.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+
+#include "../../include/glad.h"
+#include "internal.h"
+
+namespace {
+
+thread_local char g_err[512] = "no error";
+
+glad_status fail(glad_status s, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return s;
+}
+
+bool is_pow2(int x) { return x > 0 && (x & (x - 1)) == 0; }
+int ilog2(int x) {
+  int r = 0;
+  while ((1 << r) < x) ++r;
+  return r;
+}
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+int num_sms() {
+  static int n = [] {
+    int dev = 0, v = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    return v > 0 ? v : 148;
+  }();
+  return n;
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult qr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &qr) != cudaSuccess ||
+        qr != cudaDriverEntryPointSuccess)
+      return static_cast<PFN_cuTensorMapEncodeTiled_v12000>(nullptr);
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+  }();
+  return fn;
+}
+
+glad_status check_layout(const glad_cache_layout* L) {
+  if (!L) return fail(GLAD_ERR_INVALID_ARG, "layout is NULL");
+  if (L->num_pages < 1) return fail(GLAD_ERR_INVALID_ARG, "layout.num_pages=%d must be >= 1", L->num_pages);
+  if (!is_pow2(L->page_size))
+    return fail(GLAD_ERR_INVALID_ARG, "layout.page_size=%d must be a power of two >= 1", L->page_size);
+  if (L->n_heads_kv < 1 || L->d_head < 8 || L->d_rope < 0 || L->d_head % 8 || L->d_rope % 8)
+    return fail(GLAD_ERR_INVALID_ARG, "layout dims n_heads_kv=%d d_head=%d d_rope=%d invalid", L->n_heads_kv,
+                L->d_head, L->d_rope);
+  const int64_t w = static_cast<int64_t>(L->n_heads_kv) * L->d_head + L->d_rope;
+  if (L->row_stride < w || L->row_stride % 8)
+    return fail(GLAD_ERR_INVALID_ARG, "layout.row_stride=%lld must be >= %lld and a multiple of 8",
+                static_cast<long long>(L->row_stride), static_cast<long long>(w));
+  if (static_cast<int64_t>(L->num_pages) * L->page_size >= (int64_t(1) << 31))
+    return fail(GLAD_ERR_INVALID_ARG, "pool has >= 2^31 rows");
+  return GLAD_OK;
+}
+
+int64_t row_width(const glad_cache_layout* L) {
+  return static_cast<int64_t>(L->n_heads_kv) * L->d_head + L->d_rope;
+}
+
+// Choose the split count from host-known data only (max length bound =
+// bt_stride * page_size): fill the SMs with >= 90% wave efficiency, keep
+// >= 8 tiles per split.
+int32_t plan_splits(int64_t units, int64_t max_len) {
+  const int sms = num_sms();
+  const int64_t tiles = (max_len + 127) / 128;
+  const int smax = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(32, tiles / 8)));
+  if (units <= 0) return 1;
+  int best = 1;
+  double best_eff = 0.0;
+  for (int s = 1; s <= smax; ++s) {
+    const double x = static_cast<double>(units) * s / sms;
+    const double eff = x / std::ceil(x);
+    if (eff >= 0.9) return s;
+    if (eff > best_eff + 1e-9) { best_eff = eff; best = s; }
+  }
+  return best;
+}
+
+enum Variant { kGLA, kMLA, kGTA };
+
+struct DecodeGeom {
+  glad::DecodeKey key;
+  int g_q, n_qblk;
+};
+
+glad_status decode_geom(Variant v, const glad_cache_layout* L, int32_t Lq, int32_t H, DecodeGeom* g) {
+  glad_status s = check_layout(L);
+  if (s != GLAD_OK) return s;
+  if (Lq < 1) return fail(GLAD_ERR_INVALID_ARG, "Lq=%d must be >= 1", Lq);
+  if (H < 1 || H % L->n_heads_kv)
+    return fail(GLAD_ERR_INVALID_ARG, "H=%d must be a positive multiple of n_heads_kv=%d", H, L->n_heads_kv);
+  if (v == kMLA && L->n_heads_kv != 1)
+    return fail(GLAD_ERR_INVALID_ARG, "MLA requires n_heads_kv == 1 (got %d)", L->n_heads_kv);
+  if (v == kGTA && L->d_rope * 2 != L->d_head)
+    return fail(GLAD_ERR_INVALID_ARG, "GTA requires d_rope == d_head/2 (got d_head=%d d_rope=%d)", L->d_head,
+                L->d_rope);
+  g->g_q = H / L->n_heads_kv;
+  g->key.d_v = L->d_head;
+  g->key.d_kn = (v == kGTA) ? L->d_head / 2 : L->d_head;
+  g->key.d_r = L->d_rope;
+  const int64_t nq_total = static_cast<int64_t>(Lq) * g->g_q;
+  const int maxnq = glad::decode_max_nq(L->d_head);
+  g->key.nq = nq_total <= 16 ? 16 : nq_total <= 32 ? 32 : maxnq;
+  g->n_qblk = static_cast<int>((nq_total + g->key.nq - 1) / g->key.nq);
+  if (!glad::decode_supported(g->key))
+    return fail(GLAD_ERR_UNSUPPORTED, "no decode kernel for d_head=%d d_rope=%d (variant %d, rows/CTA %d)",
+                L->d_head, L->d_rope, static_cast<int>(v), g->key.nq);
+  if (static_cast<int64_t>(L->n_heads_kv) * g->n_qblk > 65535)
+    return fail(GLAD_ERR_UNSUPPORTED, "too many head blocks");
+  return GLAD_OK;
+}
+
+size_t ws_bytes_for(int64_t rows, int32_t d_v, int32_t S) {
+  if (S <= 1) return 0;
+  const size_t o = static_cast<size_t>(S) * rows * d_v * sizeof(float);
+  const size_t l = static_cast<size_t>(S) * rows * sizeof(float);
+  return ((o + 255) & ~size_t(255)) + ((l + 255) & ~size_t(255));
+}
+
+glad_status decode_common(Variant v, const void* q, const void* pool, const glad_cache_layout* L,
+                          const int32_t* block_table, int32_t bt_stride, const int32_t* seqlens, int32_t B,
+                          int32_t Lq, int32_t H, float scale, int32_t causal, void* out, float* lse, void* ws,
+                          size_t ws_bytes, int32_t num_splits, void* stream) {
+  DecodeGeom g;
+  glad_status s = decode_geom(v, L, Lq, H, &g);
+  if (s != GLAD_OK) return s;
+  if (B < 0) return fail(GLAD_ERR_INVALID_ARG, "B=%d < 0", B);
+  if (B == 0) return GLAD_OK;
+  if (B > 65535) return fail(GLAD_ERR_UNSUPPORTED, "B=%d > 65535", B);
+  if (!q || !pool || !block_table || !seqlens || !out || !lse)
+    return fail(GLAD_ERR_INVALID_ARG, "NULL tensor pointer (q=%p pool=%p bt=%p seqlens=%p out=%p lse=%p)", q,
+                pool, block_table, seqlens, out, lse);
+  if (!aligned16(q) || !aligned16(pool) || !aligned16(out))
+    return fail(GLAD_ERR_INVALID_ARG, "q, pool and out must be 16-byte aligned");
+  if (bt_stride < 1) return fail(GLAD_ERR_INVALID_ARG, "bt_stride=%d < 1", bt_stride);
+  if (!(scale > 0.f) || !std::isfinite(scale))
+    return fail(GLAD_ERR_INVALID_ARG, "softmax_scale=%g must be finite and > 0", scale);
+  if (num_splits < 0) return fail(GLAD_ERR_INVALID_ARG, "num_splits=%d < 0", num_splits);
+  const int64_t units = static_cast<int64_t>(B) * L->n_heads_kv * g.n_qblk;
+  const int64_t max_len = static_cast<int64_t>(bt_stride) * L->page_size;
+  int32_t S = num_splits > 0 ? num_splits : plan_splits(units, max_len);
+  if (S > 65535) return fail(GLAD_ERR_INVALID_ARG, "num_splits=%d too large", S);
+  const int64_t rows = static_cast<int64_t>(B) * Lq * H;
+  const size_t need = ws_bytes_for(rows, L->d_head, S);
+  if (S > 1 && (ws == nullptr || ws_bytes < need))
+    return fail(GLAD_ERR_WORKSPACE, "workspace %zu bytes < required %zu for %d splits", ws_bytes, need, S);
+
+  auto enc = encode_fn();
+  if (!enc) return fail(GLAD_ERR_CUDA, "cuTensorMapEncodeTiled entry point unavailable");
+  CUtensorMap tmap;
+  const int box_rows = L->page_size < 128 ? L->page_size : 128;
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(row_width(L)),
+                        static_cast<cuuint64_t>(L->num_pages) * static_cast<cuuint64_t>(L->page_size)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(L->row_stride) * 2};
+  cuuint32_t box[2] = {64u, static_cast<cuuint32_t>(box_rows)};
+  cuuint32_t estr[2] = {1u, 1u};
+  CUresult cr = enc(&tmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(pool), dims, strides, box, estr,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (cr != CUDA_SUCCESS) return fail(GLAD_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", static_cast<int>(cr));
+
+  glad::DecodeParams p;
+  p.q = static_cast<const __nv_bfloat16*>(q);
+  p.block_table = block_table;
+  p.seqlens = seqlens;
+  p.out = static_cast<__nv_bfloat16*>(out);
+  p.lse = lse;
+  const size_t o_bytes = ((static_cast<size_t>(S) * rows * L->d_head * sizeof(float)) + 255) & ~size_t(255);
+  p.o_part = S > 1 ? static_cast<float*>(ws) : nullptr;
+  p.lse_part = S > 1 ? reinterpret_cast<float*>(static_cast<char*>(ws) + o_bytes) : nullptr;
+  p.bt_stride = bt_stride;
+  p.B = B;
+  p.Lq = Lq;
+  p.H = H;
+  p.g_q = g.g_q;
+  p.d_head = L->d_head;
+  p.rope_col = L->n_heads_kv * L->d_head;
+  p.page_size = L->page_size;
+  p.log2_page = ilog2(L->page_size);
+  p.box_rows = box_rows;
+  p.num_splits = S;
+  p.n_qblk = g.n_qblk;
+  p.causal = causal ? 1 : 0;
+  p.scale_log2 = scale * 1.4426950408889634f;
+  dim3 grid(static_cast<unsigned>(S), static_cast<unsigned>(L->n_heads_kv * g.n_qblk), static_cast<unsigned>(B));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  cudaError_t e = glad::launch_decode(g.key, tmap, p, grid, st);
+  if (e != cudaSuccess) return fail(GLAD_ERR_CUDA, "decode launch failed: %s", cudaGetErrorString(e));
+  if (S > 1) {
+    e = glad::launch_combine(p.o_part, p.lse_part, S, rows, L->d_head, out, lse, st);
+    if (e != cudaSuccess) return fail(GLAD_ERR_CUDA, "combine launch failed: %s", cudaGetErrorString(e));
+  }
+  return GLAD_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* glad_last_error(void) { return g_err; }
+
+const char* glad_version(void) { return "glad 0.1.0 sm_100a"; }
+
+size_t glad_pool_bytes(const glad_cache_layout* L) {
+  if (check_layout(L) != GLAD_OK) return 0;
+  return static_cast<size_t>(L->num_pages) * L->page_size * static_cast<size_t>(L->row_stride) * 2;
+}
+
+glad_status glad_cache_append(const glad_cache_layout* L, void* pool, const int32_t* block_table, int32_t bt_stride,
+                              const int32_t* seqlens_before, const void* rows, int32_t B, int32_t n_new,
+                              void* stream) {
+  glad_status s = check_layout(L);
+  if (s != GLAD_OK) return s;
+  if (B < 0 || n_new < 0) return fail(GLAD_ERR_INVALID_ARG, "B=%d n_new=%d must be >= 0", B, n_new);
+  if (B == 0 || n_new == 0) return GLAD_OK;
+  if (!pool || !block_table || !seqlens_before || !rows) return fail(GLAD_ERR_INVALID_ARG, "NULL pointer");
+  if (!aligned16(pool) || !aligned16(rows)) return fail(GLAD_ERR_INVALID_ARG, "pool/rows must be 16-byte aligned");
+  if (bt_stride < 1) return fail(GLAD_ERR_INVALID_ARG, "bt_stride=%d < 1", bt_stride);
+  cudaError_t e = glad::launch_append(pool, L->row_stride, L->page_size, block_table, bt_stride, seqlens_before,
+                                      rows, B, n_new, static_cast<int32_t>(row_width(L)),
+                                      static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return fail(GLAD_ERR_CUDA, "append launch failed: %s", cudaGetErrorString(e));
+  return GLAD_OK;
+}
+
+glad_status glad_paged_gather(const glad_cache_layout* L, const void* pool, const int32_t* block_table,
+                              int32_t bt_stride, const int32_t* seqlens, int32_t B, int32_t max_len, void* dense_out,
+                              void* stream) {
+  glad_status s = check_layout(L);
+  if (s != GLAD_OK) return s;
+  if (B < 0 || max_len < 0) return fail(GLAD_ERR_INVALID_ARG, "B=%d max_len=%d must be >= 0", B, max_len);
+  if (B == 0 || max_len == 0) return GLAD_OK;
+  if (!pool || !block_table || !seqlens || !dense_out) return fail(GLAD_ERR_INVALID_ARG, "NULL pointer");
+  if (!aligned16(pool) || !aligned16(dense_out))
+    return fail(GLAD_ERR_INVALID_ARG, "pool/dense_out must be 16-byte aligned");
+  cudaError_t e = glad::launch_gather(pool, L->row_stride, L->page_size, block_table, bt_stride, seqlens, B, max_len,
+                                      static_cast<int32_t>(row_width(L)), dense_out,
+                                      static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return fail(GLAD_ERR_CUDA, "gather launch failed: %s", cudaGetErrorString(e));
+  return GLAD_OK;
+}
+
+size_t glad_decode_workspace_bytes(int32_t B, int32_t Lq, int32_t H, int32_t d_v, int32_t max_splits) {
+  if (B <= 0 || Lq <= 0 || H <= 0 || d_v <= 0) return 0;
+  return ws_bytes_for(static_cast<int64_t>(B) * Lq * H, d_v, max_splits);
+}
+
+int32_t glad_decode_num_splits(const glad_cache_layout* L, int32_t B, int32_t Lq, int32_t H, int32_t bt_stride,
+                               int32_t variant) {
+  DecodeGeom g;
+  Variant v = variant == GLAD_GTA ? kGTA : variant == GLAD_MLA ? kMLA : kGLA;
+  if (decode_geom(v, L, Lq, H, &g) != GLAD_OK || B <= 0 || bt_stride <= 0) return -1;
+  return plan_splits(static_cast<int64_t>(B) * L->n_heads_kv * g.n_qblk,
+                     static_cast<int64_t>(bt_stride) * L->page_size);
+}
+
+glad_status glad_gla_decode(const void* q, const void* pool, const glad_cache_layout* layout,
+                            const int32_t* block_table, int32_t bt_stride, const int32_t* seqlens, int32_t B,
+                            int32_t Lq, int32_t H, float softmax_scale, int32_t causal, void* out, float* lse,
+                            void* workspace, size_t ws_bytes, int32_t num_splits, void* stream) {
+  return decode_common(kGLA, q, pool, layout, block_table, bt_stride, seqlens, B, Lq, H, softmax_scale, causal, out,
+                       lse, workspace, ws_bytes, num_splits, stream);
+}
+
+glad_status glad_mla_decode(const void* q, const void* pool, const glad_cache_layout* layout,
+                            const int32_t* block_table, int32_t bt_stride, const int32_t* seqlens, int32_t B,
+                            int32_t Lq, int32_t H, float softmax_scale, int32_t causal, void* out, float* lse,
+                            void* workspace, size_t ws_bytes, int32_t num_splits, void* stream) {
+  return decode_common(kMLA, q, pool, layout, block_table, bt_stride, seqlens, B, Lq, H, softmax_scale, causal, out,
+                       lse, workspace, ws_bytes, num_splits, stream);
+}
+
+glad_status glad_gta_decode(const void* q, const void* pool, const glad_cache_layout* layout,
+                            const int32_t* block_table, int32_t bt_stride, const int32_t* seqlens, int32_t B,
+                            int32_t Lq, int32_t H, float softmax_scale, int32_t causal, void* out, float* lse,
+                            void* workspace, size_t ws_bytes, int32_t num_splits, void* stream) {
+  return decode_common(kGTA, q, pool, layout, block_table, bt_stride, seqlens, B, Lq, H, softmax_scale, causal, out,
+                       lse, workspace, ws_bytes, num_splits, stream);
+}
+
+glad_status glad_splitkv_combine(const float* o_part, const float* lse_part, int32_t S, int32_t B, int32_t Lq,
+                                 int32_t H, int32_t d_v, void* out, float* lse, void* stream) {
+  if (S < 1 || B < 0 || Lq < 1 || H < 1 || d_v < 8 || d_v % 8)
+    return fail(GLAD_ERR_INVALID_ARG, "combine dims S=%d B=%d Lq=%d H=%d d_v=%d invalid", S, B, Lq, H, d_v);
+  if (B == 0) return GLAD_OK;
+  if (!o_part || !lse_part || !out || !lse) return fail(GLAD_ERR_INVALID_ARG, "NULL pointer");
+  if (!aligned16(o_part) || !aligned16(out)) return fail(GLAD_ERR_INVALID_ARG, "o_part/out must be 16-byte aligned");
+  cudaError_t e = glad::launch_combine(o_part, lse_part, S, static_cast<int64_t>(B) * Lq * H, d_v, out, lse,
+                                       static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return fail(GLAD_ERR_CUDA, "combine launch failed: %s", cudaGetErrorString(e));
+  return GLAD_OK;
+}
+
+int32_t glad_tp_duplication(int32_t N, int32_t g_q, int32_t h_q) {
+  if (N < 1 || g_q < 1 || h_q < 1 || g_q > h_q) return -1;
+  return static_cast<int32_t>((static_cast<int64_t>(N) * g_q + h_q - 1) / h_q);
+}
+
+glad_status glad_tp_shard(int32_t h_q, int32_t n_kv_heads, int32_t N, int32_t rank, int32_t* kv_begin,
+                          int32_t* kv_end, int32_t* q_begin, int32_t* q_end) {
+  if (!kv_begin || !kv_end || !q_begin || !q_end) return fail(GLAD_ERR_INVALID_ARG, "NULL output pointer");
+  if (h_q < 1 || n_kv_heads < 1 || N < 1 || rank < 0 || rank >= N)
+    return fail(GLAD_ERR_INVALID_ARG, "h_q=%d n_kv=%d N=%d rank=%d invalid", h_q, n_kv_heads, N, rank);
+  if (h_q % n_kv_heads) return fail(GLAD_ERR_INVALID_ARG, "n_kv_heads=%d must divide h_q=%d", n_kv_heads, h_q);
+  if (h_q % N) return fail(GLAD_ERR_INVALID_ARG, "N=%d must divide h_q=%d", N, h_q);
+  if (n_kv_heads >= N) {
+    if (n_kv_heads % N) return fail(GLAD_ERR_INVALID_ARG, "N=%d must divide n_kv_heads=%d", N, n_kv_heads);
+    const int per = n_kv_heads / N;
+    *kv_begin = rank * per;
+    *kv_end = (rank + 1) * per;
+  } else {
+    if (N % n_kv_heads) return fail(GLAD_ERR_INVALID_ARG, "n_kv_heads=%d must divide N=%d", n_kv_heads, N);
+    const int D = N / n_kv_heads;
+    *kv_begin = rank / D;
+    *kv_end = rank / D + 1;
+  }
+  const int qp = h_q / N;
+  *q_begin = rank * qp;
+  *q_end = (rank + 1) * qp;
+  return GLAD_OK;
+}
+
+int64_t glad_kv_bytes_per_token_per_device(int32_t variant, int32_t n_kv_heads, int32_t d_head, int32_t d_rope,
+                                           int32_t N, int32_t dtype_bytes) {
+  if (n_kv_heads < 1 || d_head < 1 || d_rope < 0 || N < 1 || dtype_bytes < 1) return -1;
+  int m_kv;
+  bool rope;
+  switch (variant) {
+    case GLAD_MHA: case GLAD_MQA: case GLAD_GQA: m_kv = 2; rope = false; break;
+    case GLAD_GTA: case GLAD_GLA: case GLAD_MLA: m_kv = 1; rope = true; break;
+    default: return -1;
+  }
+  const int64_t heads = std::max<int64_t>(1, (n_kv_heads + N - 1) / N);
+  return (static_cast<int64_t>(m_kv) * heads * d_head + (rope ? d_rope : 0)) * dtype_bytes;
+}
+
+}  // extern "C"

@@ -1,0 +1,493 @@
+// Paged GLA / MLA / GTA decode attention for sm_100a (tcgen05 + TMEM + TMA).
+//
+// What it computes (per query row n of a (batch b, latent/KV head i) unit):
+//   s_j = scale * (q_nope . K_nope_j + q_rope . k_rope_j),  j visible
+//   o   = sum_j softmax(s)_j V_j,   lse = ln sum_j exp(s_j)
+// GLA/MLA: K_nope = V = latent c_i (d_c), k_rope = the
+// token's single decoupled RoPE key.  GTA: K_nope = first half of
+// the tied state, V = the full tied state, k_rope = the single K_RoPE head.
+//
+// B200 design ("swap-AB"):
+//  * tokens sit on the UMMA M axis (M = 128 = one tile of T tokens), the
+//    g_q*Lq query rows that share the latent head sit on N (16/32/64).  This
+//    keeps every tcgen05.mma at the full-rate M = 128 shape even for g_q = 8.
+//  * S^T[T x NQ] = K_tile . Q^T    (A = KV tile, K-major SW128, straight from
+//    the TMA-staged paged rows; B = Q, K-major SW128) -> TMEM, double-buffered.
+//  * O^T[D_V x NQ] += V^T . P^T    (A = the SAME smem KV tile read MN-major:
+//    the latent is loaded once and reused as K and V; B = P^T bf16,
+//    MN-major no-swizzle, written by the softmax warps) -> TMEM accumulator.
+//  * Paged loads: one 2-D TMA box of [min(page,128) rows x 64 cols] per
+//    (page run, 64-column chunk); the row coordinate comes from the block
+//    table (int32, one lookup per page run; the TMA unit does the address
+//    generation that P:301-318 does with cooperative cp.async).
+//  * Warp roles (384 threads): w0 TMA producer, w1 UMMA issuer (one thread),
+//    w2-3 Q loader (+ TMEM alloc), w4-7 / w8-11 two softmax warpgroups, each
+//    owning half of the query columns for all 128 token lanes.
+//  * Online softmax with lazy rescaling: the running max only moves when a
+//    score exceeds it by > 2^8 (vote via barrier.red.or), so the cross-lane
+//    max reduction and the TMEM O rescale run on a handful of tiles per unit.
+//  * Split-KV: blockIdx.x = split; partial (o / l, lse) go to a workspace and
+//    glad_splitkv_combine merges them (LSE merge).
+#pragma once
+#include <cuda.h>
+#include <cuda_bf16.h>
+
+#include "ptx.cuh"
+
+namespace glad {
+
+struct DecodeParams {
+  const __nv_bfloat16* q;   // [B, Lq, H, DQ]
+  const int32_t* block_table;
+  const int32_t* seqlens;
+  __nv_bfloat16* out;       // [B, Lq, H, D_V]
+  float* lse;               // [B, Lq, H]
+  float* o_part;            // [S, B, Lq, H, D_V]
+  float* lse_part;          // [S, B, Lq, H]
+  int32_t bt_stride;
+  int32_t B, Lq, H, g_q;
+  int32_t d_head;           // column offset between heads in a cache row
+  int32_t rope_col;         // column of the RoPE part in a cache row
+  int32_t page_size, log2_page, box_rows;
+  int32_t num_splits, n_qblk;
+  int32_t causal;
+  float scale_log2;         // softmax_scale * log2(e)
+};
+
+template <int D_V_, int D_KN_, int D_R_, int NQ_>
+struct DecodeCfg {
+  static constexpr int D_V = D_V_;    // value width (= state width)
+  static constexpr int D_KN = D_KN_;  // key part taken from the state
+  static constexpr int D_R = D_R_;    // rope width
+  static constexpr int NQ = NQ_;      // query rows per CTA (UMMA N)
+  static constexpr int T = 128;       // tokens per tile (UMMA M)
+  static constexpr int DQ = D_KN + D_R;
+  static constexpr int NCH_V = D_V / 64;
+  static constexpr int NCH = NCH_V + 1;  // + rope chunk
+  static constexpr int NCH_QK = D_KN / 64;
+  static constexpr int NQCH = NCH_QK + 1;
+  static constexpr int RK = D_R / 16;
+  static constexpr int CHUNK = T * 128;  // one [128 tokens x 64 cols] bf16 box set
+  static constexpr int STAGE = NCH * CHUNK;
+  static constexpr int QCHUNK = NQ * 128;
+  static constexpr int QBYTES = NQCH * QCHUNK;
+  static constexpr int PBYTES = T * NQ * 2;
+  static constexpr int NBLK_O = D_V / 128;
+  static constexpr int NWG = 2;
+  static constexpr int CW = NQ / NWG;
+  static constexpr int AUX = 2048;
+  static constexpr int AVAIL = 227 * 1024 - 1024 - AUX;
+  static constexpr int NP = (AVAIL - QBYTES - 2 * STAGE - 2 * PBYTES >= 0) ? 2 : 1;
+  static constexpr int NS_RAW = (AVAIL - QBYTES - NP * PBYTES) / STAGE;
+  static constexpr int NS = NS_RAW > 4 ? 4 : NS_RAW;
+  static constexpr int OFF_Q = NS * STAGE;
+  static constexpr int OFF_P = OFF_Q + QBYTES;
+  static constexpr int OFF_AUX = OFF_P + NP * PBYTES;
+  static constexpr int SMEM_BYTES = 1024 + OFF_AUX + AUX;
+  static constexpr int TMEM_O = 2 * NQ;
+  static constexpr int TMEM_USED = 2 * NQ + NBLK_O * NQ;
+  static constexpr int TMEM_COLS =
+      TMEM_USED <= 32 ? 32 : TMEM_USED <= 64 ? 64 : TMEM_USED <= 128 ? 128 : TMEM_USED <= 256 ? 256 : 512;
+  static constexpr int NTHREADS = 384;
+  static_assert(NS >= 1, "a KV stage does not fit in shared memory");
+  static_assert(D_V % 128 == 0 && D_KN % 64 == 0 && D_KN <= D_V, "unsupported head dims");
+  static_assert(D_R % 16 == 0 && D_R >= 16 && D_R <= 64, "unsupported rope dim");
+  static_assert(NQ == 16 || NQ == 32 || NQ == 64, "NQ must be 16/32/64");
+  static_assert(TMEM_USED <= 512, "TMEM budget");
+  static_assert(QCHUNK % 1024 == 0, "Q chunk alignment");
+};
+
+// Column reduction of a warp: v[CW] per lane (lane = token) -> every lane
+// returns the reduction over the 32 lanes of column (lane >> (5 - log2 CW)).
+// Halving butterfly: CW-1 shuffles instead of 5*CW.
+template <int CW, bool MAX>
+__device__ __forceinline__ float warp_col_reduce(float (&v)[CW], int lane) {
+  static_assert(CW >= 2 && CW <= 32 && (CW & (CW - 1)) == 0, "CW");
+  int o = 16;
+#pragma unroll
+  for (int K = CW; K > 1; K >>= 1, o >>= 1) {
+    const bool upper = (lane & o) != 0;
+#pragma unroll
+    for (int i = 0; i < K / 2; ++i) {
+      const float send = upper ? v[i] : v[i + K / 2];
+      const float keep = upper ? v[i + K / 2] : v[i];
+      const float recv = __shfl_xor_sync(0xffffffffu, send, o);
+      v[i] = MAX ? fmaxf(keep, recv) : keep + recv;
+    }
+  }
+#pragma unroll
+  for (; o >= 1; o >>= 1) {
+    const float recv = __shfl_xor_sync(0xffffffffu, v[0], o);
+    v[0] = MAX ? fmaxf(v[0], recv) : v[0] + recv;
+  }
+  return v[0];
+}
+template <int CW>
+__device__ __forceinline__ constexpr int col_shift() {
+  return CW == 32 ? 0 : CW == 16 ? 1 : CW == 8 ? 2 : CW == 4 ? 3 : 4;
+}
+
+template <class C>
+__device__ __forceinline__ void tmem_load_cols(uint32_t taddr, float (&x)[C::CW]) {
+  if constexpr (C::CW % 16 == 0) {
+#pragma unroll
+    for (int cc = 0; cc < C::CW; cc += 16) tmem_ld16(taddr + cc, x + cc);
+  } else {
+#pragma unroll
+    for (int cc = 0; cc < C::CW; cc += 8) tmem_ld8(taddr + cc, x + cc);
+  }
+}
+template <class C>
+__device__ __forceinline__ void tmem_store_cols(uint32_t taddr, const float (&x)[C::CW]) {
+  if constexpr (C::CW % 16 == 0) {
+#pragma unroll
+    for (int cc = 0; cc < C::CW; cc += 16) tmem_st16(taddr + cc, x + cc);
+  } else {
+#pragma unroll
+    for (int cc = 0; cc < C::CW; cc += 8) tmem_st8(taddr + cc, x + cc);
+  }
+}
+
+template <class C>
+__global__ void __launch_bounds__(C::NTHREADS, 1)
+    decode_kernel(const __grid_constant__ CUtensorMap tmap, const DecodeParams p) {
+  constexpr int T = C::T, NQ = C::NQ, CW = C::CW, NS = C::NS, NP = C::NP;
+  constexpr float TAU = 8.0f;  // lazy-rescale threshold (log2 units)
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const uint32_t sbase = smem_u32(smem);
+  uint8_t* aux = smem + C::OFF_AUX;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(aux);
+  uint64_t* kv_full = bars;       // [4]
+  uint64_t* kv_empty = bars + 4;  // [4]
+  uint64_t* s_full = bars + 8;    // [2]
+  uint64_t* s_empty = bars + 10;  // [2]
+  uint64_t* p_full = bars + 12;   // [2]
+  uint64_t* p_empty = bars + 14;  // [2]
+  uint64_t* q_full = bars + 16;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(aux + 256);
+  int* vend_s = reinterpret_cast<int*>(aux + 320);       // [NQ] visible-key end per query column
+  float* m_s = reinterpret_cast<float*>(aux + 640);      // [NQ] final running max
+  float* red = reinterpret_cast<float*>(aux + 1024);     // [2 wg][4 warps][32]
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int b = blockIdx.z;
+  const int head = blockIdx.y / p.n_qblk;
+  const int qb = blockIdx.y - head * p.n_qblk;
+  const int split = blockIdx.x;
+  const int L = p.seqlens[b];
+  const int nq_total = p.Lq * p.g_q;
+  const int n0 = qb * NQ;
+  const int nq = min(NQ, nq_total - n0);
+  int kv_end = L;
+  if (p.causal) {
+    const int t_last = (n0 + nq - 1) / p.g_q;
+    kv_end = max(0, min(L, L - p.Lq + t_last + 1));
+  }
+  const int ntiles_all = (kv_end + T - 1) / T;
+  const int per = (ntiles_all + p.num_splits - 1) / p.num_splits;
+  const int tile_begin = split * per;
+  const int ntiles = max(0, min(ntiles_all, tile_begin + per) - tile_begin);
+  const size_t n_rows_total = static_cast<size_t>(p.B) * p.Lq * p.H;
+
+  if (ntiles == 0) {  // nothing visible in this split: empty partial / empty output
+    for (int idx = threadIdx.x; idx < nq * C::D_V; idx += blockDim.x) {
+      const int n = idx / C::D_V, d = idx - n * C::D_V;
+      const int ng = n0 + n, t = ng / p.g_q, h = head * p.g_q + (ng - t * p.g_q);
+      const size_t row = (static_cast<size_t>(b) * p.Lq + t) * p.H + h;
+      if (p.num_splits == 1) {
+        p.out[row * C::D_V + d] = __float2bfloat16(0.f);
+        if (d == 0) p.lse[row] = -INFINITY;
+      } else {
+        p.o_part[(split * n_rows_total + row) * C::D_V + d] = 0.f;
+        if (d == 0) p.lse_part[split * n_rows_total + row] = -INFINITY;
+      }
+    }
+    return;
+  }
+
+  // ------------------------------------------------------------- setup
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < NS; ++i) { mbar_init(&kv_full[i], 1); mbar_init(&kv_empty[i], 1); }
+    for (int i = 0; i < 2; ++i) { mbar_init(&s_full[i], 1); mbar_init(&s_empty[i], 8); }
+    for (int i = 0; i < NP; ++i) { mbar_init(&p_full[i], 8); mbar_init(&p_empty[i], 1); }
+    mbar_init(q_full, 64);
+    fence_barrier_init();
+    tma_prefetch_desc(&tmap);
+  }
+  if (threadIdx.x < NQ) {
+    const int n = threadIdx.x;
+    int ve = 0;
+    if (n < nq) {
+      const int t = (n0 + n) / p.g_q;
+      ve = p.causal ? max(0, min(L, L - p.Lq + t + 1)) : L;
+    }
+    vend_s[n] = ve;
+  }
+  if (warp == 2) { tmem_alloc(tmem_slot, C::TMEM_COLS); tmem_relinquish(); }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    // ========================= TMA producer (all 32 lanes issue) =========================
+    const int* bt_row = p.block_table + static_cast<size_t>(b) * p.bt_stride;
+    const int box_rows = p.box_rows;
+    for (int it = 0; it < ntiles; ++it) {
+      const int stage = it % NS;
+      mbar_wait(&kv_empty[stage], ((it / NS) & 1) ^ 1);
+      const int p0 = (tile_begin + it) * T;
+      const int ntok = min(T, kv_end - p0);
+      const int nbox = (ntok + box_rows - 1) / box_rows;
+      if (lane == 0) mbar_arrive_expect_tx(&kv_full[stage], static_cast<uint32_t>(nbox * C::NCH * box_rows * 128));
+      __syncwarp();
+      for (int bx = lane; bx < nbox * C::NCH; bx += 32) {
+        const int box = bx / C::NCH, ch = bx - box * C::NCH;
+        const int pos = p0 + box * box_rows;
+        const int page = __ldg(bt_row + (pos >> p.log2_page));
+        const int row = page * p.page_size + (pos & (p.page_size - 1));
+        const int col = ch < C::NCH_V ? head * p.d_head + ch * 64 : p.rope_col;
+        const uint32_t dst = sbase + stage * C::STAGE + ch * C::CHUNK + box * box_rows * 128;
+        tma_load_2d(dst, &tmap, &kv_full[stage], col, row);
+      }
+    }
+  } else if (warp == 1) {
+    // ========================= UMMA issuer (one thread) =========================
+    if (lane == 0) {
+      mbar_wait(q_full, 0);
+      tc_fence_after();
+      constexpr uint32_t idesc_qk = make_idesc_bf16(128, NQ, false, false);
+      constexpr uint32_t idesc_pv = make_idesc_bf16(128, NQ, true, true);
+      const uint32_t q_base = sbase + C::OFF_Q;
+      auto issue_qk = [&](int it) {
+        const int stage = it % NS;
+        mbar_wait(&kv_full[stage], (it / NS) & 1);
+        const int sb = it & 1;
+        mbar_wait(&s_empty[sb], ((it >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem + sb * NQ;
+        const uint32_t kv = sbase + stage * C::STAGE;
+#pragma unroll
+        for (int c = 0; c < C::NCH_QK; ++c) {
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            umma_f16_ss(d, desc_kmajor_sw128(kv + c * C::CHUNK + k * 32),
+                        desc_kmajor_sw128(q_base + c * C::QCHUNK + k * 32), idesc_qk, (c | k) != 0);
+        }
+#pragma unroll
+        for (int k = 0; k < C::RK; ++k)
+          umma_f16_ss(d, desc_kmajor_sw128(kv + C::NCH_V * C::CHUNK + k * 32),
+                      desc_kmajor_sw128(q_base + C::NCH_QK * C::QCHUNK + k * 32), idesc_qk, 1u);
+        umma_commit(&s_full[sb]);
+      };
+      auto issue_pv = [&](int j) {
+        const int pb = j % NP;
+        mbar_wait(&p_full[pb], (j / NP) & 1);
+        tc_fence_after();
+        const int stage = j % NS;
+        const uint32_t kv = sbase + stage * C::STAGE;
+        const uint32_t pt = sbase + C::OFF_P + pb * C::PBYTES;
+#pragma unroll
+        for (int blk = 0; blk < C::NBLK_O; ++blk) {
+#pragma unroll
+          for (int k = 0; k < T / 16; ++k)
+            umma_f16_ss(tmem + C::TMEM_O + blk * NQ, desc_mnmajor_sw128(kv + 2 * blk * C::CHUNK + k * 2048, C::CHUNK),
+                        desc_mnmajor_noswz(pt + k * 256, 128, 2048), idesc_pv, (j > 0 || k > 0) ? 1u : 0u);
+        }
+        umma_commit(&kv_empty[stage]);
+        umma_commit(&p_empty[pb]);
+      };
+      if constexpr (NS >= 2) {
+        for (int it = 0; it < ntiles; ++it) {
+          issue_qk(it);
+          if (it > 0) issue_pv(it - 1);
+        }
+        issue_pv(ntiles - 1);
+      } else {
+        for (int it = 0; it < ntiles; ++it) { issue_qk(it); issue_pv(it); }
+      }
+    }
+  } else if (warp < 4) {
+    // ========================= Q loader (64 threads) =========================
+    const int tid = threadIdx.x - 64;
+    for (int idx = tid; idx < NQ * C::NQCH * 8; idx += 64) {
+      const int n = idx / (C::NQCH * 8);
+      const int u = idx - n * (C::NQCH * 8);
+      const int ch = u >> 3, w = u & 7;
+      uint4 v = make_uint4(0u, 0u, 0u, 0u);
+      if (n < nq) {
+        const bool rope = ch >= C::NCH_QK;
+        const int col = rope ? C::D_KN + w * 8 : ch * 64 + w * 8;
+        if (!rope || w * 8 < C::D_R) {
+          const int ng = n0 + n, t = ng / p.g_q, h = head * p.g_q + (ng - t * p.g_q);
+          const __nv_bfloat16* src = p.q + ((static_cast<size_t>(b) * p.Lq + t) * p.H + h) * C::DQ + col;
+          v = __ldg(reinterpret_cast<const uint4*>(src));
+        }
+      }
+      st_shared_v4(sbase + C::OFF_Q + ch * C::QCHUNK + n * 128 + ((w ^ (n & 7)) << 4), v.x, v.y, v.z, v.w);
+    }
+    fence_proxy_async_smem();
+    mbar_arrive(q_full);
+  } else {
+    // ========================= softmax / correction / epilogue =========================
+    const int wg = (warp - 4) >> 2;
+    const int wq = warp & 3;
+    const int r = wq * 32 + lane;  // TMEM lane: token row of S^T, d row of O^T
+    const int c0 = wg * CW;
+    const uint32_t lane_addr = static_cast<uint32_t>(wq * 32) << 16;
+    const uint32_t bar_id = 1 + wg;
+    int min_vend = 1 << 30;
+    for (int n = 0; n < nq; ++n) min_vend = min(min_vend, vend_s[n]);
+    float m[CW], l[CW];
+#pragma unroll
+    for (int n = 0; n < CW; ++n) { m[n] = -INFINITY; l[n] = 0.f; }
+
+    for (int it = 0; it < ntiles; ++it) {
+      const int sb = it & 1;
+      mbar_wait(&s_full[sb], (it >> 1) & 1);
+      tc_fence_after();
+      float x[CW];
+      tmem_load_cols<C>(tmem + lane_addr + sb * NQ + c0, x);
+      tmem_ld_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&s_empty[sb]);
+
+      const int p0 = (tile_begin + it) * T;
+      const int tok = p0 + r;
+      const bool full = (p0 + T <= min_vend);
+#pragma unroll
+      for (int n = 0; n < CW; ++n) {
+        const bool ok = (c0 + n < nq) && (full || tok < vend_s[c0 + n]);
+        x[n] = ok ? x[n] * p.scale_log2 : -INFINITY;
+      }
+      bool need = false;
+#pragma unroll
+      for (int n = 0; n < CW; ++n) need |= (x[n] > m[n] + TAU);
+      if (named_bar_red_or(bar_id, 128, need)) {
+        float tmp[CW];
+#pragma unroll
+        for (int n = 0; n < CW; ++n) tmp[n] = x[n];
+        const float cm = warp_col_reduce<CW, true>(tmp, lane);
+        if ((lane & ((1 << col_shift<CW>()) - 1)) == 0) red[(wg * 4 + wq) * 32 + (lane >> col_shift<CW>())] = cm;
+        named_bar_sync(bar_id, 128);
+        float alpha[CW];
+        bool any_scale = false;
+#pragma unroll
+        for (int n = 0; n < CW; ++n) {
+          const float* rr = red + wg * 128 + n;
+          const float mt = fmaxf(fmaxf(rr[0], rr[32]), fmaxf(rr[64], rr[96]));
+          const float mn = fmaxf(m[n], mt);
+          alpha[n] = (mn == -INFINITY) ? 1.f : ex2(m[n] - mn);
+          any_scale |= (alpha[n] != 1.f);
+          m[n] = mn;
+          l[n] *= alpha[n];
+        }
+        named_bar_sync(bar_id, 128);
+        if (it > 0 && any_scale) {  // rescale the O^T columns of this WG (rare)
+          const int j = it - 1;
+          mbar_wait(&p_empty[j % NP], (j / NP) & 1);
+          tc_fence_after();
+#pragma unroll
+          for (int blk = 0; blk < C::NBLK_O; ++blk) {
+            float o[CW];
+            const uint32_t ta = tmem + lane_addr + C::TMEM_O + blk * NQ + c0;
+            tmem_load_cols<C>(ta, o);
+            tmem_ld_wait();
+#pragma unroll
+            for (int n = 0; n < CW; ++n) o[n] *= alpha[n];
+            tmem_store_cols<C>(ta, o);
+          }
+          tmem_st_wait();
+        }
+      }
+      // probabilities -> bf16 P^T (MN-major, no swizzle: [NQ/8][128 tok][8])
+      const int pb = it % NP;
+      mbar_wait(&p_empty[pb], ((it / NP) & 1) ^ 1);
+      uint32_t packed[CW / 2];
+#pragma unroll
+      for (int n = 0; n < CW; n += 2) {
+        const float ms0 = (m[n] == -INFINITY) ? 0.f : m[n];
+        const float ms1 = (m[n + 1] == -INFINITY) ? 0.f : m[n + 1];
+        const __nv_bfloat162 v = __floats2bfloat162_rn(ex2(x[n] - ms0), ex2(x[n + 1] - ms1));
+        l[n] += __low2float(v);
+        l[n + 1] += __high2float(v);
+        packed[n / 2] = *reinterpret_cast<const uint32_t*>(&v);
+      }
+      const uint32_t pt = sbase + C::OFF_P + pb * C::PBYTES;
+#pragma unroll
+      for (int g = 0; g < CW / 8; ++g)
+        st_shared_v4(pt + (c0 / 8 + g) * 2048 + r * 16, packed[4 * g], packed[4 * g + 1], packed[4 * g + 2],
+                     packed[4 * g + 3]);
+      if (wg == 0 && tok >= kv_end) {  // never-visible rows: zero V so 0 * garbage cannot give NaN
+        const uint32_t kvrow = sbase + (it % NS) * C::STAGE + r * 128;
+#pragma unroll
+        for (int ch = 0; ch < C::NCH_V; ++ch)
+#pragma unroll
+          for (int u = 0; u < 8; ++u) st_shared_v4(kvrow + ch * C::CHUNK + u * 16, 0u, 0u, 0u, 0u);
+      }
+      fence_proxy_async_smem();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&p_full[pb]);
+    }
+
+    // ------------------------------------------------------------- epilogue
+    float tmp[CW];
+#pragma unroll
+    for (int n = 0; n < CW; ++n) tmp[n] = l[n];
+    const float cs = warp_col_reduce<CW, false>(tmp, lane);
+    if ((lane & ((1 << col_shift<CW>()) - 1)) == 0) red[(wg * 4 + wq) * 32 + (lane >> col_shift<CW>())] = cs;
+    if (threadIdx.x == 128 + wg * 128) {
+#pragma unroll
+      for (int n = 0; n < CW; ++n) m_s[c0 + n] = m[n];
+    }
+    named_bar_sync(bar_id, 128);
+    float inv_l[CW];
+#pragma unroll
+    for (int n = 0; n < CW; ++n) {
+      const float* rr = red + wg * 128 + n;
+      const float ls = (rr[0] + rr[32]) + (rr[64] + rr[96]);
+      inv_l[n] = ls > 0.f ? 1.f / ls : 0.f;
+    }
+    if (r < CW && c0 + r < nq) {
+      const float* rr = red + wg * 128 + r;
+      const float ls = (rr[0] + rr[32]) + (rr[64] + rr[96]);
+      const float lse = ls > 0.f ? (m_s[c0 + r] + __log2f(ls)) * 0.69314718055994531f : -INFINITY;
+      const int ng = n0 + c0 + r, t = ng / p.g_q, h = head * p.g_q + (ng - t * p.g_q);
+      const size_t row = (static_cast<size_t>(b) * p.Lq + t) * p.H + h;
+      if (p.num_splits == 1) p.lse[row] = lse;
+      else p.lse_part[split * n_rows_total + row] = lse;
+    }
+    const int j = ntiles - 1;
+    mbar_wait(&p_empty[j % NP], (j / NP) & 1);
+    tc_fence_after();
+#pragma unroll
+    for (int blk = 0; blk < C::NBLK_O; ++blk) {
+      float o[CW];
+      tmem_load_cols<C>(tmem + lane_addr + C::TMEM_O + blk * NQ + c0, o);
+      tmem_ld_wait();
+      const int d = blk * 128 + r;
+#pragma unroll
+      for (int n = 0; n < CW; ++n) {
+        if (c0 + n < nq) {
+          const int ng = n0 + c0 + n, t = ng / p.g_q, h = head * p.g_q + (ng - t * p.g_q);
+          const size_t row = (static_cast<size_t>(b) * p.Lq + t) * p.H + h;
+          const float val = o[n] * inv_l[n];
+          if (p.num_splits == 1) p.out[row * C::D_V + d] = __float2bfloat16(val);
+          else p.o_part[(split * n_rows_total + row) * C::D_V + d] = val;
+        }
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem, C::TMEM_COLS);
+  }
+}
+
+}  // namespace glad

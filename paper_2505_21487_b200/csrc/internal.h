@@ -1,0 +1,34 @@
+// Internal (C++) interface between the C-ABI layer and the kernel launchers.
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "decode.cuh"
+
+namespace glad {
+
+// Kernel family key: value width, key-from-state width, rope width, query
+// rows per CTA.
+struct DecodeKey {
+  int d_v, d_kn, d_r, nq;
+};
+
+// Returns cudaErrorInvalidValue (and does not launch) if no instantiation
+// matches `key`.
+cudaError_t launch_decode(const DecodeKey& key, const CUtensorMap& tmap, const DecodeParams& p, dim3 grid,
+                          cudaStream_t stream);
+bool decode_supported(const DecodeKey& key);
+int decode_max_nq(int d_v);
+
+cudaError_t launch_append(void* pool, int64_t row_stride, int page_size, const int32_t* block_table,
+                          int32_t bt_stride, const int32_t* seqlens_before, const void* rows, int32_t B,
+                          int32_t n_new, int32_t width, cudaStream_t stream);
+cudaError_t launch_gather(const void* pool, int64_t row_stride, int page_size, const int32_t* block_table,
+                          int32_t bt_stride, const int32_t* seqlens, int32_t B, int32_t max_len, int32_t width,
+                          void* dense_out, cudaStream_t stream);
+cudaError_t launch_combine(const float* o_part, const float* lse_part, int32_t S, int64_t rows, int32_t d_v,
+                           void* out, float* lse, cudaStream_t stream);
+
+}  // namespace glad

@@ -1,0 +1,242 @@
+"""ctypes binding of libglad (include/glad.h).  Argument marshalling only:
+every step of the decode path runs in the library's sm_100a kernels.  Torch is
+used for device memory and streams.  There is no fallback: if libglad.so is
+missing or fails to load, every call raises.
+"""
+
+import ctypes
+import math
+import os
+
+import torch
+
+_LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libglad.so")
+_lib = None
+
+GLAD_OK, GLAD_ERR_INVALID_ARG, GLAD_ERR_UNSUPPORTED, GLAD_ERR_WORKSPACE, GLAD_ERR_CUDA = range(5)
+MHA, MQA, GQA, GTA, GLA, MLA = range(6)
+
+
+class GladError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"glad status {status}: {msg}")
+        self.status = status
+
+
+class CacheLayout(ctypes.Structure):
+    """glad_cache_layout (include/glad.h)."""
+    _fields_ = [("num_pages", ctypes.c_int32), ("page_size", ctypes.c_int32),
+                ("n_heads_kv", ctypes.c_int32), ("d_head", ctypes.c_int32),
+                ("d_rope", ctypes.c_int32), ("_reserved", ctypes.c_int32),
+                ("row_stride", ctypes.c_int64)]
+
+    @property
+    def width(self):
+        return self.n_heads_kv * self.d_head + self.d_rope
+
+    def __repr__(self):
+        return (f"CacheLayout(num_pages={self.num_pages}, page_size={self.page_size}, "
+                f"n_heads_kv={self.n_heads_kv}, d_head={self.d_head}, d_rope={self.d_rope}, "
+                f"row_stride={self.row_stride})")
+
+
+def make_layout(num_pages, page_size, n_heads_kv, d_head, d_rope, row_stride=None):
+    w = n_heads_kv * d_head + d_rope
+    rs = row_stride if row_stride is not None else -(-w // 8) * 8
+    return CacheLayout(int(num_pages), int(page_size), int(n_heads_kv), int(d_head), int(d_rope), 0, int(rs))
+
+
+_I32P = ctypes.POINTER(ctypes.c_int32)
+_VP = ctypes.c_void_p
+
+
+def _sig(lib):
+    L = ctypes.POINTER(CacheLayout)
+    S = ctypes.c_int
+    dec = [_VP, _VP, L, _VP, ctypes.c_int32, _VP, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
+           ctypes.c_float, ctypes.c_int32, _VP, _VP, _VP, ctypes.c_size_t, ctypes.c_int32, _VP]
+    table = {
+        "glad_last_error": ([], ctypes.c_char_p),
+        "glad_version": ([], ctypes.c_char_p),
+        "glad_pool_bytes": ([L], ctypes.c_size_t),
+        "glad_cache_append": ([L, _VP, _VP, ctypes.c_int32, _VP, _VP, ctypes.c_int32, ctypes.c_int32, _VP], S),
+        "glad_paged_gather": ([L, _VP, _VP, ctypes.c_int32, _VP, ctypes.c_int32, ctypes.c_int32, _VP, _VP], S),
+        "glad_decode_workspace_bytes": ([ctypes.c_int32] * 5, ctypes.c_size_t),
+        "glad_decode_num_splits": ([L, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
+                                    ctypes.c_int32], ctypes.c_int32),
+        "glad_gla_decode": (dec, S),
+        "glad_mla_decode": (dec, S),
+        "glad_gta_decode": (dec, S),
+        "glad_splitkv_combine": ([_VP, _VP] + [ctypes.c_int32] * 5 + [_VP, _VP, _VP], S),
+        "glad_tp_duplication": ([ctypes.c_int32] * 3, ctypes.c_int32),
+        "glad_tp_shard": ([ctypes.c_int32] * 4 + [_I32P] * 4, S),
+        "glad_kv_bytes_per_token_per_device": ([ctypes.c_int32] * 6, ctypes.c_int64),
+    }
+    for name, (args, res) in table.items():
+        f = getattr(lib, name)
+        f.argtypes = args
+        f.restype = res
+    return lib
+
+
+def lib():
+    """Load libglad.so (raises if it is missing — there is no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(_LIB_PATH):
+            raise RuntimeError(f"libglad.so not built ({_LIB_PATH}); run __graft_entry__.build() "
+                               "or `python -m paper_2505_21487_b200.build`")
+        _lib = _sig(ctypes.CDLL(_LIB_PATH))
+    return _lib
+
+
+def exported_symbols():
+    return ["glad_last_error", "glad_version", "glad_pool_bytes", "glad_cache_append", "glad_paged_gather",
+            "glad_decode_workspace_bytes", "glad_decode_num_splits", "glad_gla_decode", "glad_mla_decode",
+            "glad_gta_decode", "glad_splitkv_combine", "glad_tp_duplication", "glad_tp_shard",
+            "glad_kv_bytes_per_token_per_device"]
+
+
+def _check(status):
+    if status != GLAD_OK:
+        raise GladError(status, lib().glad_last_error().decode())
+
+
+def _ptr(t):
+    return ctypes.c_void_p(t.data_ptr()) if t is not None else ctypes.c_void_p(0)
+
+
+def _stream(stream):
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+def _need(t, dtype, name, device=True):
+    if t.dtype != dtype:
+        raise TypeError(f"{name}: expected {dtype}, got {t.dtype}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    if device and not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor")
+
+
+# ------------------------------------------------------------------ calls
+def pool_bytes(layout):
+    return lib().glad_pool_bytes(ctypes.byref(layout))
+
+
+def cache_append(layout, pool, block_table, seqlens_before, rows, stream=None):
+    """rows [B, n_new, width] bf16 -> pool (in place)."""
+    _need(pool, torch.bfloat16, "pool"); _need(rows, torch.bfloat16, "rows")
+    _need(block_table, torch.int32, "block_table"); _need(seqlens_before, torch.int32, "seqlens_before")
+    B, n_new, w = rows.shape
+    if w != layout.width:
+        raise ValueError(f"rows width {w} != layout width {layout.width}")
+    _check(lib().glad_cache_append(ctypes.byref(layout), _ptr(pool), _ptr(block_table), block_table.shape[1],
+                                   _ptr(seqlens_before), _ptr(rows), B, n_new, _stream(stream)))
+
+
+def paged_gather(layout, pool, block_table, seqlens, max_len, out=None, stream=None):
+    _need(pool, torch.bfloat16, "pool"); _need(block_table, torch.int32, "block_table")
+    _need(seqlens, torch.int32, "seqlens")
+    B = seqlens.shape[0]
+    if out is None:
+        out = torch.empty(B, max_len, layout.width, dtype=torch.bfloat16, device=pool.device)
+    _check(lib().glad_paged_gather(ctypes.byref(layout), _ptr(pool), _ptr(block_table), block_table.shape[1],
+                                   _ptr(seqlens), B, max_len, _ptr(out), _stream(stream)))
+    return out
+
+
+def workspace_bytes(B, Lq, H, d_v, splits):
+    return lib().glad_decode_workspace_bytes(B, Lq, H, d_v, splits)
+
+
+def num_splits(layout, B, Lq, H, bt_stride, variant=GLA):
+    return lib().glad_decode_num_splits(ctypes.byref(layout), B, Lq, H, bt_stride, variant)
+
+
+class Workspace:
+    """Reusable split-KV workspace (grows on demand; keeps CUDA-graph capture
+    safe as long as it is sized before capture)."""
+
+    def __init__(self, device="cuda"):
+        self.buf = None
+        self.device = device
+
+    def get(self, nbytes):
+        if nbytes == 0:
+            return None
+        if self.buf is None or self.buf.numel() < nbytes:
+            self.buf = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+        return self.buf
+
+
+_default_ws = {}
+
+
+def _decode(fn, variant, q, pool, layout, block_table, seqlens, softmax_scale, causal=True, out=None,
+            lse=None, splits=0, workspace=None, stream=None):
+    _need(q, torch.bfloat16, "q"); _need(pool, torch.bfloat16, "pool")
+    _need(block_table, torch.int32, "block_table"); _need(seqlens, torch.int32, "seqlens")
+    B, Lq, H, _ = q.shape
+    d_v = layout.d_head
+    if out is None:
+        out = torch.empty(B, Lq, H, d_v, dtype=torch.bfloat16, device=q.device)
+    if lse is None:
+        lse = torch.empty(B, Lq, H, dtype=torch.float32, device=q.device)
+    bt_stride = block_table.shape[1]
+    S = splits if splits > 0 else num_splits(layout, B, Lq, H, bt_stride, variant)
+    if S < 0:
+        S = 1
+    nbytes = workspace_bytes(B, Lq, H, d_v, S)
+    if workspace is None:
+        workspace = _default_ws.setdefault(q.device, Workspace(q.device))
+    ws = workspace.get(nbytes)
+    _check(fn(_ptr(q), _ptr(pool), ctypes.byref(layout), _ptr(block_table), bt_stride, _ptr(seqlens), B, Lq, H,
+              float(softmax_scale), 1 if causal else 0, _ptr(out), _ptr(lse), _ptr(ws), nbytes, S,
+              _stream(stream)))
+    return out, lse
+
+
+def gla_decode(q, pool, layout, block_table, seqlens, softmax_scale, causal=True, **kw):
+    """GLA decode (glad_gla_decode).  q [B, Lq, H, d_c + d_R] bf16."""
+    return _decode(lib().glad_gla_decode, GLA, q, pool, layout, block_table, seqlens, softmax_scale, causal, **kw)
+
+
+def mla_decode(q, pool, layout, block_table, seqlens, softmax_scale, causal=True, **kw):
+    return _decode(lib().glad_mla_decode, MLA, q, pool, layout, block_table, seqlens, softmax_scale, causal, **kw)
+
+
+def gta_decode(q, pool, layout, block_table, seqlens, softmax_scale, causal=True, **kw):
+    return _decode(lib().glad_gta_decode, GTA, q, pool, layout, block_table, seqlens, softmax_scale, causal, **kw)
+
+
+def splitkv_combine(o_part, lse_part, out=None, lse=None, stream=None):
+    _need(o_part, torch.float32, "o_part"); _need(lse_part, torch.float32, "lse_part")
+    S, B, Lq, H, d_v = o_part.shape
+    if out is None:
+        out = torch.empty(B, Lq, H, d_v, dtype=torch.bfloat16, device=o_part.device)
+    if lse is None:
+        lse = torch.empty(B, Lq, H, dtype=torch.float32, device=o_part.device)
+    _check(lib().glad_splitkv_combine(_ptr(o_part), _ptr(lse_part), S, B, Lq, H, d_v, _ptr(out), _ptr(lse),
+                                      _stream(stream)))
+    return out, lse
+
+
+def tp_duplication(N, g_q, h_q):
+    return lib().glad_tp_duplication(N, g_q, h_q)
+
+
+def tp_shard(h_q, n_kv_heads, N, rank):
+    vals = [ctypes.c_int32() for _ in range(4)]
+    _check(lib().glad_tp_shard(h_q, n_kv_heads, N, rank, *[ctypes.byref(v) for v in vals]))
+    return tuple(v.value for v in vals)
+
+
+def kv_bytes_per_token_per_device(variant, n_kv_heads, d_head, d_rope, N, dtype_bytes=2):
+    return lib().glad_kv_bytes_per_token_per_device(variant, n_kv_heads, d_head, d_rope, N, dtype_bytes)
+
+
+def version():
+    return lib().glad_version().decode()

@@ -1,0 +1,263 @@
+"""GPU parity: the sm_100a kernels (through the C ABI) vs the fp64 oracle on
+the same seeded inputs.  Tolerances (BASELINE north_star): output max-abs
+<= 1e-2 and rel-L2 <= 5e-3, LSE max-abs <= 1e-2; paging bit-exact."""
+
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import synth
+from oracle import attention as OA
+from oracle import paging as OP
+from paper_2505_21487_b200 import glad
+
+from gpu_side import DEV, absorb_inputs, build_paged, check, latent_rows, rope_torch
+
+pytestmark = pytest.mark.gpu
+
+
+def f64(t):
+    return t.to(torch.float64).cpu().numpy()
+
+
+# ------------------------------------------------------------------ paging
+@pytest.mark.parametrize("page_size", [1, 2, 4, 16, 64, 128, 256])
+def test_append_gather_bitexact(page_size):
+    B, Lmax, W = 3, 300, 288
+    rows = synth.normal_bf16((B, Lmax, W), seed=page_size)
+    sl = np.array([300, 1, 171], dtype=np.int32)
+    layout, pool, bt = build_paged(rows, sl, page_size, 2, 128, 32, seed=page_size, row_stride=296)
+    dense = glad.paged_gather(layout, pool, bt, torch.from_numpy(sl).to(DEV), Lmax)
+    torch.cuda.synchronize()
+    d = dense.cpu()
+    for b in range(B):
+        assert torch.equal(d[b, : sl[b]].view(torch.int16), rows[b, : sl[b]].view(torch.int16))
+        assert torch.all(d[b, sl[b]:].float() == 0)
+    # the oracle's naive 64-bit address formula names the same physical rows
+    pool_c = pool.cpu().reshape(-1, layout.row_stride)
+    bt_c = bt.cpu().numpy()
+    for b in range(B):
+        for j in range(0, int(sl[b]), 7):
+            r = OP.physical_row(bt_c, page_size, b, j)
+            assert torch.equal(pool_c[r, :W].view(torch.int16), rows[b, j].view(torch.int16))
+
+
+def test_append_in_chunks_matches_single():
+    """Appending a sequence as several decode steps (seqlens_before offsets)
+    writes the same bytes as one bulk append (append-only)."""
+    B, L, W, page = 2, 96, 320, 16
+    rows = synth.normal_bf16((B, L, W), seed=5)
+    sl = np.array([L, L], dtype=np.int32)
+    layout, pool1, bt = build_paged(rows, sl, page, 1, 256, 64, seed=1)
+    pool2 = torch.full_like(pool1, float("nan"))
+    done = 0
+    for n_new in (1, 2, 13, 80):
+        before = torch.full((B,), done, dtype=torch.int32, device=DEV)
+        glad.cache_append(layout, pool2, bt, before, rows[:, done:done + n_new].contiguous().to(DEV))
+        done += n_new
+    torch.cuda.synchronize()
+    a = pool1.cpu().view(torch.int16)
+    b = pool2.cpu().view(torch.int16)
+    mask = ~torch.isnan(pool1.cpu().float())
+    assert torch.equal(a[mask], b[mask])
+
+
+# ------------------------------------------------------------ GLA / MLA
+def run_latent(B, Lq, H, h_c, d_c, d_R, seqlens, page, splits=0, causal=True, scale=None, seed=0,
+               q_scale=1.0):
+    Lmax = int(max(seqlens.max(), 1))
+    q, c, kr = synth.latent_kernel_inputs(B, Lq, H, h_c, d_c, d_R, Lmax, seed=seed, q_scale=q_scale)
+    layout, pool, bt = build_paged(latent_rows(c, kr), seqlens, page, h_c, d_c, d_R, seed=seed)
+    scale = scale if scale is not None else 1.0 / math.sqrt(d_c // 2 + d_R)
+    sl_d = torch.from_numpy(seqlens.astype(np.int32)).to(DEV)
+    fn = glad.mla_decode if h_c == 1 and d_c == 512 else glad.gla_decode
+    out, lse = fn(q.to(DEV), pool, layout, bt, sl_d, scale, causal=causal, splits=splits)
+    torch.cuda.synchronize()
+    o_ref, lse_ref = OA.latent_decode(f64(q), f64(c), f64(kr), seqlens, scale, causal=causal)
+    return out, lse, o_ref, lse_ref
+
+
+def test_c1_gla2_oracle_scale():
+    """BASELINE configs[0]: GLA-2, B=2, ctx 256, Lq=1, 16 q heads, 2 latent
+    heads d_c=128 + d_R=32, page 16."""
+    sl = np.array([256, 256])
+    for seed in range(3):
+        out, lse, o_ref, lse_ref = run_latent(2, 1, 16, 2, 128, 32, sl, 16, seed=seed)
+        check(out, lse, o_ref, lse_ref, what=f"C1 seed {seed}")
+
+
+def test_c1_against_unabsorbed_definition():
+    """End to end against the UNabsorbed fp64 definition: GPU side absorbs
+    W_UK into the query and rotates the RoPE parts (torch), the kernel
+    attends to the latent; the oracle up-projects per head."""
+    B, Lq, H, h_c, d_c, d_R, d_h = 2, 2, 16, 2, 128, 32, 64
+    sl = np.array([256, 201])
+    x = synth.gla_method_inputs(B, Lq, H, h_c, d_c, d_R, d_h, 256, seed=4)
+    q, c, kr = absorb_inputs(x, sl, Lq)
+    layout, pool, bt = build_paged(latent_rows(c, kr), sl, 16, h_c, d_c, d_R, seed=4)
+    scale = 1.0 / math.sqrt(d_h + d_R)
+    out, lse = glad.gla_decode(q.to(DEV), pool, layout, bt, torch.from_numpy(sl.astype(np.int32)).to(DEV), scale)
+    torch.cuda.synchronize()
+    _, o_lat, lse_u = OA.gla_unabsorbed(f64(x["q_nope"]), f64(x["q_pe"]), f64(x["c"]), f64(x["k_pe"]),
+                                        f64(x["W_UK"]), f64(x["W_UV"]), sl, scale)
+    check(out, lse, o_lat, lse_u, what="unabsorbed")
+
+
+GLA_SWEEP = [
+    # B, Lq, H, h_c, d_c, d_R, lens, page, splits, causal
+    (2, 1, 128, 2, 256, 64, [1024, 777], 64, 0, True),
+    (2, 2, 128, 2, 256, 64, [1024, 777], 64, 0, True),
+    (2, 1, 128, 2, 256, 64, [1024, 777], 1, 3, True),
+    (3, 4, 16, 2, 128, 32, [300, 129, 5], 16, 2, True),
+    (3, 3, 16, 2, 128, 32, [300, 129, 5], 16, 1, False),
+    (2, 1, 32, 8, 256, 64, [700, 64], 64, 1, True),        # GLA-8, g_q = 4 -> 16-row tiles
+    (1, 2, 64, 4, 256, 64, [2000], 16, 5, True),
+    (4, 1, 32, 2, 128, 64, [128, 127, 129, 1], 2, 0, True),
+    (2, 1, 16, 2, 256, 32, [555, 999], 128, 2, True),
+]
+
+
+@pytest.mark.parametrize("cfg", GLA_SWEEP, ids=lambda c: "B{}Lq{}H{}hc{}dc{}dr{}p{}s{}c{}".format(
+    c[0], c[1], c[2], c[3], c[4], c[5], c[7], c[8], int(c[9])))
+def test_gla_sweep(cfg):
+    B, Lq, H, h_c, d_c, d_R, lens, page, splits, causal = cfg
+    out, lse, o_ref, lse_ref = run_latent(B, Lq, H, h_c, d_c, d_R, np.array(lens), page, splits=splits,
+                                          causal=causal, seed=GLA_SWEEP.index(cfg))
+    check(out, lse, o_ref, lse_ref, what=str(cfg))
+
+
+def test_peaked_and_large_scores():
+    """Peaked regime (q x 4) exercises the lazy-rescale path many times."""
+    out, lse, o_ref, lse_ref = run_latent(2, 2, 32, 2, 256, 64, np.array([900, 650]), 64, splits=1,
+                                          seed=17, q_scale=4.0)
+    check(out, lse, o_ref, lse_ref, what="peaked")
+
+
+@pytest.mark.parametrize("Lq,H", [(1, 16), (2, 16), (1, 128)])
+def test_mla_baseline(Lq, H):
+    out, lse, o_ref, lse_ref = run_latent(2, Lq, H, 1, 512, 64, np.array([700, 300]), 64, seed=Lq + H)
+    check(out, lse, o_ref, lse_ref, what=f"MLA Lq={Lq} H={H}")
+
+
+def test_empty_and_tiny_sequences():
+    out, lse, o_ref, lse_ref = run_latent(4, 2, 16, 2, 128, 32, np.array([0, 1, 2, 3]), 16, splits=1)
+    check(out, lse, o_ref, lse_ref, what="tiny")
+    assert torch.all(out[0].float() == 0) and torch.all(torch.isneginf(lse[0]))
+    # causal Lq=2 with L=1: first query sees nothing
+    assert torch.all(torch.isneginf(lse[1, 0]))
+
+
+def test_page_size_and_permutation_invariance_bitexact():
+    """Tiling is in logical token space, so page size and page placement do
+    not change a single bit of the output for a fixed split plan."""
+    B, Lq, H, h_c, d_c, d_R = 2, 2, 32, 2, 256, 64
+    sl = np.array([1000, 613])
+    q, c, kr = synth.latent_kernel_inputs(B, Lq, H, h_c, d_c, d_R, 1000, seed=21)
+    rows = latent_rows(c, kr)
+    sl_d = torch.from_numpy(sl.astype(np.int32)).to(DEV)
+    outs = []
+    for page, seed in [(64, 0), (64, 1), (1, 2), (16, 3), (256, 4)]:
+        layout, pool, bt = build_paged(rows, sl, page, h_c, d_c, d_R, seed=seed)
+        o, l = glad.gla_decode(q.to(DEV), pool, layout, bt, sl_d, 0.07, splits=2)
+        outs.append((o.cpu().view(torch.int16), l.cpu()))
+    for o, l in outs[1:]:
+        assert torch.equal(o, outs[0][0]) and torch.equal(l, outs[0][1])
+
+
+def test_split_count_changes_only_rounding():
+    B, Lq, H = 2, 1, 128
+    sl = np.array([3000, 2500])
+    ref = None
+    for s in (1, 2, 4, 7):
+        out, lse, o_ref, lse_ref = run_latent(B, Lq, H, 2, 256, 64, sl, 64, splits=s, seed=33)
+        check(out, lse, o_ref, lse_ref, what=f"splits={s}")
+
+
+# ------------------------------------------------------------------- GTA
+def run_gta(B, Lq, H, h_kv, seqlens, page, splits=0, causal=True, seed=0):
+    d_h = 128
+    Lmax = int(max(seqlens.max(), 1))
+    q, kv, kr = synth.gta_kernel_inputs(B, Lq, H, h_kv, d_h, Lmax, seed=seed)
+    rows = torch.cat([kv.reshape(B, Lmax, -1), kr], -1).contiguous()
+    layout, pool, bt = build_paged(rows, seqlens, page, h_kv, d_h, d_h // 2, seed=seed)
+    scale = 1.0 / math.sqrt(d_h)
+    out, lse = glad.gta_decode(q.to(DEV), pool, layout, bt, torch.from_numpy(seqlens.astype(np.int32)).to(DEV),
+                               scale, causal=causal, splits=splits)
+    torch.cuda.synchronize()
+    o_ref, lse_ref = OA.tied_decode(f64(q), f64(kv), f64(kr), seqlens, scale, causal=causal)
+    return out, lse, o_ref, lse_ref
+
+
+@pytest.mark.parametrize("cfg", [(2, 1, 64, 8, [700, 333], 64, 0), (2, 2, 64, 8, [700, 333], 16, 2),
+                                 (3, 1, 32, 2, [129, 1, 400], 1, 1), (1, 4, 64, 4, [1500], 64, 3)])
+def test_gta(cfg):
+    B, Lq, H, h_kv, lens, page, splits = cfg
+    out, lse, o_ref, lse_ref = run_gta(B, Lq, H, h_kv, np.array(lens), page, splits=splits, seed=7)
+    check(out, lse, o_ref, lse_ref, what=f"GTA {cfg}")
+
+
+def test_gta_end_to_end_unrotated():
+    """GPU side rotates q's RoPE half and K_RoPE (torch); oracle gta_decode
+    rotates on its own from the unrotated tensors (tied half never
+    rotated)."""
+    B, Lq, H, h_kv, d_h = 2, 2, 16, 4, 128
+    sl = np.array([300, 111])
+    q, kv, kr = synth.gta_kernel_inputs(B, Lq, H, h_kv, d_h, 300, seed=9)
+    pos_q = torch.tensor([[int(sl[b]) - Lq + t for t in range(Lq)] for b in range(B)])[..., None]
+    q_rot = torch.cat([q[..., :64].double(), rope_torch(q[..., 64:], pos_q)], -1).to(torch.bfloat16)
+    kr_rot = rope_torch(kr, torch.arange(300)[None].expand(B, 300)).to(torch.bfloat16)
+    rows = torch.cat([kv.reshape(B, 300, -1), kr_rot], -1).contiguous()
+    layout, pool, bt = build_paged(rows, sl, 64, h_kv, d_h, 64, seed=9)
+    out, lse = glad.gta_decode(q_rot.to(DEV), pool, layout, bt, torch.from_numpy(sl.astype(np.int32)).to(DEV),
+                               1 / math.sqrt(d_h))
+    o_ref, lse_ref = OA.gta_decode(f64(q), f64(kv), f64(kr), sl, 1 / math.sqrt(d_h))
+    check(out, lse, o_ref, lse_ref, what="GTA e2e")
+
+
+# --------------------------------------------------------------- combine
+def test_splitkv_combine_vs_oracle():
+    S, B, Lq, H, d_v = 5, 3, 2, 4, 256
+    g = torch.Generator().manual_seed(3)
+    o_part = torch.randn(S, B, Lq, H, d_v, generator=g)
+    lse_part = torch.randn(S, B, Lq, H, generator=g) * 3
+    lse_part[2] = -float("inf")            # an empty split
+    lse_part[:, 1, 0, 0] = -float("inf")   # a row with no keys at all
+    o_part[2] = float("nan")               # never read
+    out, lse = glad.splitkv_combine(o_part.to(DEV), lse_part.to(DEV))
+    torch.cuda.synchronize()
+    o_ref, lse_ref = OA.merge_partials(np.where(np.isnan(f64(o_part)), 0, f64(o_part)), f64(lse_part))
+    check(out, lse, o_ref, lse_ref, what="combine")
+
+
+# ------------------------------------------------------ full bench sizes
+@pytest.mark.slow
+def test_c2_full_size_sampled():
+    """BASELINE configs[1] at full size (B=128, ctx 8K, h_q=128, GLA-2
+    2x256 + 64, page 64) in bench.py's launch configuration; sampled
+    (b, latent head) units recomputed one by one by the oracle."""
+    from paper_2505_21487_b200 import workloads
+    wl = workloads.get("c2_gla2")
+    st = workloads.build_device_state(wl, seed=1)
+    out, lse = workloads.run(wl, st)
+    torch.cuda.synchronize()
+    _sampled_latent_check(wl, st, out, lse, samples=[(0, 0), (37, 1), (127, 0), (127, 1)])
+
+
+def _sampled_latent_check(wl, st, out, lse, samples):
+    layout, pool, bt, sl, q = st["layout"], st["pool"], st["block_table"], st["seqlens"], st["q"]
+    g_q = wl.H // wl.h_c
+    for b, i in samples:
+        L = int(sl[b].item())
+        pos = torch.arange(L, device=DEV)
+        prow = bt[b, pos // layout.page_size].long() * layout.page_size + pos % layout.page_size
+        rows = pool.reshape(-1, layout.row_stride)[prow]
+        c_i = rows[:, i * wl.d_c:(i + 1) * wl.d_c].cpu()
+        kr = rows[:, wl.h_c * wl.d_c: wl.h_c * wl.d_c + wl.d_R].cpu()
+        qr = q[b, :, i * g_q:(i + 1) * g_q].reshape(-1, q.shape[-1]).cpu()
+        nvis = [OA.visible_count(L, wl.Lq, t, True) for t in range(wl.Lq) for _ in range(g_q)]
+        o_ref, lse_ref = OA.latent_decode_unit(qr, c_i, kr, nvis, wl.scale)
+        o_g = out[b, :, i * g_q:(i + 1) * g_q].reshape(-1, wl.d_c)
+        l_g = lse[b, :, i * g_q:(i + 1) * g_q].reshape(-1)
+        check(o_g, l_g, o_ref, lse_ref, what=f"sample b={b} head={i}")
