@@ -178,7 +178,7 @@ def run_ours(args, rank, world, local_rank):
         base = name.replace("_tp1", "").replace("_tp2", "").replace("_tp4", "").replace("_tp8", "")
         name = base.replace("c5_gla8", f"c5_gla8_tp{world}")
     wl = workloads.get(name)
-    st = workloads.build_device_state(wl, seed=wl.seed + (0 if tp else rank), device=dev)
+    st = workloads.build_device_state(wl, seed=wl.seed + (0 if tp else rank), device=dev, splits=args.splits)
     sl = st["seqlens_host"]
     stream = torch.cuda.current_stream(dev)
 
@@ -351,6 +351,7 @@ def main():
     ap.add_argument("--workload", default="c2_gla2")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--splits", type=int, default=0, help="force the KV split count (0 = library heuristic)")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))

@@ -175,6 +175,14 @@ GLAD_API glad_status glad_gta_decode(const void* q, const void* pool, const glad
 GLAD_API glad_status glad_splitkv_combine(const float* o_part, const float* lse_part, int32_t S, int32_t B, int32_t Lq,
                                  int32_t H, int32_t d_v, void* out, float* lse, void* stream);
 
+/*
+ * Debug only: when device_buf != NULL every subsequent decode launch writes a
+ * per-CTA timeline (globaltimer ns; layout in csrc/decode.cuh, kTraceStride
+ * uint64 per CTA, CTAs in launch order) into it.  The caller sizes it for
+ * the grid.  NULL turns tracing off (the default).  Not thread-safe.
+ */
+GLAD_API void glad_debug_set_trace(void* device_buf);
+
 /* ---- tp_shard helpers: host-only, pure (no CUDA) ---- */
 
 /* D = ceil(N * g_q / h_q).  Returns -1 on invalid input. */

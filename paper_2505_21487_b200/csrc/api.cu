@@ -14,6 +14,7 @@
 namespace {
 
 thread_local char g_err[512] = "no error";
+uint64_t* g_trace = nullptr;  // debug timeline buffer (glad_debug_set_trace)
 
 glad_status fail(glad_status s, const char* fmt, ...) {
   va_list ap;
@@ -198,6 +199,7 @@ glad_status decode_common(Variant v, const void* q, const void* pool, const glad
   p.n_qblk = g.n_qblk;
   p.causal = causal ? 1 : 0;
   p.scale_log2 = scale * 1.4426950408889634f;
+  p.trace = g_trace;
   dim3 grid(static_cast<unsigned>(S), static_cast<unsigned>(L->n_heads_kv * g.n_qblk), static_cast<unsigned>(B));
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   cudaError_t e = glad::launch_decode(g.key, tmap, p, grid, st);
@@ -216,6 +218,8 @@ extern "C" {
 const char* glad_last_error(void) { return g_err; }
 
 const char* glad_version(void) { return "glad 0.1.0 sm_100a"; }
+
+void glad_debug_set_trace(void* device_buf) { g_trace = static_cast<uint64_t*>(device_buf); }
 
 size_t glad_pool_bytes(const glad_cache_layout* L) {
   if (check_layout(L) != GLAD_OK) return 0;

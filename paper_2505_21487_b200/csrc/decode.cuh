@@ -52,7 +52,13 @@ struct DecodeParams {
   int32_t num_splits, n_qblk;
   int32_t causal;
   float scale_log2;         // softmax_scale * log2(e)
+  uint64_t* trace;          // debug timeline (nullptr = off): [cta][kTraceStride]
 };
+// Debug timeline layout per CTA (globaltimer ns): [0] start, [1] Q ready (MMA),
+// [2] end, then per tile i < kTraceTiles: [8+5i] load issued, [9+5i] QK issued,
+// [10+5i] S seen by softmax, [11+5i] P written, [12+5i] PV issued.
+constexpr int kTraceTiles = 64;
+constexpr int kTraceStride = 8 + 5 * kTraceTiles;
 
 template <int D_V_, int D_KN_, int D_R_, int NQ_>
 struct DecodeCfg {
@@ -71,18 +77,19 @@ struct DecodeCfg {
   static constexpr int STAGE = NCH * CHUNK;
   static constexpr int QCHUNK = NQ * 128;
   static constexpr int QBYTES = NQCH * QCHUNK;
+  // P^T (bf16, [NQ/8][128 tok][8]) lives in the stage's RoPE chunk, which is
+  // dead once QK of that tile has completed: P is thereby multi-buffered with
+  // the KV stages at zero extra shared memory.
   static constexpr int PBYTES = T * NQ * 2;
   static constexpr int NBLK_O = D_V / 128;
   static constexpr int NWG = 2;
   static constexpr int CW = NQ / NWG;
-  static constexpr int AUX = 2048;
+  static constexpr int AUX = 3072;
   static constexpr int AVAIL = 227 * 1024 - 1024 - AUX;
-  static constexpr int NP = (AVAIL - QBYTES - 2 * STAGE - 2 * PBYTES >= 0) ? 2 : 1;
-  static constexpr int NS_RAW = (AVAIL - QBYTES - NP * PBYTES) / STAGE;
+  static constexpr int NS_RAW = (AVAIL - QBYTES) / STAGE;
   static constexpr int NS = NS_RAW > 4 ? 4 : NS_RAW;
   static constexpr int OFF_Q = NS * STAGE;
-  static constexpr int OFF_P = OFF_Q + QBYTES;
-  static constexpr int OFF_AUX = OFF_P + NP * PBYTES;
+  static constexpr int OFF_AUX = OFF_Q + QBYTES;
   static constexpr int SMEM_BYTES = 1024 + OFF_AUX + AUX;
   static constexpr int TMEM_O = 2 * NQ;
   static constexpr int TMEM_USED = 2 * NQ + NBLK_O * NQ;
@@ -90,6 +97,7 @@ struct DecodeCfg {
       TMEM_USED <= 32 ? 32 : TMEM_USED <= 64 ? 64 : TMEM_USED <= 128 ? 128 : TMEM_USED <= 256 ? 256 : 512;
   static constexpr int NTHREADS = 384;
   static_assert(NS >= 1, "a KV stage does not fit in shared memory");
+  static_assert(PBYTES <= CHUNK, "P^T must fit in the RoPE chunk");
   static_assert(D_V % 128 == 0 && D_KN % 64 == 0 && D_KN <= D_V, "unsupported head dims");
   static_assert(D_R % 16 == 0 && D_R >= 16 && D_R <= 64, "unsupported rope dim");
   static_assert(NQ == 16 || NQ == 32 || NQ == 64, "NQ must be 16/32/64");
@@ -151,24 +159,26 @@ __device__ __forceinline__ void tmem_store_cols(uint32_t taddr, const float (&x)
 template <class C>
 __global__ void __launch_bounds__(C::NTHREADS, 1)
     decode_kernel(const __grid_constant__ CUtensorMap tmap, const DecodeParams p) {
-  constexpr int T = C::T, NQ = C::NQ, CW = C::CW, NS = C::NS, NP = C::NP;
+  constexpr int T = C::T, NQ = C::NQ, CW = C::CW, NS = C::NS;
   constexpr float TAU = 8.0f;  // lazy-rescale threshold (log2 units)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const uint32_t sbase = smem_u32(smem);
   uint8_t* aux = smem + C::OFF_AUX;
   uint64_t* bars = reinterpret_cast<uint64_t*>(aux);
-  uint64_t* kv_full = bars;       // [4]
-  uint64_t* kv_empty = bars + 4;  // [4]
-  uint64_t* s_full = bars + 8;    // [2]
-  uint64_t* s_empty = bars + 10;  // [2]
-  uint64_t* p_full = bars + 12;   // [2]
-  uint64_t* p_empty = bars + 14;  // [2]
-  uint64_t* q_full = bars + 16;
+  uint64_t* kv_full = bars;        // [4] TMA -> MMA      (tx bytes)
+  uint64_t* kv_empty = bars + 4;   // [4] PV done -> TMA  (stage incl. its P^T slot is free)
+  uint64_t* s_full = bars + 8;     // [2] QK done -> softmax
+  uint64_t* s_empty = bars + 10;   // [2] softmax read S -> MMA
+  uint64_t* p_full = bars + 12;    // [4] P^T written (per stage) -> MMA
+  uint64_t* pv_done = bars + 16;   // [4] PV(j) complete, j % 4 (O rescale / epilogue)
+  uint64_t* q_full = bars + 20;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(aux + 256);
-  int* vend_s = reinterpret_cast<int*>(aux + 320);       // [NQ] visible-key end per query column
-  float* m_s = reinterpret_cast<float*>(aux + 640);      // [NQ] final running max
-  float* red = reinterpret_cast<float*>(aux + 1024);     // [2 wg][4 warps][32]
+  int* vend_s = reinterpret_cast<int*>(aux + 320);         // [NQ] visible-key end per query column
+  float* m_run = reinterpret_cast<float*>(aux + 640);      // [NQ] running max (log2 units)
+  float* thr_s = reinterpret_cast<float*>(aux + 896);      // [NQ] rescale trigger in raw score units
+  float* red = reinterpret_cast<float*>(aux + 1280);       // [2 wg][4 warps][32]
+  float* alpha_s = reinterpret_cast<float*>(aux + 2304);   // [NQ] rescale factors / 1/l
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int b = blockIdx.z;
@@ -198,9 +208,8 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
       if (p.num_splits == 1) {
         p.out[row * C::D_V + d] = __float2bfloat16(0.f);
         if (d == 0) p.lse[row] = -INFINITY;
-      } else {
-        p.o_part[(split * n_rows_total + row) * C::D_V + d] = 0.f;
-        if (d == 0) p.lse_part[split * n_rows_total + row] = -INFINITY;
+      } else if (d == 0) {
+        p.lse_part[split * n_rows_total + row] = -INFINITY;  // o_part never read for an empty split
       }
     }
     return;
@@ -208,9 +217,13 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
 
   // ------------------------------------------------------------- setup
   if (threadIdx.x == 0) {
-    for (int i = 0; i < NS; ++i) { mbar_init(&kv_full[i], 1); mbar_init(&kv_empty[i], 1); }
+    for (int i = 0; i < NS; ++i) {
+      mbar_init(&kv_full[i], 1);
+      mbar_init(&kv_empty[i], 1);
+      mbar_init(&p_full[i], 8);
+    }
     for (int i = 0; i < 2; ++i) { mbar_init(&s_full[i], 1); mbar_init(&s_empty[i], 8); }
-    for (int i = 0; i < NP; ++i) { mbar_init(&p_full[i], 8); mbar_init(&p_empty[i], 1); }
+    for (int i = 0; i < 4; ++i) mbar_init(&pv_done[i], 1);
     mbar_init(q_full, 64);
     fence_barrier_init();
     tma_prefetch_desc(&tmap);
@@ -223,15 +236,22 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
       ve = p.causal ? max(0, min(L, L - p.Lq + t + 1)) : L;
     }
     vend_s[n] = ve;
+    m_run[n] = -INFINITY;
+    thr_s[n] = -INFINITY;
   }
   if (warp == 2) { tmem_alloc(tmem_slot, C::TMEM_COLS); tmem_relinquish(); }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  uint64_t* trace = p.trace ? p.trace + static_cast<size_t>((blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x +
+                                                             blockIdx.x) * kTraceStride
+                            : nullptr;
+  if (trace && threadIdx.x == 0) trace[0] = globaltimer();
 
   if (warp == 0) {
     // ========================= TMA producer (all 32 lanes issue) =========================
+    named_bar_sync(3, 96);  // Q loads are issued first: the first QK needs Q, not a second tile
     const int* bt_row = p.block_table + static_cast<size_t>(b) * p.bt_stride;
     const int box_rows = p.box_rows;
     for (int it = 0; it < ntiles; ++it) {
@@ -251,20 +271,24 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
         const uint32_t dst = sbase + stage * C::STAGE + ch * C::CHUNK + box * box_rows * 128;
         tma_load_2d(dst, &tmap, &kv_full[stage], col, row);
       }
+      if (trace && lane == 0 && it < kTraceTiles) trace[8 + 5 * it] = globaltimer();
     }
   } else if (warp == 1) {
     // ========================= UMMA issuer (one thread) =========================
     if (lane == 0) {
       mbar_wait(q_full, 0);
       tc_fence_after();
+      if (trace) trace[1] = globaltimer();
       constexpr uint32_t idesc_qk = make_idesc_bf16(128, NQ, false, false);
       constexpr uint32_t idesc_pv = make_idesc_bf16(128, NQ, true, true);
       const uint32_t q_base = sbase + C::OFF_Q;
+      // QK(i) needs tile i in smem and a free S buffer; PV(j) needs P(j).
+      // Poll both and issue whichever is ready, so PV never queues behind
+      // a QK that is still waiting for its TMA load (that would serialise
+      // the load latency with the stage release).
       auto issue_qk = [&](int it) {
         const int stage = it % NS;
-        mbar_wait(&kv_full[stage], (it / NS) & 1);
         const int sb = it & 1;
-        mbar_wait(&s_empty[sb], ((it >> 1) & 1) ^ 1);
         tc_fence_after();
         const uint32_t d = tmem + sb * NQ;
         const uint32_t kv = sbase + stage * C::STAGE;
@@ -282,12 +306,10 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
         umma_commit(&s_full[sb]);
       };
       auto issue_pv = [&](int j) {
-        const int pb = j % NP;
-        mbar_wait(&p_full[pb], (j / NP) & 1);
         tc_fence_after();
         const int stage = j % NS;
         const uint32_t kv = sbase + stage * C::STAGE;
-        const uint32_t pt = sbase + C::OFF_P + pb * C::PBYTES;
+        const uint32_t pt = kv + C::NCH_V * C::CHUNK;
 #pragma unroll
         for (int blk = 0; blk < C::NBLK_O; ++blk) {
 #pragma unroll
@@ -296,37 +318,51 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
                         desc_mnmajor_noswz(pt + k * 256, 128, 2048), idesc_pv, (j > 0 || k > 0) ? 1u : 0u);
         }
         umma_commit(&kv_empty[stage]);
-        umma_commit(&p_empty[pb]);
+        umma_commit(&pv_done[j & 3]);
       };
-      if constexpr (NS >= 2) {
-        for (int it = 0; it < ntiles; ++it) {
-          issue_qk(it);
-          if (it > 0) issue_pv(it - 1);
+      int next_qk = 0, next_pv = 0;
+      long long t0 = clock64();
+      while (next_pv < ntiles) {
+        if (next_pv < next_qk &&
+            mbar_test_wait(smem_u32(&p_full[next_pv % NS]), (next_pv / NS) & 1)) {
+          if (trace && next_pv < kTraceTiles) trace[12 + 5 * next_pv] = globaltimer();
+          issue_pv(next_pv++);
+          t0 = clock64();
+        } else if (next_qk < ntiles && next_qk < next_pv + 2 &&
+                   mbar_test_wait(smem_u32(&kv_full[next_qk % NS]), (next_qk / NS) & 1) &&
+                   mbar_test_wait(smem_u32(&s_empty[next_qk & 1]), ((next_qk >> 1) & 1) ^ 1)) {
+          if (trace && next_qk < kTraceTiles) trace[9 + 5 * next_qk] = globaltimer();
+          issue_qk(next_qk++);
+          t0 = clock64();
+        } else if (clock64() - t0 > (1ll << 34)) {
+          printf("glad: MMA scheduler watchdog (block %d,%d,%d qk %d pv %d)\n", blockIdx.x, blockIdx.y,
+                 blockIdx.z, next_qk, next_pv);
+          __trap();
         }
-        issue_pv(ntiles - 1);
-      } else {
-        for (int it = 0; it < ntiles; ++it) { issue_qk(it); issue_pv(it); }
       }
     }
   } else if (warp < 4) {
-    // ========================= Q loader (64 threads) =========================
+    // ========================= Q loader (64 threads, cp.async) =========================
     const int tid = threadIdx.x - 64;
     for (int idx = tid; idx < NQ * C::NQCH * 8; idx += 64) {
       const int n = idx / (C::NQCH * 8);
       const int u = idx - n * (C::NQCH * 8);
       const int ch = u >> 3, w = u & 7;
-      uint4 v = make_uint4(0u, 0u, 0u, 0u);
+      const void* src = p.q;
+      uint32_t bytes = 0;
       if (n < nq) {
         const bool rope = ch >= C::NCH_QK;
         const int col = rope ? C::D_KN + w * 8 : ch * 64 + w * 8;
         if (!rope || w * 8 < C::D_R) {
           const int ng = n0 + n, t = ng / p.g_q, h = head * p.g_q + (ng - t * p.g_q);
-          const __nv_bfloat16* src = p.q + ((static_cast<size_t>(b) * p.Lq + t) * p.H + h) * C::DQ + col;
-          v = __ldg(reinterpret_cast<const uint4*>(src));
+          src = p.q + ((static_cast<size_t>(b) * p.Lq + t) * p.H + h) * C::DQ + col;
+          bytes = 16;
         }
       }
-      st_shared_v4(sbase + C::OFF_Q + ch * C::QCHUNK + n * 128 + ((w ^ (n & 7)) << 4), v.x, v.y, v.z, v.w);
+      cp_async16(sbase + C::OFF_Q + ch * C::QCHUNK + n * 128 + ((w ^ (n & 7)) << 4), src, bytes);
     }
+    named_bar_arrive(3, 96);
+    cp_async_wait_all();
     fence_proxy_async_smem();
     mbar_arrive(q_full);
   } else {
@@ -337,17 +373,23 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
     const int c0 = wg * CW;
     const uint32_t lane_addr = static_cast<uint32_t>(wq * 32) << 16;
     const uint32_t bar_id = 1 + wg;
+    const uint32_t m_addr = smem_u32(m_run + c0);
+    const uint32_t t_addr = smem_u32(thr_s + c0);
+    const uint32_t a_addr = smem_u32(alpha_s + c0);
+    const float sl2 = p.scale_log2;
+    const float inv_sl2 = 1.f / sl2;
     int min_vend = 1 << 30;
     for (int n = 0; n < nq; ++n) min_vend = min(min_vend, vend_s[n]);
-    float m[CW], l[CW];
+    float l[CW];
 #pragma unroll
-    for (int n = 0; n < CW; ++n) { m[n] = -INFINITY; l[n] = 0.f; }
+    for (int n = 0; n < CW; ++n) l[n] = 0.f;
 
     for (int it = 0; it < ntiles; ++it) {
       const int sb = it & 1;
       mbar_wait(&s_full[sb], (it >> 1) & 1);
       tc_fence_after();
-      float x[CW];
+      if (trace && threadIdx.x == 128 && it < kTraceTiles) trace[10 + 5 * it] = globaltimer();
+      float x[CW];  // raw scores q.k for this thread's token, this WG's query columns
       tmem_load_cols<C>(tmem + lane_addr + sb * NQ + c0, x);
       tmem_ld_wait();
       tc_fence_before();
@@ -356,38 +398,54 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
 
       const int p0 = (tile_begin + it) * T;
       const int tok = p0 + r;
-      const bool full = (p0 + T <= min_vend);
+      if (!(p0 + T <= min_vend && nq == NQ)) {  // masked tile (last tile / causal / padded columns)
 #pragma unroll
-      for (int n = 0; n < CW; ++n) {
-        const bool ok = (c0 + n < nq) && (full || tok < vend_s[c0 + n]);
-        x[n] = ok ? x[n] * p.scale_log2 : -INFINITY;
+        for (int n = 0; n < CW; ++n) {
+          const bool ok = (c0 + n < nq) && tok < vend_s[c0 + n];
+          x[n] = ok ? x[n] : -INFINITY;
+        }
       }
       bool need = false;
 #pragma unroll
-      for (int n = 0; n < CW; ++n) need |= (x[n] > m[n] + TAU);
+      for (int n = 0; n < CW; n += 4) {
+        const float4 th = ld_shared_f4(t_addr + n * 4);
+        need |= (x[n] > th.x) | (x[n + 1] > th.y) | (x[n + 2] > th.z) | (x[n + 3] > th.w);
+      }
       if (named_bar_red_or(bar_id, 128, need)) {
-        float tmp[CW];
+        // the running max moves by > 2^TAU somewhere: column max over the WG,
+        // new m / alpha (rare after the first tile)
+        // (in halves of <= 16 columns to bound register pressure)
+        constexpr int HW = CW > 16 ? 16 : CW;
 #pragma unroll
-        for (int n = 0; n < CW; ++n) tmp[n] = x[n];
-        const float cm = warp_col_reduce<CW, true>(tmp, lane);
-        if ((lane & ((1 << col_shift<CW>()) - 1)) == 0) red[(wg * 4 + wq) * 32 + (lane >> col_shift<CW>())] = cm;
-        named_bar_sync(bar_id, 128);
-        float alpha[CW];
-        bool any_scale = false;
+        for (int h0 = 0; h0 < CW; h0 += HW) {
+          float tmp[HW];
 #pragma unroll
-        for (int n = 0; n < CW; ++n) {
-          const float* rr = red + wg * 128 + n;
-          const float mt = fmaxf(fmaxf(rr[0], rr[32]), fmaxf(rr[64], rr[96]));
-          const float mn = fmaxf(m[n], mt);
-          alpha[n] = (mn == -INFINITY) ? 1.f : ex2(m[n] - mn);
-          any_scale |= (alpha[n] != 1.f);
-          m[n] = mn;
-          l[n] *= alpha[n];
+          for (int n = 0; n < HW; ++n) tmp[n] = x[h0 + n];
+          const float cm = warp_col_reduce<HW, true>(tmp, lane);
+          if ((lane & ((1 << col_shift<HW>()) - 1)) == 0)
+            red[(wg * 4 + wq) * 32 + h0 + (lane >> col_shift<HW>())] = cm;
         }
         named_bar_sync(bar_id, 128);
-        if (it > 0 && any_scale) {  // rescale the O^T columns of this WG (rare)
+        if (r < CW) {
+          const float* rr = red + wg * 128 + r;
+          const float mt = fmaxf(fmaxf(rr[0], rr[32]), fmaxf(rr[64], rr[96])) * sl2;
+          const float mo = m_run[c0 + r];
+          const float mn = fmaxf(mo, mt);
+          alpha_s[c0 + r] = (mn == -INFINITY) ? 1.f : ex2(mo - mn);
+          m_run[c0 + r] = mn;
+          thr_s[c0 + r] = (mn == -INFINITY) ? -INFINITY : (mn + TAU) * inv_sl2;
+        }
+        named_bar_sync(bar_id, 128);
+        bool any_scale = false;
+#pragma unroll
+        for (int n = 0; n < CW; n += 4) {
+          const float4 a = ld_shared_f4(a_addr + n * 4);
+          l[n] *= a.x; l[n + 1] *= a.y; l[n + 2] *= a.z; l[n + 3] *= a.w;
+          any_scale |= (a.x != 1.f) | (a.y != 1.f) | (a.z != 1.f) | (a.w != 1.f);
+        }
+        if (it > 0 && any_scale) {  // rescale this WG's O^T columns in TMEM
           const int j = it - 1;
-          mbar_wait(&p_empty[j % NP], (j / NP) & 1);
+          mbar_wait(&pv_done[j & 3], (j >> 2) & 1);
           tc_fence_after();
 #pragma unroll
           for (int blk = 0; blk < C::NBLK_O; ++blk) {
@@ -396,32 +454,39 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
             tmem_load_cols<C>(ta, o);
             tmem_ld_wait();
 #pragma unroll
-            for (int n = 0; n < CW; ++n) o[n] *= alpha[n];
+            for (int n = 0; n < CW; n += 4) {
+              const float4 a = ld_shared_f4(a_addr + n * 4);
+              o[n] *= a.x; o[n + 1] *= a.y; o[n + 2] *= a.z; o[n + 3] *= a.w;
+            }
             tmem_store_cols<C>(ta, o);
           }
           tmem_st_wait();
         }
       }
-      // probabilities -> bf16 P^T (MN-major, no swizzle: [NQ/8][128 tok][8])
-      const int pb = it % NP;
-      mbar_wait(&p_empty[pb], ((it / NP) & 1) ^ 1);
-      uint32_t packed[CW / 2];
+      // p = 2^(s*c - m): bf16 P^T into the tile's (now dead) RoPE chunk,
+      // MN-major no-swizzle [NQ/8][128 tok][8]
+      const uint32_t stage_base = sbase + (it % NS) * C::STAGE;
+      const uint32_t pt = stage_base + C::NCH_V * C::CHUNK + (c0 / 8) * 2048 + r * 16;
 #pragma unroll
-      for (int n = 0; n < CW; n += 2) {
-        const float ms0 = (m[n] == -INFINITY) ? 0.f : m[n];
-        const float ms1 = (m[n + 1] == -INFINITY) ? 0.f : m[n + 1];
-        const __nv_bfloat162 v = __floats2bfloat162_rn(ex2(x[n] - ms0), ex2(x[n + 1] - ms1));
-        l[n] += __low2float(v);
-        l[n + 1] += __high2float(v);
-        packed[n / 2] = *reinterpret_cast<const uint32_t*>(&v);
+      for (int g = 0; g < CW / 8; ++g) {
+        const float4 ma = ld_shared_f4(m_addr + g * 32);
+        const float4 mb = ld_shared_f4(m_addr + g * 32 + 16);
+        const float mv[8] = {ma.x, ma.y, ma.z, ma.w, mb.x, mb.y, mb.z, mb.w};
+        uint32_t pk[4];
+#pragma unroll
+        for (int k = 0; k < 8; k += 2) {
+          const float m0 = mv[k] == -INFINITY ? 0.f : mv[k];
+          const float m1 = mv[k + 1] == -INFINITY ? 0.f : mv[k + 1];
+          const __nv_bfloat162 v =
+              __floats2bfloat162_rn(ex2(fmaf(x[g * 8 + k], sl2, -m0)), ex2(fmaf(x[g * 8 + k + 1], sl2, -m1)));
+          l[g * 8 + k] += __low2float(v);
+          l[g * 8 + k + 1] += __high2float(v);
+          pk[k / 2] = *reinterpret_cast<const uint32_t*>(&v);
+        }
+        st_shared_v4(pt + g * 2048, pk[0], pk[1], pk[2], pk[3]);
       }
-      const uint32_t pt = sbase + C::OFF_P + pb * C::PBYTES;
-#pragma unroll
-      for (int g = 0; g < CW / 8; ++g)
-        st_shared_v4(pt + (c0 / 8 + g) * 2048 + r * 16, packed[4 * g], packed[4 * g + 1], packed[4 * g + 2],
-                     packed[4 * g + 3]);
       if (wg == 0 && tok >= kv_end) {  // never-visible rows: zero V so 0 * garbage cannot give NaN
-        const uint32_t kvrow = sbase + (it % NS) * C::STAGE + r * 128;
+        const uint32_t kvrow = stage_base + r * 128;
 #pragma unroll
         for (int ch = 0; ch < C::NCH_V; ++ch)
 #pragma unroll
@@ -430,38 +495,29 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
       fence_proxy_async_smem();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&p_full[pb]);
+      if (lane == 0) mbar_arrive(&p_full[it % NS]);
+      if (trace && threadIdx.x == 128 && it < kTraceTiles) trace[11 + 5 * it] = globaltimer();
     }
 
     // ------------------------------------------------------------- epilogue
-    float tmp[CW];
-#pragma unroll
-    for (int n = 0; n < CW; ++n) tmp[n] = l[n];
-    const float cs = warp_col_reduce<CW, false>(tmp, lane);
+    const float cs = warp_col_reduce<CW, false>(l, lane);
     if ((lane & ((1 << col_shift<CW>()) - 1)) == 0) red[(wg * 4 + wq) * 32 + (lane >> col_shift<CW>())] = cs;
-    if (threadIdx.x == 128 + wg * 128) {
-#pragma unroll
-      for (int n = 0; n < CW; ++n) m_s[c0 + n] = m[n];
-    }
     named_bar_sync(bar_id, 128);
-    float inv_l[CW];
-#pragma unroll
-    for (int n = 0; n < CW; ++n) {
-      const float* rr = red + wg * 128 + n;
-      const float ls = (rr[0] + rr[32]) + (rr[64] + rr[96]);
-      inv_l[n] = ls > 0.f ? 1.f / ls : 0.f;
-    }
-    if (r < CW && c0 + r < nq) {
+    if (r < CW) {  // fold the row sum into alpha_s as 1/l (reused below) and write lse
       const float* rr = red + wg * 128 + r;
       const float ls = (rr[0] + rr[32]) + (rr[64] + rr[96]);
-      const float lse = ls > 0.f ? (m_s[c0 + r] + __log2f(ls)) * 0.69314718055994531f : -INFINITY;
-      const int ng = n0 + c0 + r, t = ng / p.g_q, h = head * p.g_q + (ng - t * p.g_q);
-      const size_t row = (static_cast<size_t>(b) * p.Lq + t) * p.H + h;
-      if (p.num_splits == 1) p.lse[row] = lse;
-      else p.lse_part[split * n_rows_total + row] = lse;
+      alpha_s[c0 + r] = ls > 0.f ? 1.f / ls : 0.f;
+      if (c0 + r < nq) {
+        const float lse = ls > 0.f ? (m_run[c0 + r] + __log2f(ls)) * 0.69314718055994531f : -INFINITY;
+        const int ng = n0 + c0 + r, t = ng / p.g_q, h = head * p.g_q + (ng - t * p.g_q);
+        const size_t row = (static_cast<size_t>(b) * p.Lq + t) * p.H + h;
+        if (p.num_splits == 1) p.lse[row] = lse;
+        else p.lse_part[split * n_rows_total + row] = lse;
+      }
     }
+    named_bar_sync(bar_id, 128);
     const int j = ntiles - 1;
-    mbar_wait(&p_empty[j % NP], (j / NP) & 1);
+    mbar_wait(&pv_done[j & 3], (j >> 2) & 1);
     tc_fence_after();
 #pragma unroll
     for (int blk = 0; blk < C::NBLK_O; ++blk) {
@@ -474,7 +530,7 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
         if (c0 + n < nq) {
           const int ng = n0 + c0 + n, t = ng / p.g_q, h = head * p.g_q + (ng - t * p.g_q);
           const size_t row = (static_cast<size_t>(b) * p.Lq + t) * p.H + h;
-          const float val = o[n] * inv_l[n];
+          const float val = o[n] * alpha_s[c0 + n];
           if (p.num_splits == 1) p.out[row * C::D_V + d] = __float2bfloat16(val);
           else p.o_part[(split * n_rows_total + row) * C::D_V + d] = val;
         }
@@ -484,6 +540,7 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
 
   tc_fence_before();
   __syncthreads();
+  if (trace && threadIdx.x == 0) trace[2] = globaltimer();
   if (warp == 2) {
     tc_fence_after();
     tmem_dealloc(tmem, C::TMEM_COLS);

@@ -58,6 +58,7 @@ def _sig(lib):
     table = {
         "glad_last_error": ([], ctypes.c_char_p),
         "glad_version": ([], ctypes.c_char_p),
+        "glad_debug_set_trace": ([_VP], None),
         "glad_pool_bytes": ([L], ctypes.c_size_t),
         "glad_cache_append": ([L, _VP, _VP, ctypes.c_int32, _VP, _VP, ctypes.c_int32, ctypes.c_int32, _VP], S),
         "glad_paged_gather": ([L, _VP, _VP, ctypes.c_int32, _VP, ctypes.c_int32, ctypes.c_int32, _VP, _VP], S),
@@ -91,7 +92,7 @@ def lib():
 
 
 def exported_symbols():
-    return ["glad_last_error", "glad_version", "glad_pool_bytes", "glad_cache_append", "glad_paged_gather",
+    return ["glad_last_error", "glad_version", "glad_debug_set_trace", "glad_pool_bytes", "glad_cache_append", "glad_paged_gather",
             "glad_decode_workspace_bytes", "glad_decode_num_splits", "glad_gla_decode", "glad_mla_decode",
             "glad_gta_decode", "glad_splitkv_combine", "glad_tp_duplication", "glad_tp_shard",
             "glad_kv_bytes_per_token_per_device"]
@@ -236,6 +237,14 @@ def tp_shard(h_q, n_kv_heads, N, rank):
 
 def kv_bytes_per_token_per_device(variant, n_kv_heads, d_head, d_rope, N, dtype_bytes=2):
     return lib().glad_kv_bytes_per_token_per_device(variant, n_kv_heads, d_head, d_rope, N, dtype_bytes)
+
+
+TRACE_STRIDE = 8 + 5 * 64
+
+
+def debug_set_trace(buf):
+    """Debug timeline (see csrc/decode.cuh); buf: int64 CUDA tensor or None."""
+    lib().glad_debug_set_trace(_ptr(buf) if buf is not None else ctypes.c_void_p(0))
 
 
 def version():

@@ -1,0 +1,72 @@
+"""Per-CTA pipeline timeline of one decode step (debug tracing in the kernel).
+
+    python tools/trace.py --workload c2_gla2 [--splits N]
+
+Prints medians over CTAs of the per-tile stage latencies (ns):
+  load->QK   TMA load issued -> QK issued (load latency + MMA queueing)
+  QK->S      QK issued -> S seen by softmax (MMA time + signalling)
+  S->P       softmax time (S read -> P written)
+  P->PV      P written -> PV issued
+  PV->load   PV(i) issued -> load(i+NS) issued (PV time + stage release)
+  period     QK(i) -> QK(i+1) issue interval
+"""
+import argparse
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+from paper_2505_21487_b200 import glad, workloads  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--workload", default="c2_gla2")
+ap.add_argument("--splits", type=int, default=0)
+ap.add_argument("--ns", type=int, default=2, help="KV stages of the instantiation (for PV->load)")
+a = ap.parse_args()
+wl = workloads.get(a.workload)
+st = workloads.build_device_state(wl, splits=a.splits)
+for _ in range(3):
+    workloads.run(wl, st)
+torch.cuda.synchronize()
+n_ctas = 70000
+buf = torch.zeros(n_ctas * glad.TRACE_STRIDE, dtype=torch.int64, device="cuda")
+glad.debug_set_trace(buf)
+workloads.run(wl, st)
+torch.cuda.synchronize()
+glad.debug_set_trace(None)
+tr = buf.view(n_ctas, glad.TRACE_STRIDE).cpu().numpy().astype(np.int64)
+tr = tr[tr[:, 0] > 0]
+t0 = tr[:, 0].min()
+print(f"{wl.name}: splits {st['splits']}, {len(tr)} CTAs, kernel span {(tr[:, 2].max() - t0) / 1e3:.1f} us")
+print(f"CTA lifetime median {np.median(tr[:, 2] - tr[:, 0]) / 1e3:.1f} us, start->Q ready "
+      f"{np.median(tr[:, 1] - tr[:, 0]) / 1e3:.2f} us")
+T = (tr.shape[1] - 8) // 5
+tile = tr[:, 8:].reshape(len(tr), T, 5)  # load, qk, s, p, pv
+valid = tile[:, :, 1] > 0
+ntile = valid.sum(1)
+
+
+def med(x, m):
+    x = x[m]
+    return float(np.median(x)) if x.size else float("nan")
+
+
+m = valid.copy()
+m[:, 0] = False  # skip first tile (pipeline fill)
+print("median ns per tile (excluding tile 0):")
+print(f"  load->QK  {med(tile[:, :, 1] - tile[:, :, 0], m):8.0f}")
+print(f"  QK->S     {med(tile[:, :, 2] - tile[:, :, 1], m):8.0f}")
+print(f"  S->P      {med(tile[:, :, 3] - tile[:, :, 2], m):8.0f}")
+print(f"  P->PV     {med(tile[:, :, 4] - tile[:, :, 3], m):8.0f}")
+ns = a.ns
+pv_to_load = tile[:, :-ns, 4] - tile[:, ns:, 0]
+mm = valid[:, ns:] & valid[:, :-ns]
+print(f"  load(i+{ns})-PV(i) {med(-pv_to_load, mm):8.0f}")
+per = tile[:, 1:, 1] - tile[:, :-1, 1]
+print(f"  QK period {med(per, valid[:, 1:] & valid[:, :-1]):8.0f}")
+first = tile[:, 0]
+print(f"  first tile: start->load {np.median(first[:, 0] - tr[:, 0]):.0f}  load->QK {np.median(first[:, 1] - first[:, 0]):.0f}")
+last = np.array([tile[i, ntile[i] - 1, 4] for i in range(len(tr))])
+print(f"  last PV issue -> CTA end {np.median(tr[:, 2] - last):.0f}")
