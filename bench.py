@@ -178,7 +178,7 @@ def run_ours(args, rank, world, local_rank):
         base = name.replace("_tp1", "").replace("_tp2", "").replace("_tp4", "").replace("_tp8", "")
         name = base.replace("c5_gla8", f"c5_gla8_tp{world}")
     wl = workloads.get(name)
-    st = workloads.build_device_state(wl, seed=wl.seed + (0 if tp else rank), device=dev, splits=args.splits)
+    st = workloads.build_device_state(wl, seed=wl.seed + (0 if tp else rank), device=dev, num_ctas=args.ctas)
     sl = st["seqlens_host"]
     stream = torch.cuda.current_stream(dev)
 
@@ -252,19 +252,13 @@ def run_ours(args, rank, world, local_rank):
         ms = timed(run_step, args.steps)
     clocks = clk.summary()
 
-    # combine alone (same partials) -> decode kernel share of the step
-    comb_ms = 0.0
-    S = st["splits"]
-    if S > 1:
-        ws = st["workspace"].buf
-        rows = wl.B * wl.Lq * wl.H
-        o_bytes = ((S * rows * wl.d_v * 4) + 255) & ~255
-        o_part = ws[:S * rows * wl.d_v * 4].view(torch.float32).view(S, wl.B, wl.Lq, wl.H, wl.d_v)
-        lse_part = ws[o_bytes:o_bytes + S * rows * 4].view(torch.float32).view(S, wl.B, wl.Lq, wl.H)
-        comb = lambda: glad.splitkv_combine(o_part, lse_part, out=st["out"], lse=st["lse"], stream=stream)
-        comb()
-        comb_ms = timed(comb, args.steps)
-    decode_ms = max(ms - comb_ms, 1e-9)
+    # plan + merge kernels alone (same plan/partials) -> decode kernel share of the step
+    glad.debug_set_phase_mask(1 | 4)
+    aux_step = lambda: workloads.run(wl, st, stream=stream)
+    aux_step()
+    aux_ms = timed(aux_step, args.steps)
+    glad.debug_set_phase_mask(7)
+    decode_ms = max(ms - aux_ms, 1e-9)
 
     # ---- end to end through the public API with host buffers ----
     pinned_q = st["q"].cpu().pin_memory()
@@ -310,10 +304,10 @@ def run_ours(args, rank, world, local_rank):
             "peak": pk["hbm"] if bound == "hbm" else pk["bf16"], "unit": "GB/s" if bound == "hbm" else "TFLOP/s",
             "frac": hbm_frac if bound == "hbm" else ten_frac, "traffic": _traffic(wl.name),
             "peak_source": pk["src"] + " (MEASURED_PEAKS.json)",
-            "kernel": "glad::decode_kernel", "kernel_ms": decode_ms, "combine_ms": comb_ms,
+            "kernel": "glad::decode_kernel", "kernel_ms": decode_ms, "plan_merge_ms": aux_ms,
             "algorithmic_bytes": abytes, "algorithmic_flops": aflops,
             "hbm_frac": hbm_frac, "tensor_frac": ten_frac}
-    launches_per_step = 1 + (1 if S > 1 else 0)
+    launches_per_step = 3  # plan, decode, merge
 
     if rank == 0:
         cpu = None
@@ -328,7 +322,7 @@ def run_ours(args, rank, world, local_rank):
             "scaling": "strong" if tp else "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
             "config": {"workload": wl.name, "desc": wl.description, "B": wl.B, "q_len": wl.Lq, "H": wl.H,
                        "n_kv_heads": wl.h_c, "d_head": wl.d_c, "d_rope": wl.d_R, "ctx_max": wl.L,
-                       "ctx_mean": float(np.mean(sl)), "page": wl.page, "splits": S,
+                       "ctx_mean": float(np.mean(sl)), "page": wl.page, "num_ctas": st["num_ctas"] or "num_SMs",
                        "parallelism": (f"tp{world}" if tp else f"dp{world} (independent batches)"),
                        "l2": f"inputs larger than L2 ({abytes / 1e9:.2f} GB algorithmic per step > 126 MB); "
                              "no flush", "cuda_graph": graph is not None},
@@ -336,7 +330,7 @@ def run_ours(args, rank, world, local_rank):
             "roofline": roof, "cpu_baseline": cpu,
             "e2e": {"value": total_tokens / (e2e_ms * 1e-3), "unit": "tokens/s", "ms_per_step": e2e_ms,
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                    "includes": "H2D q + new KV rows (pinned), cache append, decode(+combine), D2H out + lse"},
+                    "includes": "H2D q + new KV rows (pinned), cache append, plan+decode+merge, D2H out + lse"},
             "gpu_launches": launches_per_step * args.steps,
             "clocks": clocks,
         }
@@ -351,7 +345,7 @@ def main():
     ap.add_argument("--workload", default="c2_gla2")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--splits", type=int, default=0, help="force the KV split count (0 = library heuristic)")
+    ap.add_argument("--ctas", type=int, default=0, help="persistent CTA count (0 = one per SM)")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))

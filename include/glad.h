@@ -106,17 +106,15 @@ GLAD_API glad_status glad_paged_gather(const glad_cache_layout* layout, const vo
                               void* dense_out, void* stream);
 
 /*
- * Workspace for split-KV partials: max_splits * B*Lq*H * (d_v + 1) * 4 bytes
- * (+ alignment).  Zero if max_splits <= 1.
+ * Device workspace (bytes) one decode call needs: the schedule plan
+ * (per-unit tile prefix sums) and the partial (o, lse) slots of units that
+ * the persistent schedule splits between CTAs.  `variant` is GLAD_GLA,
+ * GLAD_MLA or GLAD_GTA; num_ctas as in the decode calls.  0 on invalid input.
+ * The workspace must be 256-byte aligned; its contents need no
+ * initialisation and are overwritten by every call.
  */
-GLAD_API size_t glad_decode_workspace_bytes(int32_t B, int32_t Lq, int32_t H, int32_t d_v, int32_t max_splits);
-
-/*
- * Number of KV splits the heuristic would use (num_splits argument 0), given
- * only host-known quantities (max KV length bound = bt_stride*page_size).
- */
-GLAD_API int32_t glad_decode_num_splits(const glad_cache_layout* layout, int32_t B, int32_t Lq, int32_t H,
-                               int32_t bt_stride, int32_t variant);
+GLAD_API size_t glad_decode_workspace_bytes(const glad_cache_layout* layout, int32_t B, int32_t Lq, int32_t H,
+                                            int32_t variant, int32_t num_ctas);
 
 /*
  * GLA decode (per rank: O_i = softmax(Q_i (c_i^KV)^T) c_i^KV,
@@ -133,10 +131,13 @@ GLAD_API int32_t glad_decode_num_splits(const glad_cache_layout* layout, int32_t
  *  out     [B, Lq, H, d_head] bf16 = sum_j p_j c_j (latent space).
  *  lse     [B, Lq, H] fp32 natural-log LSE (R3); -inf and out = 0 when a
  *          query has no visible key.
- *  workspace / ws_bytes  split-KV partials (glad_decode_workspace_bytes with
- *          the num_splits actually used); may be NULL when that is 1.
- *  num_splits  0 = heuristic (glad_decode_num_splits); else the requested
- *          number of KV splits (>= 1).
+ *  workspace / ws_bytes  device workspace (glad_decode_workspace_bytes).
+ *  num_ctas  0 = one persistent CTA per SM (the default); k > 0 = exactly k
+ *          CTAs.  The KV tiles of all (sequence, head, query block) units are
+ *          split evenly across the CTAs (a unit may be cut into split-KV
+ *          segments that are LSE-merged); any k gives the same result up to
+ *          fp32 rounding order.
+ * Launches three kernels on `stream`: plan, decode, merge.
  * Requirements: H % n_heads_kv == 0; (d_head, d_rope) in {(128, 32),
  * (128, 64), (256, 32), (256, 64), (512, 64)}; Lq >= 1; q and out 16-byte
  * aligned.  Other shapes return GLAD_ERR_UNSUPPORTED.
@@ -144,13 +145,13 @@ GLAD_API int32_t glad_decode_num_splits(const glad_cache_layout* layout, int32_t
 GLAD_API glad_status glad_gla_decode(const void* q, const void* pool, const glad_cache_layout* layout,
                             const int32_t* block_table, int32_t bt_stride, const int32_t* seqlens, int32_t B,
                             int32_t Lq, int32_t H, float softmax_scale, int32_t causal, void* out, float* lse,
-                            void* workspace, size_t ws_bytes, int32_t num_splits, void* stream);
+                            void* workspace, size_t ws_bytes, int32_t num_ctas, void* stream);
 
 /* MLA baseline: GLA with a single latent head (n_heads_kv == 1). */
 GLAD_API glad_status glad_mla_decode(const void* q, const void* pool, const glad_cache_layout* layout,
                             const int32_t* block_table, int32_t bt_stride, const int32_t* seqlens, int32_t B,
                             int32_t Lq, int32_t H, float softmax_scale, int32_t causal, void* out, float* lse,
-                            void* workspace, size_t ws_bytes, int32_t num_splits, void* stream);
+                            void* workspace, size_t ws_bytes, int32_t num_ctas, void* stream);
 
 /*
  * GTA decode.  q [B, Lq, H, d_head] bf16 = [q_nope (d_head/2) ||
@@ -163,7 +164,7 @@ GLAD_API glad_status glad_mla_decode(const void* q, const void* pool, const glad
 GLAD_API glad_status glad_gta_decode(const void* q, const void* pool, const glad_cache_layout* layout,
                             const int32_t* block_table, int32_t bt_stride, const int32_t* seqlens, int32_t B,
                             int32_t Lq, int32_t H, float softmax_scale, int32_t causal, void* out, float* lse,
-                            void* workspace, size_t ws_bytes, int32_t num_splits, void* stream);
+                            void* workspace, size_t ws_bytes, int32_t num_ctas, void* stream);
 
 /*
  * Split-KV LSE merge (not in the paper; BASELINE north_star):
@@ -182,6 +183,10 @@ GLAD_API glad_status glad_splitkv_combine(const float* o_part, const float* lse_
  * the grid.  NULL turns tracing off (the default).  Not thread-safe.
  */
 GLAD_API void glad_debug_set_trace(void* device_buf);
+/* Debug/benchmark only: bit mask of the decode call's kernels to launch,
+ * 1 = plan, 2 = decode, 4 = merge (default 7).  Used to time the decode
+ * kernel alone.  Not thread-safe. */
+GLAD_API void glad_debug_set_phase_mask(int32_t mask);
 
 /* ---- tp_shard helpers: host-only, pure (no CUDA) ---- */
 

@@ -15,6 +15,7 @@ namespace {
 
 thread_local char g_err[512] = "no error";
 uint64_t* g_trace = nullptr;  // debug timeline buffer (glad_debug_set_trace)
+int g_phase_mask = 7;         // debug: which of plan(1) / decode(2) / merge(4) to launch
 
 glad_status fail(glad_status s, const char* fmt, ...) {
   va_list ap;
@@ -74,25 +75,6 @@ int64_t row_width(const glad_cache_layout* L) {
   return static_cast<int64_t>(L->n_heads_kv) * L->d_head + L->d_rope;
 }
 
-// Choose the split count from host-known data only (max length bound =
-// bt_stride * page_size): fill the SMs with >= 90% wave efficiency, keep
-// >= 8 tiles per split.
-int32_t plan_splits(int64_t units, int64_t max_len) {
-  const int sms = num_sms();
-  const int64_t tiles = (max_len + 127) / 128;
-  const int smax = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(32, tiles / 8)));
-  if (units <= 0) return 1;
-  int best = 1;
-  double best_eff = 0.0;
-  for (int s = 1; s <= smax; ++s) {
-    const double x = static_cast<double>(units) * s / sms;
-    const double eff = x / std::ceil(x);
-    if (eff >= 0.9) return s;
-    if (eff > best_eff + 1e-9) { best_eff = eff; best = s; }
-  }
-  return best;
-}
-
 enum Variant { kGLA, kMLA, kGTA };
 
 struct DecodeGeom {
@@ -127,23 +109,30 @@ glad_status decode_geom(Variant v, const glad_cache_layout* L, int32_t Lq, int32
   return GLAD_OK;
 }
 
-size_t ws_bytes_for(int64_t rows, int32_t d_v, int32_t S) {
-  if (S <= 1) return 0;
-  const size_t o = static_cast<size_t>(S) * rows * d_v * sizeof(float);
-  const size_t l = static_cast<size_t>(S) * rows * sizeof(float);
-  return ((o + 255) & ~size_t(255)) + ((l + 255) & ~size_t(255));
+// Workspace of one decode call: [plan (U+1) int32][lse_part (G+U)*NQ f32]
+// [o_part (G+U)*NQ*D_V f32], each 256-byte aligned.
+struct WsLayout {
+  size_t plan, lse, opart, total;
+};
+WsLayout ws_layout(int64_t U, int64_t G, int nq, int d_v) {
+  auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
+  WsLayout w;
+  w.plan = 0;
+  w.lse = al(static_cast<size_t>(U + 1) * 4);
+  w.opart = w.lse + al(static_cast<size_t>(G + U) * nq * 4);
+  w.total = w.opart + al(static_cast<size_t>(G + U) * nq * d_v * 4);
+  return w;
 }
 
 glad_status decode_common(Variant v, const void* q, const void* pool, const glad_cache_layout* L,
                           const int32_t* block_table, int32_t bt_stride, const int32_t* seqlens, int32_t B,
                           int32_t Lq, int32_t H, float scale, int32_t causal, void* out, float* lse, void* ws,
-                          size_t ws_bytes, int32_t num_splits, void* stream) {
+                          size_t ws_bytes, int32_t num_ctas, void* stream) {
   DecodeGeom g;
   glad_status s = decode_geom(v, L, Lq, H, &g);
   if (s != GLAD_OK) return s;
   if (B < 0) return fail(GLAD_ERR_INVALID_ARG, "B=%d < 0", B);
   if (B == 0) return GLAD_OK;
-  if (B > 65535) return fail(GLAD_ERR_UNSUPPORTED, "B=%d > 65535", B);
   if (!q || !pool || !block_table || !seqlens || !out || !lse)
     return fail(GLAD_ERR_INVALID_ARG, "NULL tensor pointer (q=%p pool=%p bt=%p seqlens=%p out=%p lse=%p)", q,
                 pool, block_table, seqlens, out, lse);
@@ -152,15 +141,14 @@ glad_status decode_common(Variant v, const void* q, const void* pool, const glad
   if (bt_stride < 1) return fail(GLAD_ERR_INVALID_ARG, "bt_stride=%d < 1", bt_stride);
   if (!(scale > 0.f) || !std::isfinite(scale))
     return fail(GLAD_ERR_INVALID_ARG, "softmax_scale=%g must be finite and > 0", scale);
-  if (num_splits < 0) return fail(GLAD_ERR_INVALID_ARG, "num_splits=%d < 0", num_splits);
-  const int64_t units = static_cast<int64_t>(B) * L->n_heads_kv * g.n_qblk;
-  const int64_t max_len = static_cast<int64_t>(bt_stride) * L->page_size;
-  int32_t S = num_splits > 0 ? num_splits : plan_splits(units, max_len);
-  if (S > 65535) return fail(GLAD_ERR_INVALID_ARG, "num_splits=%d too large", S);
-  const int64_t rows = static_cast<int64_t>(B) * Lq * H;
-  const size_t need = ws_bytes_for(rows, L->d_head, S);
-  if (S > 1 && (ws == nullptr || ws_bytes < need))
-    return fail(GLAD_ERR_WORKSPACE, "workspace %zu bytes < required %zu for %d splits", ws_bytes, need, S);
+  if (num_ctas < 0) return fail(GLAD_ERR_INVALID_ARG, "num_ctas=%d < 0", num_ctas);
+  const int64_t U = static_cast<int64_t>(B) * L->n_heads_kv * g.n_qblk;
+  if (U >= (int64_t(1) << 30)) return fail(GLAD_ERR_UNSUPPORTED, "too many work units (%lld)", (long long)U);
+  const int G = num_ctas > 0 ? num_ctas : num_sms();
+  const WsLayout wl = ws_layout(U, G, g.key.nq, L->d_head);
+  if (ws == nullptr || ws_bytes < wl.total)
+    return fail(GLAD_ERR_WORKSPACE, "workspace %zu bytes < required %zu", ws_bytes, wl.total);
+  if (reinterpret_cast<uintptr_t>(ws) & 255u) return fail(GLAD_ERR_INVALID_ARG, "workspace must be 256-byte aligned");
 
   auto enc = encode_fn();
   if (!enc) return fail(GLAD_ERR_CUDA, "cuTensorMapEncodeTiled entry point unavailable");
@@ -176,37 +164,70 @@ glad_status decode_common(Variant v, const void* q, const void* pool, const glad
                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (cr != CUDA_SUCCESS) return fail(GLAD_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", static_cast<int>(cr));
 
+  // Q as a 3-D tensor [B*Lq][H][d_qk]: a unit's NQ query rows are one box
+  // (64 cols, g_q heads, NQ/g_q positions) or (64 cols, NQ heads, 1).
+  const int dq = g.key.d_kn + g.key.d_r;
+  int q_box_h = 0, q_box_t = 0;
+  if (g.g_q % g.key.nq == 0) { q_box_h = g.key.nq; q_box_t = 1; }
+  else if (g.key.nq % g.g_q == 0) { q_box_h = g.g_q; q_box_t = g.key.nq / g.g_q; }
+  CUtensorMap qmap;
+  std::memset(&qmap, 0, sizeof(qmap));
+  bool q_tma = q_box_h > 0 && q_box_h <= 256 && q_box_t <= 256 && (reinterpret_cast<uintptr_t>(q) & 15u) == 0;
+  if (q_tma) {
+    cuuint64_t qd[3] = {static_cast<cuuint64_t>(dq), static_cast<cuuint64_t>(H),
+                        static_cast<cuuint64_t>(B) * static_cast<cuuint64_t>(Lq)};
+    cuuint64_t qs[2] = {static_cast<cuuint64_t>(dq) * 2, static_cast<cuuint64_t>(H) * dq * 2};
+    cuuint32_t qbx[3] = {64u, static_cast<cuuint32_t>(q_box_h), static_cast<cuuint32_t>(q_box_t)};
+    cuuint32_t qe[3] = {1u, 1u, 1u};
+    q_tma = enc(&qmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(q), qd, qs, qbx, qe,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  }
+
+  char* wsb = static_cast<char*>(ws);
   glad::DecodeParams p;
+  p.q_tma = q_tma ? 1 : 0;
+  p.q_box_h = q_box_h;
+  p.q_box_t = q_box_t;
   p.q = static_cast<const __nv_bfloat16*>(q);
   p.block_table = block_table;
   p.seqlens = seqlens;
+  p.plan = reinterpret_cast<const int32_t*>(wsb + wl.plan);
   p.out = static_cast<__nv_bfloat16*>(out);
   p.lse = lse;
-  const size_t o_bytes = ((static_cast<size_t>(S) * rows * L->d_head * sizeof(float)) + 255) & ~size_t(255);
-  p.o_part = S > 1 ? static_cast<float*>(ws) : nullptr;
-  p.lse_part = S > 1 ? reinterpret_cast<float*>(static_cast<char*>(ws) + o_bytes) : nullptr;
+  p.o_part = reinterpret_cast<float*>(wsb + wl.opart);
+  p.lse_part = reinterpret_cast<float*>(wsb + wl.lse);
   p.bt_stride = bt_stride;
   p.B = B;
   p.Lq = Lq;
   p.H = H;
   p.g_q = g.g_q;
+  p.n_heads_kv = L->n_heads_kv;
   p.d_head = L->d_head;
   p.rope_col = L->n_heads_kv * L->d_head;
   p.page_size = L->page_size;
   p.log2_page = ilog2(L->page_size);
   p.box_rows = box_rows;
-  p.num_splits = S;
   p.n_qblk = g.n_qblk;
+  p.n_units = static_cast<int32_t>(U);
   p.causal = causal ? 1 : 0;
   p.scale_log2 = scale * 1.4426950408889634f;
   p.trace = g_trace;
-  dim3 grid(static_cast<unsigned>(S), static_cast<unsigned>(L->n_heads_kv * g.n_qblk), static_cast<unsigned>(B));
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  cudaError_t e = glad::launch_decode(g.key, tmap, p, grid, st);
-  if (e != cudaSuccess) return fail(GLAD_ERR_CUDA, "decode launch failed: %s", cudaGetErrorString(e));
-  if (S > 1) {
-    e = glad::launch_combine(p.o_part, p.lse_part, S, rows, L->d_head, out, lse, st);
-    if (e != cudaSuccess) return fail(GLAD_ERR_CUDA, "combine launch failed: %s", cudaGetErrorString(e));
+  int32_t* plan = reinterpret_cast<int32_t*>(wsb + wl.plan);
+  cudaError_t e = cudaSuccess;
+  if (g_phase_mask & 1) {
+    e = glad::launch_plan(seqlens, plan, p.n_units, B, g.n_qblk, g.key.nq, Lq, g.g_q, p.causal, st);
+    if (e != cudaSuccess) return fail(GLAD_ERR_CUDA, "plan launch failed: %s", cudaGetErrorString(e));
+  }
+  if (g_phase_mask & 2) {
+    e = glad::launch_decode(g.key, tmap, qmap, p, G, st);
+    if (e != cudaSuccess) return fail(GLAD_ERR_CUDA, "decode launch failed: %s", cudaGetErrorString(e));
+  }
+  if (g_phase_mask & 4) {
+    e = glad::launch_merge_units(plan, p.o_part, p.lse_part, G, p.n_units, g.key.nq, g.n_qblk, B, g.g_q,
+                                 Lq, H, static_cast<int64_t>(B) * Lq * H, L->d_head, out, lse, st);
+    if (e != cudaSuccess) return fail(GLAD_ERR_CUDA, "merge launch failed: %s", cudaGetErrorString(e));
   }
   return GLAD_OK;
 }
@@ -220,6 +241,8 @@ const char* glad_last_error(void) { return g_err; }
 const char* glad_version(void) { return "glad 0.1.0 sm_100a"; }
 
 void glad_debug_set_trace(void* device_buf) { g_trace = static_cast<uint64_t*>(device_buf); }
+
+void glad_debug_set_phase_mask(int32_t mask) { g_phase_mask = mask & 7; }
 
 size_t glad_pool_bytes(const glad_cache_layout* L) {
   if (check_layout(L) != GLAD_OK) return 0;
@@ -260,42 +283,38 @@ glad_status glad_paged_gather(const glad_cache_layout* L, const void* pool, cons
   return GLAD_OK;
 }
 
-size_t glad_decode_workspace_bytes(int32_t B, int32_t Lq, int32_t H, int32_t d_v, int32_t max_splits) {
-  if (B <= 0 || Lq <= 0 || H <= 0 || d_v <= 0) return 0;
-  return ws_bytes_for(static_cast<int64_t>(B) * Lq * H, d_v, max_splits);
-}
-
-int32_t glad_decode_num_splits(const glad_cache_layout* L, int32_t B, int32_t Lq, int32_t H, int32_t bt_stride,
-                               int32_t variant) {
+size_t glad_decode_workspace_bytes(const glad_cache_layout* L, int32_t B, int32_t Lq, int32_t H, int32_t variant,
+                                   int32_t num_ctas) {
   DecodeGeom g;
   Variant v = variant == GLAD_GTA ? kGTA : variant == GLAD_MLA ? kMLA : kGLA;
-  if (decode_geom(v, L, Lq, H, &g) != GLAD_OK || B <= 0 || bt_stride <= 0) return -1;
-  return plan_splits(static_cast<int64_t>(B) * L->n_heads_kv * g.n_qblk,
-                     static_cast<int64_t>(bt_stride) * L->page_size);
+  if (B <= 0 || decode_geom(v, L, Lq, H, &g) != GLAD_OK) return 0;
+  const int64_t U = static_cast<int64_t>(B) * L->n_heads_kv * g.n_qblk;
+  const int G = num_ctas > 0 ? num_ctas : num_sms();
+  return ws_layout(U, G, g.key.nq, L->d_head).total;
 }
 
 glad_status glad_gla_decode(const void* q, const void* pool, const glad_cache_layout* layout,
                             const int32_t* block_table, int32_t bt_stride, const int32_t* seqlens, int32_t B,
                             int32_t Lq, int32_t H, float softmax_scale, int32_t causal, void* out, float* lse,
-                            void* workspace, size_t ws_bytes, int32_t num_splits, void* stream) {
+                            void* workspace, size_t ws_bytes, int32_t num_ctas, void* stream) {
   return decode_common(kGLA, q, pool, layout, block_table, bt_stride, seqlens, B, Lq, H, softmax_scale, causal, out,
-                       lse, workspace, ws_bytes, num_splits, stream);
+                       lse, workspace, ws_bytes, num_ctas, stream);
 }
 
 glad_status glad_mla_decode(const void* q, const void* pool, const glad_cache_layout* layout,
                             const int32_t* block_table, int32_t bt_stride, const int32_t* seqlens, int32_t B,
                             int32_t Lq, int32_t H, float softmax_scale, int32_t causal, void* out, float* lse,
-                            void* workspace, size_t ws_bytes, int32_t num_splits, void* stream) {
+                            void* workspace, size_t ws_bytes, int32_t num_ctas, void* stream) {
   return decode_common(kMLA, q, pool, layout, block_table, bt_stride, seqlens, B, Lq, H, softmax_scale, causal, out,
-                       lse, workspace, ws_bytes, num_splits, stream);
+                       lse, workspace, ws_bytes, num_ctas, stream);
 }
 
 glad_status glad_gta_decode(const void* q, const void* pool, const glad_cache_layout* layout,
                             const int32_t* block_table, int32_t bt_stride, const int32_t* seqlens, int32_t B,
                             int32_t Lq, int32_t H, float softmax_scale, int32_t causal, void* out, float* lse,
-                            void* workspace, size_t ws_bytes, int32_t num_splits, void* stream) {
+                            void* workspace, size_t ws_bytes, int32_t num_ctas, void* stream) {
   return decode_common(kGTA, q, pool, layout, block_table, bt_stride, seqlens, B, Lq, H, softmax_scale, causal, out,
-                       lse, workspace, ws_bytes, num_splits, stream);
+                       lse, workspace, ws_bytes, num_ctas, stream);
 }
 
 glad_status glad_splitkv_combine(const float* o_part, const float* lse_part, int32_t S, int32_t B, int32_t Lq,

@@ -7,27 +7,34 @@
 // token's single decoupled RoPE key.  GTA: K_nope = first half of
 // the tied state, V = the full tied state, k_rope = the single K_RoPE head.
 //
-// B200 design ("swap-AB"):
-//  * tokens sit on the UMMA M axis (M = 128 = one tile of T tokens), the
-//    g_q*Lq query rows that share the latent head sit on N (16/32/64).  This
-//    keeps every tcgen05.mma at the full-rate M = 128 shape even for g_q = 8.
+// B200 design:
+//  * "swap-AB": tokens sit on the UMMA M axis (M = 128 = one tile of T
+//    tokens), the g_q*Lq query rows that share the latent head sit on N
+//    (16/32/64), so every tcgen05.mma is the full-rate M = 128 shape even for
+//    g_q = 8.
 //  * S^T[T x NQ] = K_tile . Q^T    (A = KV tile, K-major SW128, straight from
 //    the TMA-staged paged rows; B = Q, K-major SW128) -> TMEM, double-buffered.
 //  * O^T[D_V x NQ] += V^T . P^T    (A = the SAME smem KV tile read MN-major:
 //    the latent is loaded once and reused as K and V; B = P^T bf16,
-//    MN-major no-swizzle, written by the softmax warps) -> TMEM accumulator.
+//    MN-major no-swizzle, written by the softmax warps into the tile's RoPE
+//    chunk, which is dead once QK is done) -> TMEM accumulator (2 buffers).
 //  * Paged loads: one 2-D TMA box of [min(page,128) rows x 64 cols] per
-//    (page run, 64-column chunk); the row coordinate comes from the block
-//    table (int32, one lookup per page run; the TMA unit does the address
-//    generation that P:301-318 does with cooperative cp.async).
-//  * Warp roles (384 threads): w0 TMA producer, w1 UMMA issuer (one thread),
-//    w2-3 Q loader (+ TMEM alloc), w4-7 / w8-11 two softmax warpgroups, each
-//    owning half of the query columns for all 128 token lanes.
+//    (page run, 64-column chunk); the int32 row coordinate comes from the
+//    block table (the TMA unit does the per-row address generation that
+//    P:301-318 does with cooperative cp.async).
+//  * Persistent, tile-balanced ("stream-K") schedule: a plan kernel turns
+//    seqlens into per-unit tile prefix sums; CTA c walks the flattened tile
+//    range [c*per, (c+1)*per) across units (unit = (b, head, query block)).
+//    A unit finished inside one CTA is written directly; a unit cut by a
+//    range boundary leaves partials (o/l, lse) in workspace slot c + u and
+//    the combine kernel merges them (split-KV LSE merge).
+//  * Warp roles (384 threads): w0 TMA producer, w1 UMMA issuer (one thread,
+//    non-blocking scheduler), w2-3 Q loader (+ TMEM alloc), w4-7 / w8-11 two
+//    softmax warpgroups, each owning half of the query columns for all 128
+//    token lanes.
 //  * Online softmax with lazy rescaling: the running max only moves when a
 //    score exceeds it by > 2^8 (vote via barrier.red.or), so the cross-lane
 //    max reduction and the TMEM O rescale run on a handful of tiles per unit.
-//  * Split-KV: blockIdx.x = split; partial (o / l, lse) go to a workspace and
-//    glad_splitkv_combine merges them (LSE merge).
 #pragma once
 #include <cuda.h>
 #include <cuda_bf16.h>
@@ -40,23 +47,28 @@ struct DecodeParams {
   const __nv_bfloat16* q;   // [B, Lq, H, DQ]
   const int32_t* block_table;
   const int32_t* seqlens;
+  const int32_t* plan;      // [U + 1] exclusive prefix sum of tiles per unit (plan_kernel)
   __nv_bfloat16* out;       // [B, Lq, H, D_V]
   float* lse;               // [B, Lq, H]
-  float* o_part;            // [S, B, Lq, H, D_V]
-  float* lse_part;          // [S, B, Lq, H]
+  float* o_part;            // [G + U][NQ][D_V] partials of split units
+  float* lse_part;          // [G + U][NQ]
   int32_t bt_stride;
   int32_t B, Lq, H, g_q;
+  int32_t n_heads_kv;       // heads (latent / tied) in the cache
   int32_t d_head;           // column offset between heads in a cache row
   int32_t rope_col;         // column of the RoPE part in a cache row
   int32_t page_size, log2_page, box_rows;
-  int32_t num_splits, n_qblk;
+  int32_t n_qblk, n_units;  // query blocks per head, U = n_heads_kv * B * n_qblk (head-major)
   int32_t causal;
+  int32_t q_tma;            // 1: Q via the 3-D tensor map (box (64, q_box_h, q_box_t)); 0: cp.async
+  int32_t q_box_h, q_box_t;
   float scale_log2;         // softmax_scale * log2(e)
   uint64_t* trace;          // debug timeline (nullptr = off): [cta][kTraceStride]
 };
-// Debug timeline layout per CTA (globaltimer ns): [0] start, [1] Q ready (MMA),
-// [2] end, then per tile i < kTraceTiles: [8+5i] load issued, [9+5i] QK issued,
-// [10+5i] S seen by softmax, [11+5i] P written, [12+5i] PV issued.
+// Debug timeline layout per CTA (globaltimer ns): [0] start, [1] first QK,
+// [2] end, [3] number of segments, then per tile i < kTraceTiles: [8+5i] load
+// issued, [9+5i] QK issued, [10+5i] S seen by softmax, [11+5i] P written,
+// [12+5i] PV issued.
 constexpr int kTraceTiles = 64;
 constexpr int kTraceStride = 8 + 5 * kTraceTiles;
 
@@ -65,7 +77,7 @@ struct DecodeCfg {
   static constexpr int D_V = D_V_;    // value width (= state width)
   static constexpr int D_KN = D_KN_;  // key part taken from the state
   static constexpr int D_R = D_R_;    // rope width
-  static constexpr int NQ = NQ_;      // query rows per CTA (UMMA N)
+  static constexpr int NQ = NQ_;      // query rows per unit (UMMA N)
   static constexpr int T = 128;       // tokens per tile (UMMA M)
   static constexpr int DQ = D_KN + D_R;
   static constexpr int NCH_V = D_V / 64;
@@ -84,15 +96,20 @@ struct DecodeCfg {
   static constexpr int NBLK_O = D_V / 128;
   static constexpr int NWG = 2;
   static constexpr int CW = NQ / NWG;
-  static constexpr int AUX = 3072;
+  static constexpr int MAXSEG = 128;  // per-CTA segment table entries (aux + 3072)
+  static constexpr int AUX = 3072 + MAXSEG * 16;
   static constexpr int AVAIL = 227 * 1024 - 1024 - AUX;
   static constexpr int NS_RAW = (AVAIL - QBYTES) / STAGE;
   static constexpr int NS = NS_RAW > 4 ? 4 : NS_RAW;
+  // a second Q buffer (next unit's Q prefetched while this one runs) when it
+  // costs no KV stage
+  static constexpr int NQB = ((AVAIL - 2 * QBYTES) / STAGE >= NS) ? 2 : 1;
   static constexpr int OFF_Q = NS * STAGE;
-  static constexpr int OFF_AUX = OFF_Q + QBYTES;
+  static constexpr int OFF_AUX = OFF_Q + NQB * QBYTES;
   static constexpr int SMEM_BYTES = 1024 + OFF_AUX + AUX;
-  static constexpr int TMEM_O = 2 * NQ;
-  static constexpr int TMEM_USED = 2 * NQ + NBLK_O * NQ;
+  static constexpr int OCOLS = NBLK_O * NQ;      // one O^T accumulator
+  static constexpr int TMEM_O = 2 * NQ;          // after the two S^T buffers
+  static constexpr int TMEM_USED = 2 * NQ + 2 * OCOLS;
   static constexpr int TMEM_COLS =
       TMEM_USED <= 32 ? 32 : TMEM_USED <= 64 ? 64 : TMEM_USED <= 128 ? 128 : TMEM_USED <= 256 ? 256 : 512;
   static constexpr int NTHREADS = 384;
@@ -156,9 +173,69 @@ __device__ __forceinline__ void tmem_store_cols(uint32_t taddr, const float (&x)
   }
 }
 
+// One unit u = ((head * B) + b) * n_qblk + qb (head-major, so the RoPE rows a
+// sequence's heads share are read by concurrently running CTAs and hit L2)
+// and the part of its
+// tile range [t0, t1) that falls in this CTA's flattened range.
+struct Seg {
+  int u, b, head, qb;
+  int n0, nq;      // query rows [n0, n0 + nq) of the head's Lq*g_q rows
+  int L, kv_end;   // keys visible to the block's last query
+  int t0, t1;      // tile range within the unit
+  bool whole;      // unit entirely inside this CTA -> write final output
+};
+
+template <int NQ>
+__device__ __forceinline__ Seg make_seg(const DecodeParams& p, int u, int cta_t0, int cta_t1) {
+  Seg s;
+  s.u = u;
+  s.qb = u % p.n_qblk;
+  const int hb = u / p.n_qblk;  // head-major: CTAs in different head ranges stream the same b together
+  s.b = hb % p.B;
+  s.head = hb / p.B;
+  const int nq_total = p.Lq * p.g_q;
+  s.n0 = s.qb * NQ;
+  s.nq = min(NQ, nq_total - s.n0);
+  s.L = __ldg(p.seqlens + s.b);
+  s.kv_end = s.L;
+  if (p.causal) {
+    const int t_last = (s.n0 + s.nq - 1) / p.g_q;
+    s.kv_end = max(0, min(s.L, s.L - p.Lq + t_last + 1));
+  }
+  const int pu0 = __ldg(p.plan + u), pu1 = __ldg(p.plan + u + 1);
+  s.t0 = max(cta_t0, pu0) - pu0;
+  s.t1 = min(cta_t1, pu1) - pu0;
+  s.whole = (s.t0 == 0 && s.t1 == pu1 - pu0);
+  return s;
+}
+
+// Segment from a table entry (u, t0, t1, L) without global loads.
+template <int NQ>
+__device__ __forceinline__ Seg seg_from_entry(const DecodeParams& p, int4 e) {
+  Seg s;
+  s.u = e.x;
+  s.qb = s.u % p.n_qblk;
+  const int hb = s.u / p.n_qblk;
+  s.b = hb % p.B;
+  s.head = hb / p.B;
+  s.n0 = s.qb * NQ;
+  s.nq = min(NQ, p.Lq * p.g_q - s.n0);
+  s.L = e.w & 0x3FFFFFFF;
+  s.kv_end = s.L;
+  if (p.causal) {
+    const int t_last = (s.n0 + s.nq - 1) / p.g_q;
+    s.kv_end = max(0, min(s.L, s.L - p.Lq + t_last + 1));
+  }
+  s.t0 = e.y;
+  s.t1 = e.z;
+  s.whole = (e.w >> 30) & 1;
+  return s;
+}
+
 template <class C>
 __global__ void __launch_bounds__(C::NTHREADS, 1)
-    decode_kernel(const __grid_constant__ CUtensorMap tmap, const DecodeParams p) {
+    decode_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUtensorMap qmap,
+                  const DecodeParams p) {
   constexpr int T = C::T, NQ = C::NQ, CW = C::CW, NS = C::NS;
   constexpr float TAU = 8.0f;  // lazy-rescale threshold (log2 units)
   extern __shared__ uint8_t smem_raw[];
@@ -172,8 +249,12 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
   uint64_t* s_empty = bars + 10;   // [2] softmax read S -> MMA
   uint64_t* p_full = bars + 12;    // [4] P^T written (per stage) -> MMA
   uint64_t* pv_done = bars + 16;   // [4] PV(j) complete, j % 4 (O rescale / epilogue)
-  uint64_t* q_full = bars + 20;
+  uint64_t* q_full = bars + 20;    // [2] Q buffer (s % NQB) of segment s loaded (64 arrivals)
+  uint64_t* q_empty = bars + 22;   // [2] last QK of segment s done: Q buffer (s % NQB) free
+  uint64_t* o_empty = bars + 24;   // [2] epilogue read O buffer (s & 1) (8 arrivals)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(aux + 256);
+  int* range_s = reinterpret_cast<int*>(aux + 264);        // [4] cta tile range, #segments, overflow unit
+  int4* segtab = reinterpret_cast<int4*>(aux + 3072);      // [MAXSEG] (u, t0, t1, L | whole << 30)
   int* vend_s = reinterpret_cast<int*>(aux + 320);         // [NQ] visible-key end per query column
   float* m_run = reinterpret_cast<float*>(aux + 640);      // [NQ] running max (log2 units)
   float* thr_s = reinterpret_cast<float*>(aux + 896);      // [NQ] rescale trigger in raw score units
@@ -181,117 +262,171 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
   float* alpha_s = reinterpret_cast<float*>(aux + 2304);   // [NQ] rescale factors / 1/l
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int b = blockIdx.z;
-  const int head = blockIdx.y / p.n_qblk;
-  const int qb = blockIdx.y - head * p.n_qblk;
-  const int split = blockIdx.x;
-  const int L = p.seqlens[b];
-  const int nq_total = p.Lq * p.g_q;
-  const int n0 = qb * NQ;
-  const int nq = min(NQ, nq_total - n0);
-  int kv_end = L;
-  if (p.causal) {
-    const int t_last = (n0 + nq - 1) / p.g_q;
-    kv_end = max(0, min(L, L - p.Lq + t_last + 1));
-  }
-  const int ntiles_all = (kv_end + T - 1) / T;
-  const int per = (ntiles_all + p.num_splits - 1) / p.num_splits;
-  const int tile_begin = split * per;
-  const int ntiles = max(0, min(ntiles_all, tile_begin + per) - tile_begin);
-  const size_t n_rows_total = static_cast<size_t>(p.B) * p.Lq * p.H;
-
-  if (ntiles == 0) {  // nothing visible in this split: empty partial / empty output
-    for (int idx = threadIdx.x; idx < nq * C::D_V; idx += blockDim.x) {
-      const int n = idx / C::D_V, d = idx - n * C::D_V;
-      const int ng = n0 + n, t = ng / p.g_q, h = head * p.g_q + (ng - t * p.g_q);
-      const size_t row = (static_cast<size_t>(b) * p.Lq + t) * p.H + h;
-      if (p.num_splits == 1) {
-        p.out[row * C::D_V + d] = __float2bfloat16(0.f);
-        if (d == 0) p.lse[row] = -INFINITY;
-      } else if (d == 0) {
-        p.lse_part[split * n_rows_total + row] = -INFINITY;  // o_part never read for an empty split
-      }
-    }
-    return;
-  }
+  const int cta = blockIdx.x;
 
   // ------------------------------------------------------------- setup
+  if (warp == 0) {
+    // Work range of this CTA and its segment table, with warp-parallel loads
+    // (a serial search over the plan would cost one L2 round trip per step).
+    const int U = p.n_units;
+    const int total = __ldg(p.plan + U);
+    const int per = (total + gridDim.x - 1) / gridDim.x;
+    const int t0 = min(total, cta * per), t1 = min(total, t0 + per);
+    int lo = 0, hi = U - 1;  // last unit with plan[u] <= t0 (plan[0] = 0)
+    while (lo < hi) {
+      const int step = (hi - lo + 32) / 32;
+      const int idx = lo + lane * step;
+      const bool ok = idx <= hi && __ldg(p.plan + idx) <= t0;
+      const unsigned m = __ballot_sync(0xffffffffu, ok);
+      const int k = 31 - __clz(m);
+      lo = lo + k * step;
+      hi = min(hi, lo + step - 1);
+    }
+    int nseg = 0, more = -1;
+    if (t0 < t1) {
+      for (int base = lo;; base += 32) {
+        const int u = base + lane;
+        int pu0 = t1, pu1 = t1;
+        if (u < U) { pu0 = __ldg(p.plan + u); pu1 = __ldg(p.plan + u + 1); }
+        const bool in = u < U && pu0 < t1;
+        const int st0 = max(t0, pu0) - pu0, st1 = min(t1, pu1) - pu0;
+        const bool has = in && st1 > st0;
+        int L = 0;
+        if (has) L = __ldg(p.seqlens + (u / p.n_qblk) % p.B);
+        const unsigned hm = __ballot_sync(0xffffffffu, has);
+        const int pos = nseg + __popc(hm & ((1u << lane) - 1));
+        const int whole = (st0 == 0 && st1 == pu1 - pu0) ? 1 : 0;
+        if (has && pos < C::MAXSEG) segtab[pos] = make_int4(u, st0, st1, L | (whole << 30));
+        const int cnt = __popc(hm);
+        if (nseg + cnt > C::MAXSEG) {  // table full: the rest is walked on the fly
+          const unsigned keep = C::MAXSEG - nseg;
+          // first unit not stored: the (keep)-th set bit of hm
+          unsigned mm = hm;
+          for (unsigned i = 0; i < keep; ++i) mm &= mm - 1;
+          more = base + __ffs(mm) - 1;
+          nseg = C::MAXSEG;
+          break;
+        }
+        nseg += cnt;
+        if (__ballot_sync(0xffffffffu, !in) != 0u) break;  // reached the end of the range
+      }
+    }
+    if (lane == 0) {
+      range_s[0] = t0;
+      range_s[1] = t1;
+      range_s[2] = nseg;
+      range_s[3] = more;
+    }
+  }
   if (threadIdx.x == 0) {
     for (int i = 0; i < NS; ++i) {
       mbar_init(&kv_full[i], 1);
       mbar_init(&kv_empty[i], 1);
       mbar_init(&p_full[i], 8);
     }
-    for (int i = 0; i < 2; ++i) { mbar_init(&s_full[i], 1); mbar_init(&s_empty[i], 8); }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&s_full[i], 1);
+      mbar_init(&s_empty[i], 8);
+      mbar_init(&o_empty[i], 8);
+    }
     for (int i = 0; i < 4; ++i) mbar_init(&pv_done[i], 1);
-    mbar_init(q_full, 64);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&q_full[i], p.q_tma ? 1 : 64);
+      mbar_init(&q_empty[i], 1);
+    }
     fence_barrier_init();
     tma_prefetch_desc(&tmap);
-  }
-  if (threadIdx.x < NQ) {
-    const int n = threadIdx.x;
-    int ve = 0;
-    if (n < nq) {
-      const int t = (n0 + n) / p.g_q;
-      ve = p.causal ? max(0, min(L, L - p.Lq + t + 1)) : L;
-    }
-    vend_s[n] = ve;
-    m_run[n] = -INFINITY;
-    thr_s[n] = -INFINITY;
+    if (p.q_tma) tma_prefetch_desc(&qmap);
   }
   if (warp == 2) { tmem_alloc(tmem_slot, C::TMEM_COLS); tmem_relinquish(); }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  uint64_t* trace = p.trace ? p.trace + static_cast<size_t>((blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x +
-                                                             blockIdx.x) * kTraceStride
-                            : nullptr;
+  const int cta_t0 = range_s[0], cta_t1 = range_s[1], nseg_tab = range_s[2], u_more = range_s[3];
+  uint64_t* trace = p.trace ? p.trace + static_cast<size_t>(cta) * kTraceStride : nullptr;
   if (trace && threadIdx.x == 0) trace[0] = globaltimer();
+
+  // All roles walk the same sequence of segments: entries of the table,
+  // then (only if it overflowed) units walked on the fly from u_more.
+  // `k` counts segments, `u` is the on-the-fly cursor.
+  auto next_seg = [&](int& k, int& u, Seg& s) -> bool {
+    if (k < nseg_tab) {
+      s = seg_from_entry<NQ>(p, segtab[k++]);
+      return true;
+    }
+    if (u_more < 0) return false;
+    if (k == nseg_tab && u < u_more) u = u_more;
+    for (;; ++u) {
+      if (u >= p.n_units) return false;
+      if (__ldg(p.plan + u) >= cta_t1) return false;
+      s = make_seg<NQ>(p, u, cta_t0, cta_t1);
+      if (s.t1 > s.t0) { ++u; ++k; return true; }
+    }
+  };
 
   if (warp == 0) {
     // ========================= TMA producer (all 32 lanes issue) =========================
-    named_bar_sync(3, 96);  // Q loads are issued first: the first QK needs Q, not a second tile
-    const int* bt_row = p.block_table + static_cast<size_t>(b) * p.bt_stride;
-    const int box_rows = p.box_rows;
-    for (int it = 0; it < ntiles; ++it) {
-      const int stage = it % NS;
-      mbar_wait(&kv_empty[stage], ((it / NS) & 1) ^ 1);
-      const int p0 = (tile_begin + it) * T;
-      const int ntok = min(T, kv_end - p0);
-      const int nbox = (ntok + box_rows - 1) / box_rows;
-      if (lane == 0) mbar_arrive_expect_tx(&kv_full[stage], static_cast<uint32_t>(nbox * C::NCH * box_rows * 128));
-      __syncwarp();
-      for (int bx = lane; bx < nbox * C::NCH; bx += 32) {
-        const int box = bx / C::NCH, ch = bx - box * C::NCH;
-        const int pos = p0 + box * box_rows;
-        const int page = __ldg(bt_row + (pos >> p.log2_page));
-        const int row = page * p.page_size + (pos & (p.page_size - 1));
-        const int col = ch < C::NCH_V ? head * p.d_head + ch * 64 : p.rope_col;
-        const uint32_t dst = sbase + stage * C::STAGE + ch * C::CHUNK + box * box_rows * 128;
-        tma_load_2d(dst, &tmap, &kv_full[stage], col, row);
+    named_bar_sync(3, 96);  // the first Q load is issued first: QK needs Q, not a second tile
+    int k = 0, u = 0, it = 0;
+    Seg s;
+    while (next_seg(k, u, s)) {
+      const int* bt_row = p.block_table + static_cast<size_t>(s.b) * p.bt_stride;
+      const int box_rows = p.box_rows;
+      for (int tl = s.t0; tl < s.t1; ++tl, ++it) {
+        const int stage = it % NS;
+        const int p0 = tl * T;
+        const int ntok = min(T, s.kv_end - p0);
+        const int nbox = (ntok + box_rows - 1) / box_rows;
+        // block-table lookup for this lane's first box before the stage wait
+        int page0 = 0;
+        if (lane < nbox * C::NCH) page0 = __ldg(bt_row + ((p0 + (lane / C::NCH) * box_rows) >> p.log2_page));
+        mbar_wait(&kv_empty[stage], ((it / NS) & 1) ^ 1);
+        if (lane == 0)
+          mbar_arrive_expect_tx(&kv_full[stage], static_cast<uint32_t>(nbox * C::NCH * box_rows * 128));
+        __syncwarp();
+        for (int bx = lane; bx < nbox * C::NCH; bx += 32) {
+          const int box = bx / C::NCH, ch = bx - box * C::NCH;
+          const int pos = p0 + box * box_rows;
+          const int page = bx == lane ? page0 : __ldg(bt_row + (pos >> p.log2_page));
+          const int row = page * p.page_size + (pos & (p.page_size - 1));
+          const int col = ch < C::NCH_V ? s.head * p.d_head + ch * 64 : p.rope_col;
+          const uint32_t dst = sbase + stage * C::STAGE + ch * C::CHUNK + box * box_rows * 128;
+          tma_load_2d(dst, &tmap, &kv_full[stage], col, row);
+        }
+        if (trace && lane == 0 && it < kTraceTiles) trace[8 + 5 * it] = globaltimer();
       }
-      if (trace && lane == 0 && it < kTraceTiles) trace[8 + 5 * it] = globaltimer();
     }
   } else if (warp == 1) {
     // ========================= UMMA issuer (one thread) =========================
     if (lane == 0) {
-      mbar_wait(q_full, 0);
-      tc_fence_after();
-      if (trace) trace[1] = globaltimer();
       constexpr uint32_t idesc_qk = make_idesc_bf16(128, NQ, false, false);
       constexpr uint32_t idesc_pv = make_idesc_bf16(128, NQ, true, true);
-      const uint32_t q_base = sbase + C::OFF_Q;
-      // QK(i) needs tile i in smem and a free S buffer; PV(j) needs P(j).
-      // Poll both and issue whichever is ready, so PV never queues behind
-      // a QK that is still waiting for its TMA load (that would serialise
-      // the load latency with the stage release).
-      auto issue_qk = [&](int it) {
-        const int stage = it % NS;
-        const int sb = it & 1;
+      // The QK stream and the PV stream walk the CTA's tiles with separate
+      // cursors (segment, tile within unit).
+      struct Cursor {
+        int k, u, seg, tl, t1, t0;
+      };
+      Cursor cq{0, 0, -1, 0, 0, 0}, cp{0, 0, -1, 0, 0, 0};
+      auto advance = [&](Cursor& c) -> bool {  // move to the next tile; false when done
+        if (c.seg >= 0 && c.tl + 1 < c.t1) { ++c.tl; return true; }
+        Seg s;
+        if (!next_seg(c.k, c.u, s)) return false;
+        ++c.seg;
+        c.tl = s.t0;
+        c.t0 = s.t0;
+        c.t1 = s.t1;
+        return true;
+      };
+      bool qk_left = advance(cq), pv_left = advance(cp);
+      int next_qk = 0, next_pv = 0;
+      auto issue_qk = [&]() {
+        const int stage = next_qk % NS;
+        const int sb = next_qk & 1;
         tc_fence_after();
         const uint32_t d = tmem + sb * NQ;
         const uint32_t kv = sbase + stage * C::STAGE;
+        const uint32_t q_base = sbase + C::OFF_Q + (cq.seg % C::NQB) * C::QBYTES;
 #pragma unroll
         for (int c = 0; c < C::NCH_QK; ++c) {
 #pragma unroll
@@ -304,67 +439,110 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
           umma_f16_ss(d, desc_kmajor_sw128(kv + C::NCH_V * C::CHUNK + k * 32),
                       desc_kmajor_sw128(q_base + C::NCH_QK * C::QCHUNK + k * 32), idesc_qk, 1u);
         umma_commit(&s_full[sb]);
+        if (cq.tl + 1 == cq.t1) umma_commit(&q_empty[cq.seg % C::NQB]);  // last QK of the segment: Q free
       };
-      auto issue_pv = [&](int j) {
+      auto issue_pv = [&]() {
         tc_fence_after();
+        const int j = next_pv;
         const int stage = j % NS;
         const uint32_t kv = sbase + stage * C::STAGE;
         const uint32_t pt = kv + C::NCH_V * C::CHUNK;
+        const uint32_t obuf = tmem + C::TMEM_O + (cp.seg & 1) * C::OCOLS;
+        const bool first = (cp.tl == cp.t0);
 #pragma unroll
         for (int blk = 0; blk < C::NBLK_O; ++blk) {
 #pragma unroll
           for (int k = 0; k < T / 16; ++k)
-            umma_f16_ss(tmem + C::TMEM_O + blk * NQ, desc_mnmajor_sw128(kv + 2 * blk * C::CHUNK + k * 2048, C::CHUNK),
-                        desc_mnmajor_noswz(pt + k * 256, 128, 2048), idesc_pv, (j > 0 || k > 0) ? 1u : 0u);
+            umma_f16_ss(obuf + blk * NQ, desc_mnmajor_sw128(kv + 2 * blk * C::CHUNK + k * 2048, C::CHUNK),
+                        desc_mnmajor_noswz(pt + k * 256, 128, 2048), idesc_pv, (!first || k > 0) ? 1u : 0u);
         }
         umma_commit(&kv_empty[stage]);
         umma_commit(&pv_done[j & 3]);
       };
-      int next_qk = 0, next_pv = 0;
       long long t0 = clock64();
-      while (next_pv < ntiles) {
-        if (next_pv < next_qk &&
-            mbar_test_wait(smem_u32(&p_full[next_pv % NS]), (next_pv / NS) & 1)) {
-          if (trace && next_pv < kTraceTiles) trace[12 + 5 * next_pv] = globaltimer();
-          issue_pv(next_pv++);
-          t0 = clock64();
-        } else if (next_qk < ntiles && next_qk < next_pv + 2 &&
-                   mbar_test_wait(smem_u32(&kv_full[next_qk % NS]), (next_qk / NS) & 1) &&
-                   mbar_test_wait(smem_u32(&s_empty[next_qk & 1]), ((next_qk >> 1) & 1) ^ 1)) {
-          if (trace && next_qk < kTraceTiles) trace[9 + 5 * next_qk] = globaltimer();
-          issue_qk(next_qk++);
+      while (pv_left) {
+        bool did = false;
+        if (next_pv < next_qk && mbar_test_wait(smem_u32(&p_full[next_pv % NS]), (next_pv / NS) & 1)) {
+          // first PV of a segment reuses O buffer (seg & 1): its epilogue two segments ago must be done
+          const bool first = (cp.tl == cp.t0);
+          if (!first || cp.seg < 2 || mbar_test_wait(smem_u32(&o_empty[cp.seg & 1]), ((cp.seg - 2) >> 1) & 1)) {
+            if (trace && next_pv < kTraceTiles) trace[12 + 5 * next_pv] = globaltimer();
+            issue_pv();
+            ++next_pv;
+            pv_left = advance(cp);
+            did = true;
+          }
+        }
+        if (!did && qk_left && next_qk < next_pv + 2 &&
+            mbar_test_wait(smem_u32(&kv_full[next_qk % NS]), (next_qk / NS) & 1) &&
+            mbar_test_wait(smem_u32(&s_empty[next_qk & 1]), ((next_qk >> 1) & 1) ^ 1)) {
+          const bool first = (cq.tl == cq.t0);
+          if (!first || mbar_test_wait(smem_u32(&q_full[cq.seg % C::NQB]), (cq.seg / C::NQB) & 1)) {
+            if (trace && next_qk == 0) trace[1] = globaltimer();
+            if (trace && next_qk < kTraceTiles) trace[9 + 5 * next_qk] = globaltimer();
+            issue_qk();
+            ++next_qk;
+            qk_left = advance(cq);
+            did = true;
+          }
+        }
+        if (did) {
           t0 = clock64();
         } else if (clock64() - t0 > (1ll << 34)) {
-          printf("glad: MMA scheduler watchdog (block %d,%d,%d qk %d pv %d)\n", blockIdx.x, blockIdx.y,
-                 blockIdx.z, next_qk, next_pv);
+          printf("glad: MMA scheduler watchdog (cta %d qk %d pv %d)\n", cta, next_qk, next_pv);
           __trap();
         }
       }
+      if (trace) trace[3] = cp.seg + 1;
     }
   } else if (warp < 4) {
-    // ========================= Q loader (64 threads, cp.async) =========================
+    // ========================= Q loader: TMA (one thread) or cp.async (64 threads) =========================
     const int tid = threadIdx.x - 64;
-    for (int idx = tid; idx < NQ * C::NQCH * 8; idx += 64) {
-      const int n = idx / (C::NQCH * 8);
-      const int u = idx - n * (C::NQCH * 8);
-      const int ch = u >> 3, w = u & 7;
-      const void* src = p.q;
-      uint32_t bytes = 0;
-      if (n < nq) {
-        const bool rope = ch >= C::NCH_QK;
-        const int col = rope ? C::D_KN + w * 8 : ch * 64 + w * 8;
-        if (!rope || w * 8 < C::D_R) {
-          const int ng = n0 + n, t = ng / p.g_q, h = head * p.g_q + (ng - t * p.g_q);
-          src = p.q + ((static_cast<size_t>(b) * p.Lq + t) * p.H + h) * C::DQ + col;
-          bytes = 16;
+    int k = 0, u = 0, seg = 0;
+    Seg s;
+    while (next_seg(k, u, s)) {
+      const int qbuf = seg % C::NQB;
+      if (seg >= C::NQB) mbar_wait(&q_empty[qbuf], ((seg - C::NQB) / C::NQB) & 1);
+      const uint32_t qdst = sbase + C::OFF_Q + qbuf * C::QBYTES;
+      if (p.q_tma) {
+        if (tid == 0) {
+          mbar_arrive_expect_tx(&q_full[qbuf], static_cast<uint32_t>(C::QBYTES));
+          // rows n0.. of head s.head: (t, j) = divmod(n, g_q)
+          const int c1 = s.head * p.g_q + (p.q_box_t == 1 ? s.n0 % p.g_q : 0);
+          const int c2 = s.b * p.Lq + s.n0 / p.g_q;
+#pragma unroll
+          for (int ch = 0; ch < C::NQCH; ++ch) {
+            const int col = ch < C::NCH_QK ? ch * 64 : C::D_KN;
+            tma_load_3d(qdst + ch * C::QCHUNK, &qmap, &q_full[qbuf], col, c1, c2);
+          }
         }
+        if (seg == 0) { __syncwarp(); named_bar_arrive(3, 96); }
+      } else {
+        for (int idx = tid; idx < NQ * C::NQCH * 8; idx += 64) {
+          const int n = idx / (C::NQCH * 8);
+          const int uu = idx - n * (C::NQCH * 8);
+          const int ch = uu >> 3, w = uu & 7;
+          const void* src = p.q;
+          uint32_t bytes = 0;
+          if (n < s.nq) {
+            const bool rope = ch >= C::NCH_QK;
+            const int col = rope ? C::D_KN + w * 8 : ch * 64 + w * 8;
+            if (!rope || w * 8 < C::D_R) {
+              const int ng = s.n0 + n, t = ng / p.g_q, h = s.head * p.g_q + (ng - t * p.g_q);
+              src = p.q + ((static_cast<size_t>(s.b) * p.Lq + t) * p.H + h) * C::DQ + col;
+              bytes = 16;
+            }
+          }
+          cp_async16(qdst + ch * C::QCHUNK + n * 128 + ((w ^ (n & 7)) << 4), src, bytes);
+        }
+        if (seg == 0) named_bar_arrive(3, 96);
+        cp_async_wait_all();
+        fence_proxy_async_smem();
+        mbar_arrive(&q_full[qbuf]);
       }
-      cp_async16(sbase + C::OFF_Q + ch * C::QCHUNK + n * 128 + ((w ^ (n & 7)) << 4), src, bytes);
+      ++seg;
     }
-    named_bar_arrive(3, 96);
-    cp_async_wait_all();
-    fence_proxy_async_smem();
-    mbar_arrive(q_full);
+    if (seg == 0) named_bar_arrive(3, 96);  // no work: release the producer
   } else {
     // ========================= softmax / correction / epilogue =========================
     const int wg = (warp - 4) >> 2;
@@ -378,163 +556,192 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
     const uint32_t a_addr = smem_u32(alpha_s + c0);
     const float sl2 = p.scale_log2;
     const float inv_sl2 = 1.f / sl2;
-    int min_vend = 1 << 30;
-    for (int n = 0; n < nq; ++n) min_vend = min(min_vend, vend_s[n]);
-    float l[CW];
-#pragma unroll
-    for (int n = 0; n < CW; ++n) l[n] = 0.f;
-
-    for (int it = 0; it < ntiles; ++it) {
-      const int sb = it & 1;
-      mbar_wait(&s_full[sb], (it >> 1) & 1);
-      tc_fence_after();
-      if (trace && threadIdx.x == 128 && it < kTraceTiles) trace[10 + 5 * it] = globaltimer();
-      float x[CW];  // raw scores q.k for this thread's token, this WG's query columns
-      tmem_load_cols<C>(tmem + lane_addr + sb * NQ + c0, x);
-      tmem_ld_wait();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&s_empty[sb]);
-
-      const int p0 = (tile_begin + it) * T;
-      const int tok = p0 + r;
-      if (!(p0 + T <= min_vend && nq == NQ)) {  // masked tile (last tile / causal / padded columns)
-#pragma unroll
-        for (int n = 0; n < CW; ++n) {
-          const bool ok = (c0 + n < nq) && tok < vend_s[c0 + n];
-          x[n] = ok ? x[n] : -INFINITY;
+    int k = 0, u = 0, seg = 0, it = 0;
+    Seg s;
+    while (next_seg(k, u, s)) {
+      // ---- segment setup: per-column visibility, running max reset
+      if (r < CW) {
+        const int n = c0 + r;
+        int ve = 0;
+        if (n < s.nq) {
+          const int t = (s.n0 + n) / p.g_q;
+          ve = p.causal ? max(0, min(s.L, s.L - p.Lq + t + 1)) : s.L;
         }
+        vend_s[n] = ve;
+        m_run[n] = -INFINITY;
+        thr_s[n] = -INFINITY;
       }
-      bool need = false;
+      named_bar_sync(bar_id, 128);
+      const int min_vend = p.causal ? max(0, min(s.L, s.L - p.Lq + s.n0 / p.g_q + 1)) : s.L;
+      const bool all_cols = (s.nq == NQ);
+      const uint32_t obuf = tmem + C::TMEM_O + (seg & 1) * C::OCOLS;
+      float l[CW];
 #pragma unroll
-      for (int n = 0; n < CW; n += 4) {
-        const float4 th = ld_shared_f4(t_addr + n * 4);
-        need |= (x[n] > th.x) | (x[n + 1] > th.y) | (x[n + 2] > th.z) | (x[n + 3] > th.w);
-      }
-      if (named_bar_red_or(bar_id, 128, need)) {
-        // the running max moves by > 2^TAU somewhere: column max over the WG,
-        // new m / alpha (rare after the first tile)
-        // (in halves of <= 16 columns to bound register pressure)
-        constexpr int HW = CW > 16 ? 16 : CW;
+      for (int n = 0; n < CW; ++n) l[n] = 0.f;
+
+      for (int tl = s.t0; tl < s.t1; ++tl, ++it) {
+        const int sb = it & 1;
+        mbar_wait(&s_full[sb], (it >> 1) & 1);
+        tc_fence_after();
+        if (trace && threadIdx.x == 128 && it < kTraceTiles) trace[10 + 5 * it] = globaltimer();
+        float x[CW];  // raw scores q.k for this thread's token, this WG's query columns
+        tmem_load_cols<C>(tmem + lane_addr + sb * NQ + c0, x);
+        tmem_ld_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&s_empty[sb]);
+
+        const int p0 = tl * T;
+        const int tok = p0 + r;
+        if (!(p0 + T <= min_vend && all_cols)) {  // masked tile (last tile / causal / padded columns)
 #pragma unroll
-        for (int h0 = 0; h0 < CW; h0 += HW) {
-          float tmp[HW];
-#pragma unroll
-          for (int n = 0; n < HW; ++n) tmp[n] = x[h0 + n];
-          const float cm = warp_col_reduce<HW, true>(tmp, lane);
-          if ((lane & ((1 << col_shift<HW>()) - 1)) == 0)
-            red[(wg * 4 + wq) * 32 + h0 + (lane >> col_shift<HW>())] = cm;
+          for (int n = 0; n < CW; ++n) {
+            const bool ok = (c0 + n < s.nq) && tok < vend_s[c0 + n];
+            x[n] = ok ? x[n] : -INFINITY;
+          }
         }
-        named_bar_sync(bar_id, 128);
-        if (r < CW) {
-          const float* rr = red + wg * 128 + r;
-          const float mt = fmaxf(fmaxf(rr[0], rr[32]), fmaxf(rr[64], rr[96])) * sl2;
-          const float mo = m_run[c0 + r];
-          const float mn = fmaxf(mo, mt);
-          alpha_s[c0 + r] = (mn == -INFINITY) ? 1.f : ex2(mo - mn);
-          m_run[c0 + r] = mn;
-          thr_s[c0 + r] = (mn == -INFINITY) ? -INFINITY : (mn + TAU) * inv_sl2;
-        }
-        named_bar_sync(bar_id, 128);
-        bool any_scale = false;
+        bool need = false;
 #pragma unroll
         for (int n = 0; n < CW; n += 4) {
-          const float4 a = ld_shared_f4(a_addr + n * 4);
-          l[n] *= a.x; l[n + 1] *= a.y; l[n + 2] *= a.z; l[n + 3] *= a.w;
-          any_scale |= (a.x != 1.f) | (a.y != 1.f) | (a.z != 1.f) | (a.w != 1.f);
+          const float4 th = ld_shared_f4(t_addr + n * 4);
+          need |= (x[n] > th.x) | (x[n + 1] > th.y) | (x[n + 2] > th.z) | (x[n + 3] > th.w);
         }
-        if (it > 0 && any_scale) {  // rescale this WG's O^T columns in TMEM
-          const int j = it - 1;
-          mbar_wait(&pv_done[j & 3], (j >> 2) & 1);
-          tc_fence_after();
+        if (named_bar_red_or(bar_id, 128, need)) {
+          // the running max moves by > 2^TAU somewhere: column max over the WG
+          // (in halves of <= 16 columns to bound register pressure)
+          constexpr int HW = CW > 16 ? 16 : CW;
 #pragma unroll
-          for (int blk = 0; blk < C::NBLK_O; ++blk) {
-            float o[CW];
-            const uint32_t ta = tmem + lane_addr + C::TMEM_O + blk * NQ + c0;
-            tmem_load_cols<C>(ta, o);
-            tmem_ld_wait();
+          for (int h0 = 0; h0 < CW; h0 += HW) {
+            float tmp[HW];
 #pragma unroll
-            for (int n = 0; n < CW; n += 4) {
-              const float4 a = ld_shared_f4(a_addr + n * 4);
-              o[n] *= a.x; o[n + 1] *= a.y; o[n + 2] *= a.z; o[n + 3] *= a.w;
-            }
-            tmem_store_cols<C>(ta, o);
+            for (int n = 0; n < HW; ++n) tmp[n] = x[h0 + n];
+            const float cm = warp_col_reduce<HW, true>(tmp, lane);
+            if ((lane & ((1 << col_shift<HW>()) - 1)) == 0)
+              red[(wg * 4 + wq) * 32 + h0 + (lane >> col_shift<HW>())] = cm;
           }
-          tmem_st_wait();
+          named_bar_sync(bar_id, 128);
+          if (r < CW) {
+            const float* rr = red + wg * 128 + r;
+            const float mt = fmaxf(fmaxf(rr[0], rr[32]), fmaxf(rr[64], rr[96])) * sl2;
+            const float mo = m_run[c0 + r];
+            const float mn = fmaxf(mo, mt);
+            alpha_s[c0 + r] = (mn == -INFINITY) ? 1.f : ex2(mo - mn);
+            m_run[c0 + r] = mn;
+            thr_s[c0 + r] = (mn == -INFINITY) ? -INFINITY : (mn + TAU) * inv_sl2;
+          }
+          named_bar_sync(bar_id, 128);
+          bool any_scale = false;
+#pragma unroll
+          for (int n = 0; n < CW; n += 4) {
+            const float4 a = ld_shared_f4(a_addr + n * 4);
+            l[n] *= a.x; l[n + 1] *= a.y; l[n + 2] *= a.z; l[n + 3] *= a.w;
+            any_scale |= (a.x != 1.f) | (a.y != 1.f) | (a.z != 1.f) | (a.w != 1.f);
+          }
+          if (tl > s.t0 && any_scale) {  // rescale this WG's O^T columns in TMEM
+            const int j = it - 1;
+            mbar_wait(&pv_done[j & 3], (j >> 2) & 1);
+            tc_fence_after();
+#pragma unroll
+            for (int blk = 0; blk < C::NBLK_O; ++blk) {
+              float o[CW];
+              const uint32_t ta = obuf + lane_addr + blk * NQ + c0;
+              tmem_load_cols<C>(ta, o);
+              tmem_ld_wait();
+#pragma unroll
+              for (int n = 0; n < CW; n += 4) {
+                const float4 a = ld_shared_f4(a_addr + n * 4);
+                o[n] *= a.x; o[n + 1] *= a.y; o[n + 2] *= a.z; o[n + 3] *= a.w;
+              }
+              tmem_store_cols<C>(ta, o);
+            }
+            tmem_st_wait();
+          }
         }
-      }
-      // p = 2^(s*c - m): bf16 P^T into the tile's (now dead) RoPE chunk,
-      // MN-major no-swizzle [NQ/8][128 tok][8]
-      const uint32_t stage_base = sbase + (it % NS) * C::STAGE;
-      const uint32_t pt = stage_base + C::NCH_V * C::CHUNK + (c0 / 8) * 2048 + r * 16;
+        // p = 2^(s*c - m): bf16 P^T into the tile's (now dead) RoPE chunk,
+        // MN-major no-swizzle [NQ/8][128 tok][8]
+        const uint32_t stage_base = sbase + (it % NS) * C::STAGE;
+        const uint32_t pt = stage_base + C::NCH_V * C::CHUNK + (c0 / 8) * 2048 + r * 16;
 #pragma unroll
-      for (int g = 0; g < CW / 8; ++g) {
-        const float4 ma = ld_shared_f4(m_addr + g * 32);
-        const float4 mb = ld_shared_f4(m_addr + g * 32 + 16);
-        const float mv[8] = {ma.x, ma.y, ma.z, ma.w, mb.x, mb.y, mb.z, mb.w};
-        uint32_t pk[4];
+        for (int g = 0; g < CW / 8; ++g) {
+          const float4 ma = ld_shared_f4(m_addr + g * 32);
+          const float4 mb = ld_shared_f4(m_addr + g * 32 + 16);
+          const float mv[8] = {ma.x, ma.y, ma.z, ma.w, mb.x, mb.y, mb.z, mb.w};
+          uint32_t pk[4];
 #pragma unroll
-        for (int k = 0; k < 8; k += 2) {
-          const float m0 = mv[k] == -INFINITY ? 0.f : mv[k];
-          const float m1 = mv[k + 1] == -INFINITY ? 0.f : mv[k + 1];
-          const __nv_bfloat162 v =
-              __floats2bfloat162_rn(ex2(fmaf(x[g * 8 + k], sl2, -m0)), ex2(fmaf(x[g * 8 + k + 1], sl2, -m1)));
-          l[g * 8 + k] += __low2float(v);
-          l[g * 8 + k + 1] += __high2float(v);
-          pk[k / 2] = *reinterpret_cast<const uint32_t*>(&v);
+          for (int k = 0; k < 8; k += 2) {
+            const float m0 = mv[k] == -INFINITY ? 0.f : mv[k];
+            const float m1 = mv[k + 1] == -INFINITY ? 0.f : mv[k + 1];
+            const __nv_bfloat162 v =
+                __floats2bfloat162_rn(ex2(fmaf(x[g * 8 + k], sl2, -m0)), ex2(fmaf(x[g * 8 + k + 1], sl2, -m1)));
+            l[g * 8 + k] += __low2float(v);
+            l[g * 8 + k + 1] += __high2float(v);
+            pk[k / 2] = *reinterpret_cast<const uint32_t*>(&v);
+          }
+          st_shared_v4(pt + g * 2048, pk[0], pk[1], pk[2], pk[3]);
         }
-        st_shared_v4(pt + g * 2048, pk[0], pk[1], pk[2], pk[3]);
-      }
-      if (wg == 0 && tok >= kv_end) {  // never-visible rows: zero V so 0 * garbage cannot give NaN
-        const uint32_t kvrow = stage_base + r * 128;
+        if (wg == 0 && tok >= s.kv_end) {  // never-visible rows: zero V so 0 * garbage cannot give NaN
+          const uint32_t kvrow = stage_base + r * 128;
 #pragma unroll
-        for (int ch = 0; ch < C::NCH_V; ++ch)
+          for (int ch = 0; ch < C::NCH_V; ++ch)
 #pragma unroll
-          for (int u = 0; u < 8; ++u) st_shared_v4(kvrow + ch * C::CHUNK + u * 16, 0u, 0u, 0u, 0u);
+            for (int uu = 0; uu < 8; ++uu) st_shared_v4(kvrow + ch * C::CHUNK + uu * 16, 0u, 0u, 0u, 0u);
+        }
+        fence_proxy_async_smem();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&p_full[it % NS]);
+        if (trace && threadIdx.x == 128 && it < kTraceTiles) trace[11 + 5 * it] = globaltimer();
       }
-      fence_proxy_async_smem();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&p_full[it % NS]);
-      if (trace && threadIdx.x == 128 && it < kTraceTiles) trace[11 + 5 * it] = globaltimer();
-    }
 
-    // ------------------------------------------------------------- epilogue
-    const float cs = warp_col_reduce<CW, false>(l, lane);
-    if ((lane & ((1 << col_shift<CW>()) - 1)) == 0) red[(wg * 4 + wq) * 32 + (lane >> col_shift<CW>())] = cs;
-    named_bar_sync(bar_id, 128);
-    if (r < CW) {  // fold the row sum into alpha_s as 1/l (reused below) and write lse
-      const float* rr = red + wg * 128 + r;
-      const float ls = (rr[0] + rr[32]) + (rr[64] + rr[96]);
-      alpha_s[c0 + r] = ls > 0.f ? 1.f / ls : 0.f;
-      if (c0 + r < nq) {
-        const float lse = ls > 0.f ? (m_run[c0 + r] + __log2f(ls)) * 0.69314718055994531f : -INFINITY;
-        const int ng = n0 + c0 + r, t = ng / p.g_q, h = head * p.g_q + (ng - t * p.g_q);
-        const size_t row = (static_cast<size_t>(b) * p.Lq + t) * p.H + h;
-        if (p.num_splits == 1) p.lse[row] = lse;
-        else p.lse_part[split * n_rows_total + row] = lse;
-      }
-    }
-    named_bar_sync(bar_id, 128);
-    const int j = ntiles - 1;
-    mbar_wait(&pv_done[j & 3], (j >> 2) & 1);
-    tc_fence_after();
-#pragma unroll
-    for (int blk = 0; blk < C::NBLK_O; ++blk) {
-      float o[CW];
-      tmem_load_cols<C>(tmem + lane_addr + C::TMEM_O + blk * NQ + c0, o);
-      tmem_ld_wait();
-      const int d = blk * 128 + r;
-#pragma unroll
-      for (int n = 0; n < CW; ++n) {
-        if (c0 + n < nq) {
-          const int ng = n0 + c0 + n, t = ng / p.g_q, h = head * p.g_q + (ng - t * p.g_q);
-          const size_t row = (static_cast<size_t>(b) * p.Lq + t) * p.H + h;
-          const float val = o[n] * alpha_s[c0 + n];
-          if (p.num_splits == 1) p.out[row * C::D_V + d] = __float2bfloat16(val);
-          else p.o_part[(split * n_rows_total + row) * C::D_V + d] = val;
+      // ------------------------------------------------------- segment epilogue
+      const float cs = warp_col_reduce<CW, false>(l, lane);
+      if ((lane & ((1 << col_shift<CW>()) - 1)) == 0) red[(wg * 4 + wq) * 32 + (lane >> col_shift<CW>())] = cs;
+      named_bar_sync(bar_id, 128);
+      const int slot = cta + s.u;  // partial slot of a split unit
+      if (r < CW) {  // fold the row sum into alpha_s as 1/l (reused below) and write lse
+        const float* rr = red + wg * 128 + r;
+        const float ls = (rr[0] + rr[32]) + (rr[64] + rr[96]);
+        alpha_s[c0 + r] = ls > 0.f ? 1.f / ls : 0.f;
+        if (c0 + r < s.nq) {
+          const float lse = ls > 0.f ? (m_run[c0 + r] + __log2f(ls)) * 0.69314718055994531f : -INFINITY;
+          if (s.whole) {
+            const int ng = s.n0 + c0 + r, t = ng / p.g_q, h = s.head * p.g_q + (ng - t * p.g_q);
+            p.lse[(static_cast<size_t>(s.b) * p.Lq + t) * p.H + h] = lse;
+          } else {
+            p.lse_part[static_cast<size_t>(slot) * NQ + c0 + r] = lse;
+          }
         }
       }
+      named_bar_sync(bar_id, 128);
+      const int j = it - 1;  // last tile of this segment
+      mbar_wait(&pv_done[j & 3], (j >> 2) & 1);
+      tc_fence_after();
+#pragma unroll
+      for (int blk = 0; blk < C::NBLK_O; ++blk) {
+        float o[CW];
+        tmem_load_cols<C>(obuf + lane_addr + blk * NQ + c0, o);
+        tmem_ld_wait();
+        if (blk == C::NBLK_O - 1) {  // O buffer consumed: the segment after next may reuse it
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&o_empty[seg & 1]);
+        }
+        const int d = blk * 128 + r;
+#pragma unroll
+        for (int n = 0; n < CW; ++n) {
+          if (c0 + n < s.nq) {
+            const float val = o[n] * alpha_s[c0 + n];
+            if (s.whole) {
+              const int ng = s.n0 + c0 + n, t = ng / p.g_q, h = s.head * p.g_q + (ng - t * p.g_q);
+              p.out[((static_cast<size_t>(s.b) * p.Lq + t) * p.H + h) * C::D_V + d] = __float2bfloat16(val);
+            } else {
+              p.o_part[(static_cast<size_t>(slot) * NQ + c0 + n) * C::D_V + d] = val;
+            }
+          }
+        }
+      }
+      named_bar_sync(bar_id, 128);  // alpha_s / m_run reads done before the next segment resets them
+      ++seg;
     }
   }
 

@@ -59,12 +59,11 @@ def _sig(lib):
         "glad_last_error": ([], ctypes.c_char_p),
         "glad_version": ([], ctypes.c_char_p),
         "glad_debug_set_trace": ([_VP], None),
+        "glad_debug_set_phase_mask": ([ctypes.c_int32], None),
         "glad_pool_bytes": ([L], ctypes.c_size_t),
         "glad_cache_append": ([L, _VP, _VP, ctypes.c_int32, _VP, _VP, ctypes.c_int32, ctypes.c_int32, _VP], S),
         "glad_paged_gather": ([L, _VP, _VP, ctypes.c_int32, _VP, ctypes.c_int32, ctypes.c_int32, _VP, _VP], S),
-        "glad_decode_workspace_bytes": ([ctypes.c_int32] * 5, ctypes.c_size_t),
-        "glad_decode_num_splits": ([L, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
-                                    ctypes.c_int32], ctypes.c_int32),
+        "glad_decode_workspace_bytes": ([L] + [ctypes.c_int32] * 5, ctypes.c_size_t),
         "glad_gla_decode": (dec, S),
         "glad_mla_decode": (dec, S),
         "glad_gta_decode": (dec, S),
@@ -92,8 +91,8 @@ def lib():
 
 
 def exported_symbols():
-    return ["glad_last_error", "glad_version", "glad_debug_set_trace", "glad_pool_bytes", "glad_cache_append", "glad_paged_gather",
-            "glad_decode_workspace_bytes", "glad_decode_num_splits", "glad_gla_decode", "glad_mla_decode",
+    return ["glad_last_error", "glad_version", "glad_debug_set_trace", "glad_debug_set_phase_mask", "glad_pool_bytes", "glad_cache_append", "glad_paged_gather",
+            "glad_decode_workspace_bytes", "glad_gla_decode", "glad_mla_decode",
             "glad_gta_decode", "glad_splitkv_combine", "glad_tp_duplication", "glad_tp_shard",
             "glad_kv_bytes_per_token_per_device"]
 
@@ -149,12 +148,8 @@ def paged_gather(layout, pool, block_table, seqlens, max_len, out=None, stream=N
     return out
 
 
-def workspace_bytes(B, Lq, H, d_v, splits):
-    return lib().glad_decode_workspace_bytes(B, Lq, H, d_v, splits)
-
-
-def num_splits(layout, B, Lq, H, bt_stride, variant=GLA):
-    return lib().glad_decode_num_splits(ctypes.byref(layout), B, Lq, H, bt_stride, variant)
+def workspace_bytes(layout, B, Lq, H, variant=GLA, num_ctas=0):
+    return lib().glad_decode_workspace_bytes(ctypes.byref(layout), B, Lq, H, variant, num_ctas)
 
 
 class Workspace:
@@ -169,7 +164,7 @@ class Workspace:
         if nbytes == 0:
             return None
         if self.buf is None or self.buf.numel() < nbytes:
-            self.buf = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+            self.buf = torch.empty(nbytes + 256, dtype=torch.uint8, device=self.device)
         return self.buf
 
 
@@ -177,7 +172,7 @@ _default_ws = {}
 
 
 def _decode(fn, variant, q, pool, layout, block_table, seqlens, softmax_scale, causal=True, out=None,
-            lse=None, splits=0, workspace=None, stream=None):
+            lse=None, num_ctas=0, workspace=None, stream=None):
     _need(q, torch.bfloat16, "q"); _need(pool, torch.bfloat16, "pool")
     _need(block_table, torch.int32, "block_table"); _need(seqlens, torch.int32, "seqlens")
     B, Lq, H, _ = q.shape
@@ -186,17 +181,13 @@ def _decode(fn, variant, q, pool, layout, block_table, seqlens, softmax_scale, c
         out = torch.empty(B, Lq, H, d_v, dtype=torch.bfloat16, device=q.device)
     if lse is None:
         lse = torch.empty(B, Lq, H, dtype=torch.float32, device=q.device)
-    bt_stride = block_table.shape[1]
-    S = splits if splits > 0 else num_splits(layout, B, Lq, H, bt_stride, variant)
-    if S < 0:
-        S = 1
-    nbytes = workspace_bytes(B, Lq, H, d_v, S)
+    nbytes = workspace_bytes(layout, B, Lq, H, variant, num_ctas)
     if workspace is None:
         workspace = _default_ws.setdefault(q.device, Workspace(q.device))
     ws = workspace.get(nbytes)
-    _check(fn(_ptr(q), _ptr(pool), ctypes.byref(layout), _ptr(block_table), bt_stride, _ptr(seqlens), B, Lq, H,
-              float(softmax_scale), 1 if causal else 0, _ptr(out), _ptr(lse), _ptr(ws), nbytes, S,
-              _stream(stream)))
+    _check(fn(_ptr(q), _ptr(pool), ctypes.byref(layout), _ptr(block_table), block_table.shape[1], _ptr(seqlens),
+              B, Lq, H, float(softmax_scale), 1 if causal else 0, _ptr(out), _ptr(lse), _ptr(ws), nbytes,
+              num_ctas, _stream(stream)))
     return out, lse
 
 
@@ -245,6 +236,11 @@ TRACE_STRIDE = 8 + 5 * 64
 def debug_set_trace(buf):
     """Debug timeline (see csrc/decode.cuh); buf: int64 CUDA tensor or None."""
     lib().glad_debug_set_trace(_ptr(buf) if buf is not None else ctypes.c_void_p(0))
+
+
+def debug_set_phase_mask(mask):
+    """Debug/benchmark: launch only plan (1) / decode (2) / merge (4)."""
+    lib().glad_debug_set_phase_mask(int(mask))
 
 
 def version():

@@ -104,7 +104,7 @@ def algorithmic_flops(wl, seqlens):
     return int(2 * wl.H * (wl.d_qk + wl.d_v) * visible_counts(seqlens, wl.Lq, wl.causal).sum())
 
 
-def build_device_state(wl, seed=None, device="cuda", splits=0):
+def build_device_state(wl, seed=None, device="cuda", num_ctas=0):
     """Seeded synthetic device state: pool of N(0,1) bf16 rows (pages are a
     random permutation), block table, seqlens, queries, preallocated outputs
     and split workspace (so the step is CUDA-graph capturable)."""
@@ -115,19 +115,18 @@ def build_device_state(wl, seed=None, device="cuda", splits=0):
     pool = synth.device_pool(num_pages, wl.page, layout.row_stride, seed, device)
     q = synth.device_queries(wl.B, wl.Lq, wl.H, wl.d_qk, seed, device)
     variant = {"gla": glad.GLA, "mla": glad.MLA, "gta": glad.GTA}[wl.variant]
-    S = splits if splits > 0 else glad.num_splits(layout, wl.B, wl.Lq, wl.H, bt.shape[1], variant)
     ws = glad.Workspace(device)
-    ws.get(glad.workspace_bytes(wl.B, wl.Lq, wl.H, wl.d_v, S))
+    ws.get(glad.workspace_bytes(layout, wl.B, wl.Lq, wl.H, variant, num_ctas))
     return dict(layout=layout, pool=pool, block_table=torch.from_numpy(bt).to(device),
                 seqlens=torch.from_numpy(sl.astype(np.int32)).to(device), seqlens_host=sl, q=q,
                 out=torch.empty(wl.B, wl.Lq, wl.H, wl.d_v, dtype=torch.bfloat16, device=device),
                 lse=torch.empty(wl.B, wl.Lq, wl.H, dtype=torch.float32, device=device),
-                splits=S, workspace=ws)
+                num_ctas=num_ctas, workspace=ws)
 
 
 def run(wl, st, stream=None, q=None):
-    """One decode step through the C ABI (decode [+ combine])."""
+    """One decode step through the C ABI (plan + decode + merge kernels)."""
     fn = {"gla": glad.gla_decode, "mla": glad.mla_decode, "gta": glad.gta_decode}[wl.variant]
     return fn(st["q"] if q is None else q, st["pool"], st["layout"], st["block_table"], st["seqlens"], wl.scale,
-              causal=wl.causal, out=st["out"], lse=st["lse"], splits=st["splits"], workspace=st["workspace"],
+              causal=wl.causal, out=st["out"], lse=st["lse"], num_ctas=st["num_ctas"], workspace=st["workspace"],
               stream=stream)

@@ -65,7 +65,7 @@ def test_append_in_chunks_matches_single():
 
 
 # ------------------------------------------------------------ GLA / MLA
-def run_latent(B, Lq, H, h_c, d_c, d_R, seqlens, page, splits=0, causal=True, scale=None, seed=0,
+def run_latent(B, Lq, H, h_c, d_c, d_R, seqlens, page, ctas=0, causal=True, scale=None, seed=0,
                q_scale=1.0):
     Lmax = int(max(seqlens.max(), 1))
     q, c, kr = synth.latent_kernel_inputs(B, Lq, H, h_c, d_c, d_R, Lmax, seed=seed, q_scale=q_scale)
@@ -73,7 +73,7 @@ def run_latent(B, Lq, H, h_c, d_c, d_R, seqlens, page, splits=0, causal=True, sc
     scale = scale if scale is not None else 1.0 / math.sqrt(d_c // 2 + d_R)
     sl_d = torch.from_numpy(seqlens.astype(np.int32)).to(DEV)
     fn = glad.mla_decode if h_c == 1 and d_c == 512 else glad.gla_decode
-    out, lse = fn(q.to(DEV), pool, layout, bt, sl_d, scale, causal=causal, splits=splits)
+    out, lse = fn(q.to(DEV), pool, layout, bt, sl_d, scale, causal=causal, num_ctas=ctas)
     torch.cuda.synchronize()
     o_ref, lse_ref = OA.latent_decode(f64(q), f64(c), f64(kr), seqlens, scale, causal=causal)
     return out, lse, o_ref, lse_ref
@@ -106,7 +106,7 @@ def test_c1_against_unabsorbed_definition():
 
 
 GLA_SWEEP = [
-    # B, Lq, H, h_c, d_c, d_R, lens, page, splits, causal
+    # B, Lq, H, h_c, d_c, d_R, lens, page, num_ctas (0 = #SMs), causal
     (2, 1, 128, 2, 256, 64, [1024, 777], 64, 0, True),
     (2, 2, 128, 2, 256, 64, [1024, 777], 64, 0, True),
     (2, 1, 128, 2, 256, 64, [1024, 777], 1, 3, True),
@@ -122,15 +122,15 @@ GLA_SWEEP = [
 @pytest.mark.parametrize("cfg", GLA_SWEEP, ids=lambda c: "B{}Lq{}H{}hc{}dc{}dr{}p{}s{}c{}".format(
     c[0], c[1], c[2], c[3], c[4], c[5], c[7], c[8], int(c[9])))
 def test_gla_sweep(cfg):
-    B, Lq, H, h_c, d_c, d_R, lens, page, splits, causal = cfg
-    out, lse, o_ref, lse_ref = run_latent(B, Lq, H, h_c, d_c, d_R, np.array(lens), page, splits=splits,
+    B, Lq, H, h_c, d_c, d_R, lens, page, ctas, causal = cfg
+    out, lse, o_ref, lse_ref = run_latent(B, Lq, H, h_c, d_c, d_R, np.array(lens), page, ctas=ctas,
                                           causal=causal, seed=GLA_SWEEP.index(cfg))
     check(out, lse, o_ref, lse_ref, what=str(cfg))
 
 
 def test_peaked_and_large_scores():
     """Peaked regime (q x 4) exercises the lazy-rescale path many times."""
-    out, lse, o_ref, lse_ref = run_latent(2, 2, 32, 2, 256, 64, np.array([900, 650]), 64, splits=1,
+    out, lse, o_ref, lse_ref = run_latent(2, 2, 32, 2, 256, 64, np.array([900, 650]), 64, ctas=1,
                                           seed=17, q_scale=4.0)
     check(out, lse, o_ref, lse_ref, what="peaked")
 
@@ -142,7 +142,7 @@ def test_mla_baseline(Lq, H):
 
 
 def test_empty_and_tiny_sequences():
-    out, lse, o_ref, lse_ref = run_latent(4, 2, 16, 2, 128, 32, np.array([0, 1, 2, 3]), 16, splits=1)
+    out, lse, o_ref, lse_ref = run_latent(4, 2, 16, 2, 128, 32, np.array([0, 1, 2, 3]), 16, ctas=1)
     check(out, lse, o_ref, lse_ref, what="tiny")
     assert torch.all(out[0].float() == 0) and torch.all(torch.isneginf(lse[0]))
     # causal Lq=2 with L=1: first query sees nothing
@@ -160,23 +160,23 @@ def test_page_size_and_permutation_invariance_bitexact():
     outs = []
     for page, seed in [(64, 0), (64, 1), (1, 2), (16, 3), (256, 4)]:
         layout, pool, bt = build_paged(rows, sl, page, h_c, d_c, d_R, seed=seed)
-        o, l = glad.gla_decode(q.to(DEV), pool, layout, bt, sl_d, 0.07, splits=2)
+        o, l = glad.gla_decode(q.to(DEV), pool, layout, bt, sl_d, 0.07, num_ctas=5)
         outs.append((o.cpu().view(torch.int16), l.cpu()))
     for o, l in outs[1:]:
         assert torch.equal(o, outs[0][0]) and torch.equal(l, outs[0][1])
 
 
-def test_split_count_changes_only_rounding():
-    B, Lq, H = 2, 1, 128
-    sl = np.array([3000, 2500])
-    ref = None
-    for s in (1, 2, 4, 7):
-        out, lse, o_ref, lse_ref = run_latent(B, Lq, H, 2, 256, 64, sl, 64, splits=s, seed=33)
-        check(out, lse, o_ref, lse_ref, what=f"splits={s}")
+@pytest.mark.parametrize("ctas", [1, 2, 5, 7, 148, 300])
+def test_cta_count_changes_only_rounding(ctas):
+    """Any persistent-CTA count (1 = no split at all; 300 > tiles = many
+    empty CTAs and units cut into 1-tile segments) matches the oracle."""
+    sl = np.array([3000, 2500, 1, 700])
+    out, lse, o_ref, lse_ref = run_latent(4, 1, 128, 2, 256, 64, sl, 64, ctas=ctas, seed=33)
+    check(out, lse, o_ref, lse_ref, what=f"ctas={ctas}")
 
 
 # ------------------------------------------------------------------- GTA
-def run_gta(B, Lq, H, h_kv, seqlens, page, splits=0, causal=True, seed=0):
+def run_gta(B, Lq, H, h_kv, seqlens, page, ctas=0, causal=True, seed=0):
     d_h = 128
     Lmax = int(max(seqlens.max(), 1))
     q, kv, kr = synth.gta_kernel_inputs(B, Lq, H, h_kv, d_h, Lmax, seed=seed)
@@ -184,7 +184,7 @@ def run_gta(B, Lq, H, h_kv, seqlens, page, splits=0, causal=True, seed=0):
     layout, pool, bt = build_paged(rows, seqlens, page, h_kv, d_h, d_h // 2, seed=seed)
     scale = 1.0 / math.sqrt(d_h)
     out, lse = glad.gta_decode(q.to(DEV), pool, layout, bt, torch.from_numpy(seqlens.astype(np.int32)).to(DEV),
-                               scale, causal=causal, splits=splits)
+                               scale, causal=causal, num_ctas=ctas)
     torch.cuda.synchronize()
     o_ref, lse_ref = OA.tied_decode(f64(q), f64(kv), f64(kr), seqlens, scale, causal=causal)
     return out, lse, o_ref, lse_ref
@@ -193,8 +193,8 @@ def run_gta(B, Lq, H, h_kv, seqlens, page, splits=0, causal=True, seed=0):
 @pytest.mark.parametrize("cfg", [(2, 1, 64, 8, [700, 333], 64, 0), (2, 2, 64, 8, [700, 333], 16, 2),
                                  (3, 1, 32, 2, [129, 1, 400], 1, 1), (1, 4, 64, 4, [1500], 64, 3)])
 def test_gta(cfg):
-    B, Lq, H, h_kv, lens, page, splits = cfg
-    out, lse, o_ref, lse_ref = run_gta(B, Lq, H, h_kv, np.array(lens), page, splits=splits, seed=7)
+    B, Lq, H, h_kv, lens, page, ctas = cfg
+    out, lse, o_ref, lse_ref = run_gta(B, Lq, H, h_kv, np.array(lens), page, ctas=ctas, seed=7)
     check(out, lse, o_ref, lse_ref, what=f"GTA {cfg}")
 
 
@@ -261,3 +261,14 @@ def _sampled_latent_check(wl, st, out, lse, samples):
         o_g = out[b, :, i * g_q:(i + 1) * g_q].reshape(-1, wl.d_c)
         l_g = lse[b, :, i * g_q:(i + 1) * g_q].reshape(-1)
         check(o_g, l_g, o_ref, lse_ref, what=f"sample b={b} head={i}")
+
+
+@pytest.mark.parametrize("ctas", [1, 2])
+def test_segment_table_overflow(ctas):
+    """More (sequence, head) units per CTA than the 128-entry shared-memory
+    segment table: the rest of the CTA's range is walked on the fly."""
+    B = 90
+    sl = synth.seqlens(B, 300, "uniform", r=0.01, seed=4)
+    sl[3] = 0
+    out, lse, o_ref, lse_ref = run_latent(B, 1, 16, 2, 128, 32, sl, 16, ctas=ctas, seed=8)
+    check(out, lse, o_ref, lse_ref, what=f"overflow ctas={ctas}")

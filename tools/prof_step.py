@@ -11,11 +11,11 @@ from paper_2505_21487_b200 import workloads  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--workload", default="c2_gla2")
 ap.add_argument("--steps", type=int, default=3)
-ap.add_argument("--splits", type=int, default=0)
+ap.add_argument("--ctas", type=int, default=0)
 a = ap.parse_args()
 wl = workloads.get(a.workload)
-st = workloads.build_device_state(wl, splits=a.splits)
+st = workloads.build_device_state(wl, num_ctas=a.ctas)
 for _ in range(a.steps):
     workloads.run(wl, st)
 torch.cuda.synchronize()
-print("splits", st["splits"], "done")
+print("done")

@@ -22,11 +22,11 @@ from paper_2505_21487_b200 import glad, workloads  # noqa: E402
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--workload", default="c2_gla2")
-ap.add_argument("--splits", type=int, default=0)
+ap.add_argument("--ctas", type=int, default=0)
 ap.add_argument("--ns", type=int, default=2, help="KV stages of the instantiation (for PV->load)")
 a = ap.parse_args()
 wl = workloads.get(a.workload)
-st = workloads.build_device_state(wl, splits=a.splits)
+st = workloads.build_device_state(wl, num_ctas=a.ctas)
 for _ in range(3):
     workloads.run(wl, st)
 torch.cuda.synchronize()
@@ -39,7 +39,7 @@ glad.debug_set_trace(None)
 tr = buf.view(n_ctas, glad.TRACE_STRIDE).cpu().numpy().astype(np.int64)
 tr = tr[tr[:, 0] > 0]
 t0 = tr[:, 0].min()
-print(f"{wl.name}: splits {st['splits']}, {len(tr)} CTAs, kernel span {(tr[:, 2].max() - t0) / 1e3:.1f} us")
+print(f"{wl.name}: segments/CTA {np.median(tr[:, 3]):.1f}, {len(tr)} CTAs, kernel span {(tr[:, 2].max() - t0) / 1e3:.1f} us")
 print(f"CTA lifetime median {np.median(tr[:, 2] - tr[:, 0]) / 1e3:.1f} us, start->Q ready "
       f"{np.median(tr[:, 1] - tr[:, 0]) / 1e3:.2f} us")
 T = (tr.shape[1] - 8) // 5
