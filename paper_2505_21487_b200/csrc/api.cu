@@ -6,6 +6,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "../../include/glad.h"
@@ -144,7 +145,11 @@ glad_status decode_common(Variant v, const void* q, const void* pool, const glad
   if (num_ctas < 0) return fail(GLAD_ERR_INVALID_ARG, "num_ctas=%d < 0", num_ctas);
   const int64_t U = static_cast<int64_t>(B) * L->n_heads_kv * g.n_qblk;
   if (U >= (int64_t(1) << 30)) return fail(GLAD_ERR_UNSUPPORTED, "too many work units (%lld)", (long long)U);
-  const int G = num_ctas > 0 ? num_ctas : num_sms();
+  const int G0 = num_ctas > 0 ? num_ctas : num_sms();
+  // one equal CTA group per KV head (when there are enough CTAs): keeps the
+  // heads of a sequence in lockstep so their shared RoPE rows hit L2
+  const int head_groups = (L->n_heads_kv > 1 && G0 >= L->n_heads_kv) ? 1 : 0;
+  const int G = head_groups ? (G0 / L->n_heads_kv) * L->n_heads_kv : G0;
   const WsLayout wl = ws_layout(U, G, g.key.nq, L->d_head);
   if (ws == nullptr || ws_bytes < wl.total)
     return fail(GLAD_ERR_WORKSPACE, "workspace %zu bytes < required %zu", ws_bytes, wl.total);
@@ -159,9 +164,10 @@ glad_status decode_common(Variant v, const void* q, const void* pool, const glad
   cuuint64_t strides[1] = {static_cast<cuuint64_t>(L->row_stride) * 2};
   cuuint32_t box[2] = {64u, static_cast<cuuint32_t>(box_rows)};
   cuuint32_t estr[2] = {1u, 1u};
+  // (L2 promotion none/128B/256B measured identical DRAM bytes and time)
+  const CUtensorMapL2promotion pr = CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
   CUresult cr = enc(&tmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(pool), dims, strides, box, estr,
-                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, pr, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (cr != CUDA_SUCCESS) return fail(GLAD_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", static_cast<int>(cr));
 
   // Q as a 3-D tensor [B*Lq][H][d_qk]: a unit's NQ query rows are one box
@@ -187,6 +193,7 @@ glad_status decode_common(Variant v, const void* q, const void* pool, const glad
   char* wsb = static_cast<char*>(ws);
   glad::DecodeParams p;
   p.q_tma = q_tma ? 1 : 0;
+  p.head_groups = head_groups;
   p.q_box_h = q_box_h;
   p.q_box_t = q_box_t;
   p.q = static_cast<const __nv_bfloat16*>(q);
@@ -225,8 +232,9 @@ glad_status decode_common(Variant v, const void* q, const void* pool, const glad
     if (e != cudaSuccess) return fail(GLAD_ERR_CUDA, "decode launch failed: %s", cudaGetErrorString(e));
   }
   if (g_phase_mask & 4) {
-    e = glad::launch_merge_units(plan, p.o_part, p.lse_part, G, p.n_units, g.key.nq, g.n_qblk, B, g.g_q,
-                                 Lq, H, static_cast<int64_t>(B) * Lq * H, L->d_head, out, lse, st);
+    e = glad::launch_merge_units(plan, p.o_part, p.lse_part, G, p.n_units, g.key.nq, g.n_qblk, B, L->n_heads_kv,
+                                 head_groups, g.g_q, Lq, H, static_cast<int64_t>(B) * Lq * H, L->d_head, out, lse,
+                                 st);
     if (e != cudaSuccess) return fail(GLAD_ERR_CUDA, "merge launch failed: %s", cudaGetErrorString(e));
   }
   return GLAD_OK;

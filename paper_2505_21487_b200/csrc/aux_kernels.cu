@@ -140,7 +140,7 @@ __global__ void plan_kernel(const int32_t* __restrict__ seqlens, int32_t* __rest
 // written by the decode kernel and are skipped.
 __global__ void merge_units_kernel(const int32_t* __restrict__ plan, const float* __restrict__ o_part,
                                    const float* __restrict__ lse_part, int G, int U, int nq_blk, int n_qblk,
-                                   int B, int g_q, int Lq, int H, int64_t rows, int d_v,
+                                   int B, int n_heads, int head_groups, int g_q, int Lq, int H, int64_t rows, int d_v,
                                    __nv_bfloat16* __restrict__ out, float* __restrict__ lse) {
   const int64_t row = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
@@ -160,8 +160,8 @@ __global__ void merge_units_kernel(const int32_t* __restrict__ plan, const float
     if (lane == 0) lse[row] = -INFINITY;
     return;
   }
-  const int per = (total + G - 1) / G;
-  const int c_first = pu0 / per, c_last = (pu1 - 1) / per;
+  const int c_first = cta_of_tile(pu0, G, total, n_heads, head_groups);
+  const int c_last = cta_of_tile(pu1 - 1, G, total, n_heads, head_groups);
   if (c_first == c_last) return;
   float mx = -INFINITY;
   for (int c = c_first + lane; c <= c_last; c += 32)
@@ -205,13 +205,13 @@ cudaError_t launch_plan(const int32_t* seqlens, int32_t* plan, int U, int B, int
 }
 
 cudaError_t launch_merge_units(const int32_t* plan, const float* o_part, const float* lse_part, int G, int U,
-                               int nq_blk, int n_qblk, int B, int g_q, int Lq, int H, int64_t rows, int d_v,
-                               void* out, float* lse, cudaStream_t stream) {
+                               int nq_blk, int n_qblk, int B, int n_heads, int head_groups, int g_q, int Lq, int H,
+                               int64_t rows, int d_v, void* out, float* lse, cudaStream_t stream) {
   if (rows == 0) return cudaSuccess;
   const int threads = 128;
   const int64_t blocks = (rows * 32 + threads - 1) / threads;
   merge_units_kernel<<<static_cast<unsigned>(blocks), threads, 0, stream>>>(
-      plan, o_part, lse_part, G, U, nq_blk, n_qblk, B, g_q, Lq, H, rows, d_v,
+      plan, o_part, lse_part, G, U, nq_blk, n_qblk, B, n_heads, head_groups, g_q, Lq, H, rows, d_v,
       static_cast<__nv_bfloat16*>(out), lse);
   return cudaGetLastError();
 }

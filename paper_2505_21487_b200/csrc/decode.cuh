@@ -60,6 +60,7 @@ struct DecodeParams {
   int32_t page_size, log2_page, box_rows;
   int32_t n_qblk, n_units;  // query blocks per head, U = n_heads_kv * B * n_qblk (head-major)
   int32_t causal;
+  int32_t head_groups;      // 1: CTAs form n_heads_kv equal groups, one per head (see cta_range)
   int32_t q_tma;            // 1: Q via the 3-D tensor map (box (64, q_box_h, q_box_t)); 0: cp.async
   int32_t q_box_h, q_box_t;
   float scale_log2;         // softmax_scale * log2(e)
@@ -209,6 +210,40 @@ __device__ __forceinline__ Seg make_seg(const DecodeParams& p, int u, int cta_t0
   return s;
 }
 
+// Flattened tile range of CTA c (units are head-major).  With head groups,
+// the G CTAs form n_heads_kv equal groups and group h splits head h's tiles
+// evenly, so CTA (h, k) works on the same sequences as (h', k) at the same
+// time and the RoPE rows the heads share are served from L2.
+struct CtaRange {
+  int t0, t1;
+};
+__device__ __host__ __forceinline__ CtaRange cta_range(int c, int G, int total, int n_heads, int head_groups) {
+  CtaRange r;
+  if (head_groups) {
+    const int Gh = G / n_heads, total_h = total / n_heads;
+    const int per = (total_h + Gh - 1) / Gh;
+    const int h = c / Gh, k = c - h * Gh;
+    r.t0 = h * total_h + min(total_h, k * per);
+    r.t1 = h * total_h + min(total_h, (k + 1) * per);
+  } else {
+    const int per = (total + G - 1) / G;
+    r.t0 = min(total, c * per);
+    r.t1 = min(total, r.t0 + per);
+  }
+  return r;
+}
+// CTA whose range contains tile t (inverse of cta_range).
+__device__ __host__ __forceinline__ int cta_of_tile(int t, int G, int total, int n_heads, int head_groups) {
+  if (head_groups) {
+    const int Gh = G / n_heads, total_h = total / n_heads;
+    const int per = (total_h + Gh - 1) / Gh;
+    const int h = t / total_h;
+    return h * Gh + (t - h * total_h) / per;
+  }
+  const int per = (total + G - 1) / G;
+  return t / per;
+}
+
 // Segment from a table entry (u, t0, t1, L) without global loads.
 template <int NQ>
 __device__ __forceinline__ Seg seg_from_entry(const DecodeParams& p, int4 e) {
@@ -270,8 +305,8 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
     // (a serial search over the plan would cost one L2 round trip per step).
     const int U = p.n_units;
     const int total = __ldg(p.plan + U);
-    const int per = (total + gridDim.x - 1) / gridDim.x;
-    const int t0 = min(total, cta * per), t1 = min(total, t0 + per);
+    const CtaRange rg = cta_range(cta, gridDim.x, total, p.n_heads_kv, p.head_groups);
+    const int t0 = rg.t0, t1 = rg.t1;
     int lo = 0, hi = U - 1;  // last unit with plan[u] <= t0 (plan[0] = 0)
     while (lo < hi) {
       const int step = (hi - lo + 32) / 32;
