@@ -168,7 +168,7 @@ def run_ours(args, rank, world, local_rank):
     import torch
     import torch.distributed as dist
 
-    from paper_2505_21487_b200 import glad, workloads
+    from paper_2505_21487_b200 import glad, tp, workloads
 
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
@@ -193,11 +193,9 @@ def run_ours(args, rank, world, local_rank):
 
     def step():
         out, _ = workloads.run(wl, st, stream=stream)
-        if o_proj is not None:
+        if o_proj is not None:  # row-parallel W^vo slice + one all-reduce
             w_vo, y = o_proj
-            torch.matmul(out.view(wl.B * wl.Lq, -1), w_vo, out=y)
-            if world > 1:
-                dist.all_reduce(y)
+            tp.oproj_allreduce(out.view(wl.B * wl.Lq, wl.H, wl.d_v), w_vo, out=y)
         return out
 
     for _ in range(max(3, args.warmup)):
@@ -277,9 +275,7 @@ def run_ours(args, rank, world, local_rank):
         out, lse = workloads.run(wl, st, stream=stream, q=q_d)
         if o_proj is not None:
             w_vo, y = o_proj
-            torch.matmul(out.view(wl.B * wl.Lq, -1), w_vo, out=y)
-            if world > 1:
-                dist.all_reduce(y)
+            tp.oproj_allreduce(out.view(wl.B * wl.Lq, wl.H, wl.d_v), w_vo, out=y)
         out_h.copy_(out, non_blocking=True)
         lse_h.copy_(lse, non_blocking=True)
 

@@ -272,3 +272,30 @@ def test_segment_table_overflow(ctas):
     sl[3] = 0
     out, lse, o_ref, lse_ref = run_latent(B, 1, 16, 2, 128, 32, sl, 16, ctas=ctas, seed=8)
     check(out, lse, o_ref, lse_ref, what=f"overflow ctas={ctas}")
+
+
+@pytest.mark.parametrize("N", [2, 8])
+def test_tp_sharded_gla8_emulated(N):
+    """T3' (single-GPU emulation of TP): each rank's shard — its
+    latent heads + the replicated RoPE in its own pool, its query heads —
+    decodes through the C ABI; the sum of the rank-local o_proj partials
+     equals the unsharded result computed by the oracle."""
+    from oracle import sharding as OS
+    from paper_2505_21487_b200 import tp
+    B, Lq, H, h_c, d_c, d_R, D = 2, 2, 32, 8, 256, 64, 96
+    sl = np.array([700, 333])
+    q, c, kr = synth.latent_kernel_inputs(B, Lq, H, h_c, d_c, d_R, 700, seed=31)
+    w_vo = synth.normal_bf16((H * d_c, D), seed=32, std=1.0 / math.sqrt(H * d_c))
+    scale = 1.0 / math.sqrt(192)
+    y = torch.zeros(B * Lq, D, dtype=torch.float64)
+    for r in range(N):
+        kb, ke, qb, qe = tp.shard(H, h_c, N, r)
+        rows = torch.cat([c[:, :, kb:ke].reshape(B, 700, -1), kr], -1).contiguous()
+        layout, pool, bt = build_paged(rows, sl, 64, ke - kb, d_c, d_R, seed=r)
+        out, _ = glad.gla_decode(q[:, :, qb:qe].contiguous().to(DEV), pool, layout, bt,
+                                 torch.from_numpy(sl.astype(np.int32)).to(DEV), scale)
+        y += (out.float().reshape(B * Lq, -1) @ w_vo[qb * d_c:qe * d_c].float().to(DEV)).double().cpu()
+    o_ref, _ = OA.latent_decode(f64(q), f64(c), f64(kr), sl, scale)
+    y_ref = OS.tp_oproj_allreduce(o_ref.reshape(B * Lq, H, d_c), f64(w_vo).reshape(H, d_c, D), N, h_c)
+    rel = float(np.linalg.norm(y.numpy() - y_ref) / np.linalg.norm(y_ref))
+    assert rel < 5e-3, rel
