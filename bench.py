@@ -173,17 +173,17 @@ def run_ours(args, rank, world, local_rank):
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
     name = args.workload
-    tp = name.startswith("c5")
-    if tp:
+    is_tp = name.startswith("c5")
+    if is_tp:
         base = name.replace("_tp1", "").replace("_tp2", "").replace("_tp4", "").replace("_tp8", "")
         name = base.replace("c5_gla8", f"c5_gla8_tp{world}")
     wl = workloads.get(name)
-    st = workloads.build_device_state(wl, seed=wl.seed + (0 if tp else rank), device=dev, num_ctas=args.ctas)
+    st = workloads.build_device_state(wl, seed=wl.seed + (0 if is_tp else rank), device=dev, num_ctas=args.ctas)
     sl = st["seqlens_host"]
     stream = torch.cuda.current_stream(dev)
 
     o_proj = None
-    if tp:  # row-parallel o_proj slice W_r^vo [H_loc*d_c, d_model], d_model 5120 (R15)
+    if is_tp:  # row-parallel o_proj slice W_r^vo [H_loc*d_c, d_model], d_model 5120 (R15)
         d_model = 5120
         g = torch.Generator(device=dev).manual_seed(1234 + rank)
         w_vo = (torch.randn(wl.H * wl.d_c, d_model, generator=g, device=dev) / math.sqrt(wl.H * wl.d_c)).to(
@@ -205,7 +205,7 @@ def run_ours(args, rank, world, local_rank):
     # CUDA graph of one step (host argument marshalling and TMA descriptor
     # encoding happen once at capture; replay is launch-overhead free).
     graph = None
-    if not tp:
+    if not is_tp:
         try:
             g = torch.cuda.CUDAGraph()
             s2 = torch.cuda.Stream(dev)
@@ -286,7 +286,7 @@ def run_ours(args, rank, world, local_rank):
     d2h = out_h.numel() * 2 + lse_h.numel() * 4
 
     tokens_per_rank = wl.B * wl.Lq
-    total_tokens = tokens_per_rank if tp else tokens_per_rank * world
+    total_tokens = tokens_per_rank if is_tp else tokens_per_rank * world
     value = total_tokens / (ms * 1e-3)
     abytes = workloads.algorithmic_bytes(wl, sl)
     aflops = workloads.algorithmic_flops(wl, sl)
@@ -315,11 +315,11 @@ def run_ours(args, rank, world, local_rank):
         line = {
             "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-            "scaling": "strong" if tp else "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "scaling": "strong" if is_tp else "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
             "config": {"workload": wl.name, "desc": wl.description, "B": wl.B, "q_len": wl.Lq, "H": wl.H,
                        "n_kv_heads": wl.h_c, "d_head": wl.d_c, "d_rope": wl.d_R, "ctx_max": wl.L,
                        "ctx_mean": float(np.mean(sl)), "page": wl.page, "num_ctas": st["num_ctas"] or "num_SMs",
-                       "parallelism": (f"tp{world}" if tp else f"dp{world} (independent batches)"),
+                       "parallelism": (f"tp{world}" if is_tp else f"dp{world} (independent batches)"),
                        "l2": f"inputs larger than L2 ({abytes / 1e9:.2f} GB algorithmic per step > 126 MB); "
                              "no flush", "cuda_graph": graph is not None},
             "tbps": gbs / 1e3, "tflops": tfs,
