@@ -67,11 +67,11 @@ struct DecodeParams {
   uint64_t* trace;          // debug timeline (nullptr = off): [cta][kTraceStride]
 };
 // Debug timeline layout per CTA (globaltimer ns): [0] start, [1] first QK,
-// [2] end, [3] number of segments, then per tile i < kTraceTiles: [8+5i] load
-// issued, [9+5i] QK issued, [10+5i] S seen by softmax, [11+5i] P written,
-// [12+5i] PV issued.
+// [2] end, [3] number of segments, then per tile i < kTraceTiles: [8+6i] load
+// issued, [9+6i] QK issued, [10+6i] S seen by softmax, [11+6i] P written,
+// [12+6i] PV issued, [13+6i] stage free seen by the producer (before load i).
 constexpr int kTraceTiles = 64;
-constexpr int kTraceStride = 8 + 5 * kTraceTiles;
+constexpr int kTraceStride = 8 + 6 * kTraceTiles;
 
 template <int D_V_, int D_KN_, int D_R_, int NQ_>
 struct DecodeCfg {
@@ -94,6 +94,7 @@ struct DecodeCfg {
   // dead once QK of that tile has completed: P is thereby multi-buffered with
   // the KV stages at zero extra shared memory.
   static constexpr int PBYTES = T * NQ * 2;
+  static constexpr bool P_SW128 = (NQ == 64);  // MN-major SW128 P^T: PV MMA 70 vs 81 cycles (microbench)
   static constexpr int NBLK_O = D_V / 128;
   static constexpr int NWG = 2;
   static constexpr int CW = NQ / NWG;
@@ -403,33 +404,86 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
   if (warp == 0) {
     // ========================= TMA producer (all 32 lanes issue) =========================
     named_bar_sync(3, 96);  // the first Q load is issued first: QK needs Q, not a second tile
+    const int box_rows = p.box_rows;
+    // Issue the TMA boxes of tile `tl` of segment `s`: into smem (prefetch =
+    // false, completing on kv_full[stage]) or as an L2 prefetch.  Boxes are
+    // spread over the 32 lanes; one int32 block-table lookup per box.
+    auto issue_tile = [&](const Seg& s, int tl, int stage, bool prefetch, int page0) {
+      const int* bt_row = p.block_table + static_cast<size_t>(s.b) * p.bt_stride;
+      const int p0 = tl * T;
+      const int ntok = min(T, s.kv_end - p0);
+      const int nbox = (ntok + box_rows - 1) / box_rows;
+      for (int bx = lane; bx < nbox * C::NCH; bx += 32) {
+        const int box = bx / C::NCH, ch = bx - box * C::NCH;
+        const int pos = p0 + box * box_rows;
+        const int page = (bx == lane && page0 >= 0) ? page0 : __ldg(bt_row + (pos >> p.log2_page));
+        const int row = page * p.page_size + (pos & (p.page_size - 1));
+        const int col = ch < C::NCH_V ? s.head * p.d_head + ch * 64 : p.rope_col;
+        if (prefetch) {
+          tma_prefetch_2d(&tmap, col, row);
+        } else {
+          const uint32_t dst = sbase + stage * C::STAGE + ch * C::CHUNK + box * box_rows * 128;
+          tma_load_2d(dst, &tmap, &kv_full[stage], col, row);
+        }
+      }
+      return nbox;
+    };
+    // L2 prefetch cursor, PF = NS tiles ahead of the load cursor: the tile
+    // that will refill a stage once its PV completes is already on its way
+    // to L2, so the refill does not pay the full DRAM latency inside the
+    // (release -> load -> QK -> softmax -> PV) chain.
+    int pk = 0, pu = 0, ptl = 0, pt1 = 0;
+    bool pvalid = false;
+    Seg ps;
+    auto pf_advance = [&]() {
+      if (pvalid && ptl + 1 < pt1) { ++ptl; return; }
+      pvalid = next_seg(pk, pu, ps);
+      if (pvalid) { ptl = ps.t0; pt1 = ps.t1; }
+    };
+    pf_advance();
+    for (int i = 0; i < NS && pvalid; ++i) pf_advance();
     int k = 0, u = 0, it = 0;
     Seg s;
     while (next_seg(k, u, s)) {
       const int* bt_row = p.block_table + static_cast<size_t>(s.b) * p.bt_stride;
-      const int box_rows = p.box_rows;
       for (int tl = s.t0; tl < s.t1; ++tl, ++it) {
         const int stage = it % NS;
         const int p0 = tl * T;
         const int ntok = min(T, s.kv_end - p0);
         const int nbox = (ntok + box_rows - 1) / box_rows;
-        // block-table lookup for this lane's first box before the stage wait
-        int page0 = 0;
-        if (lane < nbox * C::NCH) page0 = __ldg(bt_row + ((p0 + (lane / C::NCH) * box_rows) >> p.log2_page));
+        const int nitem = nbox * C::NCH;
+        // coordinates of this lane's first box (block-table lookup included)
+        // are computed before the stage wait: after the release only the TMA
+        // issue remains on the critical path
+        int col0 = 0, row0 = 0;
+        uint32_t dst0 = 0;
+        if (lane < nitem) {
+          const int box = lane / C::NCH, ch = lane - box * C::NCH;
+          const int pos = p0 + box * box_rows;
+          const int page = __ldg(bt_row + (pos >> p.log2_page));
+          row0 = page * p.page_size + (pos & (p.page_size - 1));
+          col0 = ch < C::NCH_V ? s.head * p.d_head + ch * 64 : p.rope_col;
+          dst0 = sbase + stage * C::STAGE + ch * C::CHUNK + box * box_rows * 128;
+        }
         mbar_wait(&kv_empty[stage], ((it / NS) & 1) ^ 1);
-        if (lane == 0)
-          mbar_arrive_expect_tx(&kv_full[stage], static_cast<uint32_t>(nbox * C::NCH * box_rows * 128));
+        if (trace && lane == 0 && it < kTraceTiles) trace[13 + 6 * it] = globaltimer();
+        if (lane == 0) mbar_arrive_expect_tx(&kv_full[stage], static_cast<uint32_t>(nitem * box_rows * 128));
         __syncwarp();
-        for (int bx = lane; bx < nbox * C::NCH; bx += 32) {
+        if (lane < nitem) tma_load_2d(dst0, &tmap, &kv_full[stage], col0, row0);
+        for (int bx = lane + 32; bx < nitem; bx += 32) {  // small pages: more boxes than lanes
           const int box = bx / C::NCH, ch = bx - box * C::NCH;
           const int pos = p0 + box * box_rows;
-          const int page = bx == lane ? page0 : __ldg(bt_row + (pos >> p.log2_page));
+          const int page = __ldg(bt_row + (pos >> p.log2_page));
           const int row = page * p.page_size + (pos & (p.page_size - 1));
           const int col = ch < C::NCH_V ? s.head * p.d_head + ch * 64 : p.rope_col;
-          const uint32_t dst = sbase + stage * C::STAGE + ch * C::CHUNK + box * box_rows * 128;
-          tma_load_2d(dst, &tmap, &kv_full[stage], col, row);
+          tma_load_2d(sbase + stage * C::STAGE + ch * C::CHUNK + box * box_rows * 128, &tmap, &kv_full[stage], col,
+                      row);
         }
-        if (trace && lane == 0 && it < kTraceTiles) trace[8 + 5 * it] = globaltimer();
+        if (trace && lane == 0 && it < kTraceTiles) trace[8 + 6 * it] = globaltimer();
+        if (pvalid) {  // L2 prefetch of tile it + NS, after the stage load so it never delays it
+          issue_tile(ps, ptl, 0, true, -1);
+          pf_advance();
+        }
       }
     }
   } else if (warp == 1) {
@@ -455,24 +509,27 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
       };
       bool qk_left = advance(cq), pv_left = advance(cp);
       int next_qk = 0, next_pv = 0;
+      // Descriptors are built once per stage / Q buffer; each MMA only adds a
+      // compile-time byte offset (>> 4) to the start-address field, so the
+      // single issuing thread spends ~1 instruction per tcgen05.mma on them.
       auto issue_qk = [&]() {
         const int stage = next_qk % NS;
         const int sb = next_qk & 1;
         tc_fence_after();
         const uint32_t d = tmem + sb * NQ;
-        const uint32_t kv = sbase + stage * C::STAGE;
-        const uint32_t q_base = sbase + C::OFF_Q + (cq.seg % C::NQB) * C::QBYTES;
+        const uint64_t ad = desc_kmajor_sw128(sbase + stage * C::STAGE);
+        const uint64_t bd = desc_kmajor_sw128(sbase + C::OFF_Q + (cq.seg % C::NQB) * C::QBYTES);
 #pragma unroll
         for (int c = 0; c < C::NCH_QK; ++c) {
 #pragma unroll
           for (int k = 0; k < 4; ++k)
-            umma_f16_ss(d, desc_kmajor_sw128(kv + c * C::CHUNK + k * 32),
-                        desc_kmajor_sw128(q_base + c * C::QCHUNK + k * 32), idesc_qk, (c | k) != 0);
+            umma_f16_ss(d, ad + static_cast<uint64_t>((c * C::CHUNK + k * 32) >> 4),
+                        bd + static_cast<uint64_t>((c * C::QCHUNK + k * 32) >> 4), idesc_qk, (c | k) != 0);
         }
 #pragma unroll
         for (int k = 0; k < C::RK; ++k)
-          umma_f16_ss(d, desc_kmajor_sw128(kv + C::NCH_V * C::CHUNK + k * 32),
-                      desc_kmajor_sw128(q_base + C::NCH_QK * C::QCHUNK + k * 32), idesc_qk, 1u);
+          umma_f16_ss(d, ad + static_cast<uint64_t>((C::NCH_V * C::CHUNK + k * 32) >> 4),
+                      bd + static_cast<uint64_t>((C::NCH_QK * C::QCHUNK + k * 32) >> 4), idesc_qk, 1u);
         umma_commit(&s_full[sb]);
         if (cq.tl + 1 == cq.t1) umma_commit(&q_empty[cq.seg % C::NQB]);  // last QK of the segment: Q free
       };
@@ -481,15 +538,18 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
         const int j = next_pv;
         const int stage = j % NS;
         const uint32_t kv = sbase + stage * C::STAGE;
-        const uint32_t pt = kv + C::NCH_V * C::CHUNK;
+        const uint64_t ad = desc_mnmajor_sw128(kv, C::CHUNK);
+        const uint64_t bd = C::P_SW128 ? desc_mnmajor_sw128(kv + C::NCH_V * C::CHUNK, 0)
+                                       : desc_mnmajor_noswz(kv + C::NCH_V * C::CHUNK, 128, 2048);
         const uint32_t obuf = tmem + C::TMEM_O + (cp.seg & 1) * C::OCOLS;
         const bool first = (cp.tl == cp.t0);
 #pragma unroll
         for (int blk = 0; blk < C::NBLK_O; ++blk) {
 #pragma unroll
           for (int k = 0; k < T / 16; ++k)
-            umma_f16_ss(obuf + blk * NQ, desc_mnmajor_sw128(kv + 2 * blk * C::CHUNK + k * 2048, C::CHUNK),
-                        desc_mnmajor_noswz(pt + k * 256, 128, 2048), idesc_pv, (!first || k > 0) ? 1u : 0u);
+            umma_f16_ss(obuf + blk * NQ, ad + static_cast<uint64_t>((2 * blk * C::CHUNK + k * 2048) >> 4),
+                        bd + static_cast<uint64_t>((C::P_SW128 ? k * 2048 : k * 256) >> 4), idesc_pv,
+                        (!first || k > 0) ? 1u : 0u);
         }
         umma_commit(&kv_empty[stage]);
         umma_commit(&pv_done[j & 3]);
@@ -501,20 +561,20 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
           // first PV of a segment reuses O buffer (seg & 1): its epilogue two segments ago must be done
           const bool first = (cp.tl == cp.t0);
           if (!first || cp.seg < 2 || mbar_test_wait(smem_u32(&o_empty[cp.seg & 1]), ((cp.seg - 2) >> 1) & 1)) {
-            if (trace && next_pv < kTraceTiles) trace[12 + 5 * next_pv] = globaltimer();
+            if (trace && next_pv < kTraceTiles) trace[12 + 6 * next_pv] = globaltimer();
             issue_pv();
             ++next_pv;
             pv_left = advance(cp);
             did = true;
           }
         }
-        if (!did && qk_left && next_qk < next_pv + 2 &&
+        if (!did && qk_left &&
             mbar_test_wait(smem_u32(&kv_full[next_qk % NS]), (next_qk / NS) & 1) &&
             mbar_test_wait(smem_u32(&s_empty[next_qk & 1]), ((next_qk >> 1) & 1) ^ 1)) {
           const bool first = (cq.tl == cq.t0);
           if (!first || mbar_test_wait(smem_u32(&q_full[cq.seg % C::NQB]), (cq.seg / C::NQB) & 1)) {
             if (trace && next_qk == 0) trace[1] = globaltimer();
-            if (trace && next_qk < kTraceTiles) trace[9 + 5 * next_qk] = globaltimer();
+            if (trace && next_qk < kTraceTiles) trace[9 + 6 * next_qk] = globaltimer();
             issue_qk();
             ++next_qk;
             qk_left = advance(cq);
@@ -618,7 +678,7 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
         const int sb = it & 1;
         mbar_wait(&s_full[sb], (it >> 1) & 1);
         tc_fence_after();
-        if (trace && threadIdx.x == 128 && it < kTraceTiles) trace[10 + 5 * it] = globaltimer();
+        if (trace && threadIdx.x == 128 && it < kTraceTiles) trace[10 + 6 * it] = globaltimer();
         float x[CW];  // raw scores q.k for this thread's token, this WG's query columns
         tmem_load_cols<C>(tmem + lane_addr + sb * NQ + c0, x);
         tmem_ld_wait();
@@ -695,7 +755,10 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
         // p = 2^(s*c - m): bf16 P^T into the tile's (now dead) RoPE chunk,
         // MN-major no-swizzle [NQ/8][128 tok][8]
         const uint32_t stage_base = sbase + (it % NS) * C::STAGE;
-        const uint32_t pt = stage_base + C::NCH_V * C::CHUNK + (c0 / 8) * 2048 + r * 16;
+        // P^T layout: NQ = 64 -> MN-major 128B-swizzled rows of 64 queries
+        // (token r at r*128, 16-B chunk j at j ^ (r & 7)); else no-swizzle
+        // core matrices [NQ/8][128 tok][8].
+        const uint32_t pbase = stage_base + C::NCH_V * C::CHUNK;
 #pragma unroll
         for (int g = 0; g < CW / 8; ++g) {
           const float4 ma = ld_shared_f4(m_addr + g * 32);
@@ -708,11 +771,15 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
             const float m1 = mv[k + 1] == -INFINITY ? 0.f : mv[k + 1];
             const __nv_bfloat162 v =
                 __floats2bfloat162_rn(ex2(fmaf(x[g * 8 + k], sl2, -m0)), ex2(fmaf(x[g * 8 + k + 1], sl2, -m1)));
+            // row sum from the bf16-rounded p the PV multiplies (numerator and
+            // denominator consistent; the fp32 sum failed the peaked parity case)
             l[g * 8 + k] += __low2float(v);
             l[g * 8 + k + 1] += __high2float(v);
             pk[k / 2] = *reinterpret_cast<const uint32_t*>(&v);
           }
-          st_shared_v4(pt + g * 2048, pk[0], pk[1], pk[2], pk[3]);
+          const int j = c0 / 8 + g;
+          const uint32_t pa = C::P_SW128 ? pbase + r * 128 + ((j ^ (r & 7)) << 4) : pbase + j * 2048 + r * 16;
+          st_shared_v4(pa, pk[0], pk[1], pk[2], pk[3]);
         }
         if (wg == 0 && tok >= s.kv_end) {  // never-visible rows: zero V so 0 * garbage cannot give NaN
           const uint32_t kvrow = stage_base + r * 128;
@@ -725,7 +792,7 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&p_full[it % NS]);
-        if (trace && threadIdx.x == 128 && it < kTraceTiles) trace[11 + 5 * it] = globaltimer();
+        if (trace && threadIdx.x == 128 && it < kTraceTiles) trace[11 + 6 * it] = globaltimer();
       }
 
       // ------------------------------------------------------- segment epilogue

@@ -1,0 +1,22 @@
+"""Cycles per tcgen05.mma (M=128, K=16) for the decode kernel's operand layouts."""
+import ctypes
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+from paper_2505_21487_b200 import glad  # noqa: E402
+
+lib = glad.lib()
+lib.glad_debug_mma_bench.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_void_p]
+out = torch.zeros(2, dtype=torch.int64, device="cuda")
+names = {0: "A K-SW128 / B K-SW128 (QK)", 1: "A MN-SW128 / B MN-noswz (PV now)", 2: "A MN-SW128 / B MN-SW128",
+         3: "A MN-SW128 / B K-SW128"}
+for n in (16, 64, 128):
+    for w in range(4):
+        assert lib.glad_debug_mma_bench(w, n, 2000, ctypes.c_void_p(out.data_ptr())) == 0
+        torch.cuda.synchronize()
+        cyc, cnt = out.tolist()
+        ideal = max(128, 128) * n / 256
+        print(f"N={n:3d} {names[w]:34s} {cyc / cnt:7.1f} cycles/MMA (dense-rate floor {ideal:.0f})")

@@ -42,8 +42,8 @@ t0 = tr[:, 0].min()
 print(f"{wl.name}: segments/CTA {np.median(tr[:, 3]):.1f}, {len(tr)} CTAs, kernel span {(tr[:, 2].max() - t0) / 1e3:.1f} us")
 print(f"CTA lifetime median {np.median(tr[:, 2] - tr[:, 0]) / 1e3:.1f} us, start->Q ready "
       f"{np.median(tr[:, 1] - tr[:, 0]) / 1e3:.2f} us")
-T = (tr.shape[1] - 8) // 5
-tile = tr[:, 8:].reshape(len(tr), T, 5)  # load, qk, s, p, pv
+T = (tr.shape[1] - 8) // 6
+tile = tr[:, 8:].reshape(len(tr), T, 6)  # load, qk, s, p, pv, free
 valid = tile[:, :, 1] > 0
 ntile = valid.sum(1)
 
@@ -61,6 +61,9 @@ print(f"  QK->S     {med(tile[:, :, 2] - tile[:, :, 1], m):8.0f}")
 print(f"  S->P      {med(tile[:, :, 3] - tile[:, :, 2], m):8.0f}")
 print(f"  P->PV     {med(tile[:, :, 4] - tile[:, :, 3], m):8.0f}")
 ns = a.ns
+pv_to_free = tile[:, ns:, 5] - tile[:, :-ns, 4]
+print(f"  free(i+{ns})-PV(i) {med(pv_to_free, valid[:, ns:] & valid[:, :-ns]):8.0f}")
+print(f"  load-free  {med(tile[:, :, 0] - tile[:, :, 5], m):8.0f}")
 pv_to_load = tile[:, :-ns, 4] - tile[:, ns:, 0]
 mm = valid[:, ns:] & valid[:, :-ns]
 print(f"  load(i+{ns})-PV(i) {med(-pv_to_load, mm):8.0f}")
@@ -70,3 +73,13 @@ first = tile[:, 0]
 print(f"  first tile: start->load {np.median(first[:, 0] - tr[:, 0]):.0f}  load->QK {np.median(first[:, 1] - first[:, 0]):.0f}")
 last = np.array([tile[i, ntile[i] - 1, 4] for i in range(len(tr))])
 print(f"  last PV issue -> CTA end {np.median(tr[:, 2] - last):.0f}")
+
+if os.environ.get("TRACE_RAW"):
+    c = int(os.environ.get("TRACE_CTA", "5"))
+    base = tr[c, 0]
+    print(f"raw timeline of CTA {c} (us from CTA start): free, load, QK, S, P, PV")
+    for i in range(8, 24):
+        if tile[c, i, 1] == 0:
+            break
+        print(f"  tile {i:2d}: " + "  ".join(f"{(tile[c, i, j] - base) / 1e3:8.2f}" if tile[c, i, j] else "       -"
+                                          for j in (5, 0, 1, 2, 3, 4)))
