@@ -68,10 +68,11 @@ struct DecodeParams {
 };
 // Debug timeline layout per CTA (globaltimer ns): [0] start, [1] first QK,
 // [2] end, [3] number of segments, then per tile i < kTraceTiles: [8+6i] load
-// issued, [9+6i] QK issued, [10+6i] S seen by softmax, [11+6i] P written,
-// [12+6i] PV issued, [13+6i] stage free seen by the producer (before load i).
+// issued, [9+7i] QK issued, [10+7i] S seen by softmax, [11+7i] P written (WG0),
+// [12+7i] PV issued, [13+7i] stage free seen by the producer (before load i),
+// [14+7i] P written by the second softmax warpgroup.
 constexpr int kTraceTiles = 64;
-constexpr int kTraceStride = 8 + 6 * kTraceTiles;
+constexpr int kTraceStride = 8 + 7 * kTraceTiles;
 
 template <int D_V_, int D_KN_, int D_R_, int NQ_>
 struct DecodeCfg {
@@ -466,7 +467,7 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
           dst0 = sbase + stage * C::STAGE + ch * C::CHUNK + box * box_rows * 128;
         }
         mbar_wait(&kv_empty[stage], ((it / NS) & 1) ^ 1);
-        if (trace && lane == 0 && it < kTraceTiles) trace[13 + 6 * it] = globaltimer();
+        if (trace && lane == 0 && it < kTraceTiles) trace[13 + 7 * it] = globaltimer();
         if (lane == 0) mbar_arrive_expect_tx(&kv_full[stage], static_cast<uint32_t>(nitem * box_rows * 128));
         __syncwarp();
         if (lane < nitem) tma_load_2d(dst0, &tmap, &kv_full[stage], col0, row0);
@@ -479,7 +480,7 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
           tma_load_2d(sbase + stage * C::STAGE + ch * C::CHUNK + box * box_rows * 128, &tmap, &kv_full[stage], col,
                       row);
         }
-        if (trace && lane == 0 && it < kTraceTiles) trace[8 + 6 * it] = globaltimer();
+        if (trace && lane == 0 && it < kTraceTiles) trace[8 + 7 * it] = globaltimer();
         if (pvalid) {  // L2 prefetch of tile it + NS, after the stage load so it never delays it
           issue_tile(ps, ptl, 0, true, -1);
           pf_advance();
@@ -561,7 +562,7 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
           // first PV of a segment reuses O buffer (seg & 1): its epilogue two segments ago must be done
           const bool first = (cp.tl == cp.t0);
           if (!first || cp.seg < 2 || mbar_test_wait(smem_u32(&o_empty[cp.seg & 1]), ((cp.seg - 2) >> 1) & 1)) {
-            if (trace && next_pv < kTraceTiles) trace[12 + 6 * next_pv] = globaltimer();
+            if (trace && next_pv < kTraceTiles) trace[12 + 7 * next_pv] = globaltimer();
             issue_pv();
             ++next_pv;
             pv_left = advance(cp);
@@ -574,7 +575,7 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
           const bool first = (cq.tl == cq.t0);
           if (!first || mbar_test_wait(smem_u32(&q_full[cq.seg % C::NQB]), (cq.seg / C::NQB) & 1)) {
             if (trace && next_qk == 0) trace[1] = globaltimer();
-            if (trace && next_qk < kTraceTiles) trace[9 + 6 * next_qk] = globaltimer();
+            if (trace && next_qk < kTraceTiles) trace[9 + 7 * next_qk] = globaltimer();
             issue_qk();
             ++next_qk;
             qk_left = advance(cq);
@@ -583,9 +584,14 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
         }
         if (did) {
           t0 = clock64();
-        } else if (clock64() - t0 > (1ll << 34)) {
-          printf("glad: MMA scheduler watchdog (cta %d qk %d pv %d)\n", cta, next_qk, next_pv);
-          __trap();
+        } else {
+          // back off: this thread shares its SM sub-partition with two softmax
+          // warps; a tight test_wait loop steals their issue slots
+          __nanosleep(40);
+          if (clock64() - t0 > (1ll << 34)) {
+            printf("glad: MMA scheduler watchdog (cta %d qk %d pv %d)\n", cta, next_qk, next_pv);
+            __trap();
+          }
         }
       }
       if (trace) trace[3] = cp.seg + 1;
@@ -678,7 +684,7 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
         const int sb = it & 1;
         mbar_wait(&s_full[sb], (it >> 1) & 1);
         tc_fence_after();
-        if (trace && threadIdx.x == 128 && it < kTraceTiles) trace[10 + 6 * it] = globaltimer();
+        if (trace && threadIdx.x == 128 && it < kTraceTiles) trace[10 + 7 * it] = globaltimer();
         float x[CW];  // raw scores q.k for this thread's token, this WG's query columns
         tmem_load_cols<C>(tmem + lane_addr + sb * NQ + c0, x);
         tmem_ld_wait();
@@ -792,7 +798,8 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&p_full[it % NS]);
-        if (trace && threadIdx.x == 128 && it < kTraceTiles) trace[11 + 6 * it] = globaltimer();
+        if (trace && threadIdx.x == 128 && it < kTraceTiles) trace[11 + 7 * it] = globaltimer();
+        if (trace && threadIdx.x == 256 && it < kTraceTiles) trace[14 + 7 * it] = globaltimer();
       }
 
       // ------------------------------------------------------- segment epilogue

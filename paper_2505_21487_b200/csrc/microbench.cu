@@ -45,11 +45,13 @@ __global__ void __launch_bounds__(128, 1) mma_bench_kernel(int which, int iters,
         umma_f16_ss(tmem, a, b, idesc, (it | k) != 0);
       }
     }
+    const long long ti = clock64();
     umma_commit(&bar);
     mbar_wait(&bar, 0);
     const long long t1 = clock64();
     out[0] = t1 - t0;
     out[1] = static_cast<long long>(iters) * 16;
+    out[2] = ti - t0;  // time spent issuing (blocks when the MMA queue is full)
   }
   tc_fence_before();
   __syncthreads();

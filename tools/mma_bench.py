@@ -10,13 +10,19 @@ from paper_2505_21487_b200 import glad  # noqa: E402
 
 lib = glad.lib()
 lib.glad_debug_mma_bench.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_void_p]
-out = torch.zeros(2, dtype=torch.int64, device="cuda")
+out = torch.zeros(3, dtype=torch.int64, device="cuda")
 names = {0: "A K-SW128 / B K-SW128 (QK)", 1: "A MN-SW128 / B MN-noswz (PV now)", 2: "A MN-SW128 / B MN-SW128",
          3: "A MN-SW128 / B K-SW128"}
+for iters in (1, 2, 2000):
+    for w in (0, 1):
+        assert lib.glad_debug_mma_bench(w, 64, iters, ctypes.c_void_p(out.data_ptr())) == 0
+        torch.cuda.synchronize()
+        cyc, cnt, iss = out.tolist()
+        print(f"{cnt:6d} MMAs N=64 {names[w]:34s} total {cyc:8d} cycles, issue loop {iss:8d} cycles")
 for n in (16, 64, 128):
     for w in range(4):
         assert lib.glad_debug_mma_bench(w, n, 2000, ctypes.c_void_p(out.data_ptr())) == 0
         torch.cuda.synchronize()
-        cyc, cnt = out.tolist()
+        cyc, cnt, iss = out.tolist()
         ideal = max(128, 128) * n / 256
         print(f"N={n:3d} {names[w]:34s} {cyc / cnt:7.1f} cycles/MMA (dense-rate floor {ideal:.0f})")

@@ -42,8 +42,8 @@ t0 = tr[:, 0].min()
 print(f"{wl.name}: segments/CTA {np.median(tr[:, 3]):.1f}, {len(tr)} CTAs, kernel span {(tr[:, 2].max() - t0) / 1e3:.1f} us")
 print(f"CTA lifetime median {np.median(tr[:, 2] - tr[:, 0]) / 1e3:.1f} us, start->Q ready "
       f"{np.median(tr[:, 1] - tr[:, 0]) / 1e3:.2f} us")
-T = (tr.shape[1] - 8) // 6
-tile = tr[:, 8:].reshape(len(tr), T, 6)  # load, qk, s, p, pv, free
+T = (tr.shape[1] - 8) // 7
+tile = tr[:, 8:].reshape(len(tr), T, 7)  # load, qk, s, p, pv, free, p_wg1
 valid = tile[:, :, 1] > 0
 ntile = valid.sum(1)
 
@@ -60,6 +60,8 @@ print(f"  load->QK  {med(tile[:, :, 1] - tile[:, :, 0], m):8.0f}")
 print(f"  QK->S     {med(tile[:, :, 2] - tile[:, :, 1], m):8.0f}")
 print(f"  S->P      {med(tile[:, :, 3] - tile[:, :, 2], m):8.0f}")
 print(f"  P->PV     {med(tile[:, :, 4] - tile[:, :, 3], m):8.0f}")
+print(f"  P(WG1)-P(WG0) {med(tile[:, :, 6] - tile[:, :, 3], m):8.0f}")
+print(f"  P(WG1)->PV {med(tile[:, :, 4] - tile[:, :, 6], m):8.0f}")
 ns = a.ns
 pv_to_free = tile[:, ns:, 5] - tile[:, :-ns, 4]
 print(f"  free(i+{ns})-PV(i) {med(pv_to_free, valid[:, ns:] & valid[:, :-ns]):8.0f}")
@@ -77,9 +79,9 @@ print(f"  last PV issue -> CTA end {np.median(tr[:, 2] - last):.0f}")
 if os.environ.get("TRACE_RAW"):
     c = int(os.environ.get("TRACE_CTA", "5"))
     base = tr[c, 0]
-    print(f"raw timeline of CTA {c} (us from CTA start): free, load, QK, S, P, PV")
+    print(f"raw timeline of CTA {c} (us from CTA start): free, load, QK, S, P0, P1, PV")
     for i in range(8, 24):
         if tile[c, i, 1] == 0:
             break
         print(f"  tile {i:2d}: " + "  ".join(f"{(tile[c, i, j] - base) / 1e3:8.2f}" if tile[c, i, j] else "       -"
-                                          for j in (5, 0, 1, 2, 3, 4)))
+                                          for j in (5, 0, 1, 2, 3, 6, 4)))
