@@ -112,7 +112,10 @@ struct DecodeCfg {
   static constexpr int SMEM_BYTES = 1024 + OFF_AUX + AUX;
   static constexpr int OCOLS = NBLK_O * NQ;      // one O^T accumulator
   static constexpr int TMEM_O = 2 * NQ;          // after the two S^T buffers
-  static constexpr int TMEM_USED = 2 * NQ + 2 * OCOLS;
+  // two O buffers (the next unit's first PV overlaps this unit's epilogue)
+  // when TMEM allows, else one (MLA d_c = 512 with 64 rows)
+  static constexpr int NOB = (2 * NQ + 2 * OCOLS <= 512) ? 2 : 1;
+  static constexpr int TMEM_USED = 2 * NQ + NOB * OCOLS;
   static constexpr int TMEM_COLS =
       TMEM_USED <= 32 ? 32 : TMEM_USED <= 64 ? 64 : TMEM_USED <= 128 ? 128 : TMEM_USED <= 256 ? 256 : 512;
   static constexpr int NTHREADS = 384;
@@ -542,7 +545,7 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
         const uint64_t ad = desc_mnmajor_sw128(kv, C::CHUNK);
         const uint64_t bd = C::P_SW128 ? desc_mnmajor_sw128(kv + C::NCH_V * C::CHUNK, 0)
                                        : desc_mnmajor_noswz(kv + C::NCH_V * C::CHUNK, 128, 2048);
-        const uint32_t obuf = tmem + C::TMEM_O + (cp.seg & 1) * C::OCOLS;
+        const uint32_t obuf = tmem + C::TMEM_O + (cp.seg % C::NOB) * C::OCOLS;
         const bool first = (cp.tl == cp.t0);
 #pragma unroll
         for (int blk = 0; blk < C::NBLK_O; ++blk) {
@@ -559,9 +562,11 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
       while (pv_left) {
         bool did = false;
         if (next_pv < next_qk && mbar_test_wait(smem_u32(&p_full[next_pv % NS]), (next_pv / NS) & 1)) {
-          // first PV of a segment reuses O buffer (seg & 1): its epilogue two segments ago must be done
+          // first PV of a segment reuses O buffer (seg % NOB): the epilogue of
+          // segment seg - NOB must have read it
           const bool first = (cp.tl == cp.t0);
-          if (!first || cp.seg < 2 || mbar_test_wait(smem_u32(&o_empty[cp.seg & 1]), ((cp.seg - 2) >> 1) & 1)) {
+          if (!first || cp.seg < C::NOB ||
+              mbar_test_wait(smem_u32(&o_empty[cp.seg % C::NOB]), ((cp.seg - C::NOB) / C::NOB) & 1)) {
             if (trace && next_pv < kTraceTiles) trace[12 + 7 * next_pv] = globaltimer();
             issue_pv();
             ++next_pv;
@@ -675,7 +680,7 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
       named_bar_sync(bar_id, 128);
       const int min_vend = p.causal ? max(0, min(s.L, s.L - p.Lq + s.n0 / p.g_q + 1)) : s.L;
       const bool all_cols = (s.nq == NQ);
-      const uint32_t obuf = tmem + C::TMEM_O + (seg & 1) * C::OCOLS;
+      const uint32_t obuf = tmem + C::TMEM_O + (seg % C::NOB) * C::OCOLS;
       float l[CW];
 #pragma unroll
       for (int n = 0; n < CW; ++n) l[n] = 0.f;
@@ -833,7 +838,7 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
         if (blk == C::NBLK_O - 1) {  // O buffer consumed: the segment after next may reuse it
           tc_fence_before();
           __syncwarp();
-          if (lane == 0) mbar_arrive(&o_empty[seg & 1]);
+          if (lane == 0) mbar_arrive(&o_empty[seg % C::NOB]);
         }
         const int d = blk * 128 + r;
 #pragma unroll

@@ -25,15 +25,14 @@ cudaError_t launch_nq(int nq, const CUtensorMap& tmap, const CUtensorMap& qmap, 
     case 16: return launch_one<DV, DKN, DR, 16>(tmap, qmap, p, grid, s);
     case 32: return launch_one<DV, DKN, DR, 32>(tmap, qmap, p, grid, s);
     case 64:
-      if constexpr (DV <= 256) return launch_one<DV, DKN, DR, 64>(tmap, qmap, p, grid, s);
-      else return cudaErrorInvalidValue;
+      return launch_one<DV, DKN, DR, 64>(tmap, qmap, p, grid, s);
     default: return cudaErrorInvalidValue;
   }
 }
 
 }  // namespace
 
-int decode_max_nq(int d_v) { return d_v <= 256 ? 64 : 32; }
+int decode_max_nq(int) { return 64; }
 
 bool decode_supported(const DecodeKey& k) {
   if (k.nq != 16 && k.nq != 32 && k.nq != 64) return false;
