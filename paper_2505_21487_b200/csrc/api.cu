@@ -78,6 +78,18 @@ int64_t row_width(const glad_cache_layout* L) {
 
 enum Variant { kGLA, kMLA, kGTA };
 
+int g_tile_override = 0;  // debug: force 64 / 128-token tiles (glad_debug_set_tile)
+
+// KV tile height.  64-token tiles (M = 64 QK) fit twice as many stages, but
+// measured slower on every BASELINE shape (C2 0.47 vs 0.36 ms, GTA 1.06 vs
+// 0.63 ms): QK then re-reads Q from smem per 64 tokens and the SS MMAs are
+// smem-read bound, so the tensor pipe becomes the bottleneck.  128 is the
+// default; 64 stays available (and tested) via glad_debug_set_tile.
+int tile_tokens(const glad::DecodeKey&) {
+  if (g_tile_override == 64 || g_tile_override == 128) return g_tile_override;
+  return 128;
+}
+
 struct DecodeGeom {
   glad::DecodeKey key;
   int g_q, n_qblk;
@@ -101,6 +113,7 @@ glad_status decode_geom(Variant v, const glad_cache_layout* L, int32_t Lq, int32
   const int64_t nq_total = static_cast<int64_t>(Lq) * g->g_q;
   const int maxnq = glad::decode_max_nq(L->d_head);
   g->key.nq = nq_total <= 16 ? 16 : nq_total <= 32 ? 32 : maxnq;
+  g->key.t = tile_tokens(g->key);
   g->n_qblk = static_cast<int>((nq_total + g->key.nq - 1) / g->key.nq);
   if (!glad::decode_supported(g->key))
     return fail(GLAD_ERR_UNSUPPORTED, "no decode kernel for d_head=%d d_rope=%d (variant %d, rows/CTA %d)",
@@ -158,7 +171,7 @@ glad_status decode_common(Variant v, const void* q, const void* pool, const glad
   auto enc = encode_fn();
   if (!enc) return fail(GLAD_ERR_CUDA, "cuTensorMapEncodeTiled entry point unavailable");
   CUtensorMap tmap;
-  const int box_rows = L->page_size < 128 ? L->page_size : 128;
+  const int box_rows = L->page_size < g.key.t ? L->page_size : g.key.t;
   cuuint64_t dims[2] = {static_cast<cuuint64_t>(row_width(L)),
                         static_cast<cuuint64_t>(L->num_pages) * static_cast<cuuint64_t>(L->page_size)};
   cuuint64_t strides[1] = {static_cast<cuuint64_t>(L->row_stride) * 2};
@@ -224,7 +237,7 @@ glad_status decode_common(Variant v, const void* q, const void* pool, const glad
   int32_t* plan = reinterpret_cast<int32_t*>(wsb + wl.plan);
   cudaError_t e = cudaSuccess;
   if (g_phase_mask & 1) {
-    e = glad::launch_plan(seqlens, plan, p.n_units, B, g.n_qblk, g.key.nq, Lq, g.g_q, p.causal, st);
+    e = glad::launch_plan(seqlens, plan, p.n_units, B, g.key.t, g.n_qblk, g.key.nq, Lq, g.g_q, p.causal, st);
     if (e != cudaSuccess) return fail(GLAD_ERR_CUDA, "plan launch failed: %s", cudaGetErrorString(e));
   }
   if (g_phase_mask & 2) {
@@ -251,6 +264,8 @@ const char* glad_version(void) { return "glad 0.1.0 sm_100a"; }
 void glad_debug_set_trace(void* device_buf) { g_trace = static_cast<uint64_t*>(device_buf); }
 
 void glad_debug_set_phase_mask(int32_t mask) { g_phase_mask = mask & 7; }
+
+void glad_debug_set_tile(int32_t tokens) { g_tile_override = tokens; }
 
 size_t glad_pool_bytes(const glad_cache_layout* L) {
   if (check_layout(L) != GLAD_OK) return 0;

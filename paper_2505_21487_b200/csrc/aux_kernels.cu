@@ -87,7 +87,7 @@ __global__ void combine_kernel(const float* __restrict__ o_part, const float* __
 
 // Decode schedule plan (one CTA): tiles per unit u = (b, head, query block)
 // -> exclusive prefix sum plan[0..U]; plan[U] = total tiles.
-__global__ void plan_kernel(const int32_t* __restrict__ seqlens, int32_t* __restrict__ plan, int U, int B,
+__global__ void plan_kernel(const int32_t* __restrict__ seqlens, int32_t* __restrict__ plan, int U, int B, int tile,
                             int n_qblk, int nq_blk, int Lq, int g_q, int causal) {
   __shared__ int warp_sums[32];
   __shared__ int carry;
@@ -105,7 +105,7 @@ __global__ void plan_kernel(const int32_t* __restrict__ seqlens, int32_t* __rest
       const int L = seqlens[b];
       int kv_end = L;
       if (causal) kv_end = max(0, min(L, L - Lq + (n0 + nq - 1) / g_q + 1));
-      tiles = (kv_end + 127) / 128;
+      tiles = (kv_end + tile - 1) / tile;
     }
     int v = tiles;  // inclusive warp scan
 #pragma unroll
@@ -198,9 +198,9 @@ __global__ void merge_units_kernel(const int32_t* __restrict__ plan, const float
   }
 }
 
-cudaError_t launch_plan(const int32_t* seqlens, int32_t* plan, int U, int B, int n_qblk, int nq_blk, int Lq,
+cudaError_t launch_plan(const int32_t* seqlens, int32_t* plan, int U, int B, int tile, int n_qblk, int nq_blk, int Lq,
                         int g_q, int causal, cudaStream_t stream) {
-  plan_kernel<<<1, 1024, 0, stream>>>(seqlens, plan, U, B, n_qblk, nq_blk, Lq, g_q, causal);
+  plan_kernel<<<1, 1024, 0, stream>>>(seqlens, plan, U, B, tile, n_qblk, nq_blk, Lq, g_q, causal);
   return cudaGetLastError();
 }
 

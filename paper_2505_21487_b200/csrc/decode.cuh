@@ -74,20 +74,21 @@ struct DecodeParams {
 constexpr int kTraceTiles = 64;
 constexpr int kTraceStride = 8 + 7 * kTraceTiles;
 
-template <int D_V_, int D_KN_, int D_R_, int NQ_>
+template <int D_V_, int D_KN_, int D_R_, int NQ_, int T_ = 128>
 struct DecodeCfg {
   static constexpr int D_V = D_V_;    // value width (= state width)
   static constexpr int D_KN = D_KN_;  // key part taken from the state
   static constexpr int D_R = D_R_;    // rope width
   static constexpr int NQ = NQ_;      // query rows per unit (UMMA N)
-  static constexpr int T = 128;       // tokens per tile (UMMA M)
+  static constexpr int T = T_;        // tokens per tile (UMMA M of QK: 128, or 64 = 40 KB GLA-2 stages)
+  static constexpr int LANES = T == 128 ? 32 : 16;  // token lanes per warp quarter in S^T (M=64: 16)
   static constexpr int DQ = D_KN + D_R;
   static constexpr int NCH_V = D_V / 64;
   static constexpr int NCH = NCH_V + 1;  // + rope chunk
   static constexpr int NCH_QK = D_KN / 64;
   static constexpr int NQCH = NCH_QK + 1;
   static constexpr int RK = D_R / 16;
-  static constexpr int CHUNK = T * 128;  // one [128 tokens x 64 cols] bf16 box set
+  static constexpr int CHUNK = T * 128;  // one [T tokens x 64 cols] bf16 box set
   static constexpr int STAGE = NCH * CHUNK;
   static constexpr int QCHUNK = NQ * 128;
   static constexpr int QBYTES = NQCH * QCHUNK;
@@ -99,6 +100,7 @@ struct DecodeCfg {
   static constexpr int NBLK_O = D_V / 128;
   static constexpr int NWG = 2;
   static constexpr int CW = NQ / NWG;
+  static constexpr int HC = T == 128 ? CW : CW / 2;  // columns per softmax thread (T=64: a thread pair per token)
   static constexpr int MAXSEG = 128;  // per-CTA segment table entries (aux + 3072)
   static constexpr int AUX = 3072 + MAXSEG * 16;
   static constexpr int AVAIL = 227 * 1024 - 1024 - AUX;
@@ -126,15 +128,17 @@ struct DecodeCfg {
   static_assert(NQ == 16 || NQ == 32 || NQ == 64, "NQ must be 16/32/64");
   static_assert(TMEM_USED <= 512, "TMEM budget");
   static_assert(QCHUNK % 1024 == 0, "Q chunk alignment");
+  static_assert(T == 128 || T == 64, "tile height");
 };
 
-// Column reduction of a warp: v[CW] per lane (lane = token) -> every lane
-// returns the reduction over the 32 lanes of column (lane >> (5 - log2 CW)).
-// Halving butterfly: CW-1 shuffles instead of 5*CW.
-template <int CW, bool MAX>
+// Column reduction over groups of LANES lanes (32, or 16 for the halves of a
+// warp): v[CW] per lane (lane = token) -> every lane returns the reduction
+// over its group of column ((lane % LANES) >> (log2 LANES - log2 CW)).
+// Halving butterfly: CW-1 shuffles instead of log2(LANES)*CW.
+template <int CW, bool MAX, int LANES = 32>
 __device__ __forceinline__ float warp_col_reduce(float (&v)[CW], int lane) {
-  static_assert(CW >= 2 && CW <= 32 && (CW & (CW - 1)) == 0, "CW");
-  int o = 16;
+  static_assert(CW >= 2 && CW <= LANES && (CW & (CW - 1)) == 0, "CW");
+  int o = LANES / 2;
 #pragma unroll
   for (int K = CW; K > 1; K >>= 1, o >>= 1) {
     const bool upper = (lane & o) != 0;
@@ -153,9 +157,9 @@ __device__ __forceinline__ float warp_col_reduce(float (&v)[CW], int lane) {
   }
   return v[0];
 }
-template <int CW>
+template <int CW, int LANES = 32>
 __device__ __forceinline__ constexpr int col_shift() {
-  return CW == 32 ? 0 : CW == 16 ? 1 : CW == 8 ? 2 : CW == 4 ? 3 : 4;
+  return (LANES == 32 ? 5 : 4) - (CW == 32 ? 5 : CW == 16 ? 4 : CW == 8 ? 3 : CW == 4 ? 2 : 1);
 }
 
 template <class C>
@@ -166,6 +170,20 @@ __device__ __forceinline__ void tmem_load_cols(uint32_t taddr, float (&x)[C::CW]
   } else {
 #pragma unroll
     for (int cc = 0; cc < C::CW; cc += 8) tmem_ld8(taddr + cc, x + cc);
+  }
+}
+// S^T columns of this thread: T = 128 -> 32x32b (CW columns); T = 64 -> the
+// two-half 16-lane load (HC = CW/2 columns each, thread pair per token).
+template <class C>
+__device__ __forceinline__ void tmem_load_s(uint32_t taddr, float (&x)[C::HC]) {
+  if constexpr (C::T == 128) {
+    tmem_load_cols<C>(taddr, x);
+  } else if constexpr (C::HC == 16) {
+    tmem_ld16x2_x16(taddr, x);
+  } else if constexpr (C::HC == 8) {
+    tmem_ld16x2_x8(taddr, x);
+  } else {
+    tmem_ld16x2_x4(taddr, x);
   }
 }
 template <class C>
@@ -493,7 +511,7 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
   } else if (warp == 1) {
     // ========================= UMMA issuer (one thread) =========================
     if (lane == 0) {
-      constexpr uint32_t idesc_qk = make_idesc_bf16(128, NQ, false, false);
+      constexpr uint32_t idesc_qk = make_idesc_bf16(T, NQ, false, false);
       constexpr uint32_t idesc_pv = make_idesc_bf16(128, NQ, true, true);
       // The QK stream and the PV stream walk the CTA's tiles with separate
       // cursors (segment, tile within unit).
@@ -544,7 +562,7 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
         const uint32_t kv = sbase + stage * C::STAGE;
         const uint64_t ad = desc_mnmajor_sw128(kv, C::CHUNK);
         const uint64_t bd = C::P_SW128 ? desc_mnmajor_sw128(kv + C::NCH_V * C::CHUNK, 0)
-                                       : desc_mnmajor_noswz(kv + C::NCH_V * C::CHUNK, 128, 2048);
+                                       : desc_mnmajor_noswz(kv + C::NCH_V * C::CHUNK, 128, T * 16);
         const uint32_t obuf = tmem + C::TMEM_O + (cp.seg % C::NOB) * C::OCOLS;
         const bool first = (cp.tl == cp.t0);
 #pragma unroll
@@ -651,15 +669,24 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
     if (seg == 0) named_bar_arrive(3, 96);  // no work: release the producer
   } else {
     // ========================= softmax / correction / epilogue =========================
+    // Thread -> data: T = 128: token tr = 32*wq + lane, columns [c0, c0 + CW).
+    // T = 64 (M = 64 S^T: 16 lanes per quarter): token tr = 16*wq + lane % 16,
+    // columns [cb, cb + HC) with cb = c0 + (lane / 16) * HC.  O^T (M = 128) is
+    // always one d row per TMEM lane r = 32*wq + lane.
+    constexpr int HC = C::HC, LANES = C::LANES;
     const int wg = (warp - 4) >> 2;
     const int wq = warp & 3;
-    const int r = wq * 32 + lane;  // TMEM lane: token row of S^T, d row of O^T
+    const int r = wq * 32 + lane;  // TMEM lane of O^T (d row)
+    const int half = T == 128 ? 0 : (lane >> 4);
+    const int tr = T == 128 ? r : wq * 16 + (lane & 15);  // token row of S^T within the tile
     const int c0 = wg * CW;
+    const int cb = c0 + half * HC;
     const uint32_t lane_addr = static_cast<uint32_t>(wq * 32) << 16;
     const uint32_t bar_id = 1 + wg;
-    const uint32_t m_addr = smem_u32(m_run + c0);
-    const uint32_t t_addr = smem_u32(thr_s + c0);
-    const uint32_t a_addr = smem_u32(alpha_s + c0);
+    const uint32_t m_addr = smem_u32(m_run + cb);
+    const uint32_t t_addr = smem_u32(thr_s + cb);
+    const uint32_t a_addr = smem_u32(alpha_s + cb);
+    const uint32_t ao_addr = smem_u32(alpha_s + c0);  // O^T rescale: all CW columns of the WG
     const float sl2 = p.scale_log2;
     const float inv_sl2 = 1.f / sl2;
     int k = 0, u = 0, seg = 0, it = 0;
@@ -681,49 +708,51 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
       const int min_vend = p.causal ? max(0, min(s.L, s.L - p.Lq + s.n0 / p.g_q + 1)) : s.L;
       const bool all_cols = (s.nq == NQ);
       const uint32_t obuf = tmem + C::TMEM_O + (seg % C::NOB) * C::OCOLS;
-      float l[CW];
+      float l[HC];
 #pragma unroll
-      for (int n = 0; n < CW; ++n) l[n] = 0.f;
+      for (int n = 0; n < HC; ++n) l[n] = 0.f;
 
       for (int tl = s.t0; tl < s.t1; ++tl, ++it) {
         const int sb = it & 1;
         mbar_wait(&s_full[sb], (it >> 1) & 1);
         tc_fence_after();
         if (trace && threadIdx.x == 128 && it < kTraceTiles) trace[10 + 7 * it] = globaltimer();
-        float x[CW];  // raw scores q.k for this thread's token, this WG's query columns
-        tmem_load_cols<C>(tmem + lane_addr + sb * NQ + c0, x);
+        float x[HC];  // raw scores q.k for this thread's token and columns
+        tmem_load_s<C>(tmem + lane_addr + sb * NQ + c0, x);
         tmem_ld_wait();
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&s_empty[sb]);
 
         const int p0 = tl * T;
-        const int tok = p0 + r;
+        const int tok = p0 + tr;
         if (!(p0 + T <= min_vend && all_cols)) {  // masked tile (last tile / causal / padded columns)
 #pragma unroll
-          for (int n = 0; n < CW; ++n) {
-            const bool ok = (c0 + n < s.nq) && tok < vend_s[c0 + n];
+          for (int n = 0; n < HC; ++n) {
+            const bool ok = (cb + n < s.nq) && tok < vend_s[cb + n];
             x[n] = ok ? x[n] : -INFINITY;
           }
         }
         bool need = false;
+        if constexpr (HC >= 4) {
 #pragma unroll
-        for (int n = 0; n < CW; n += 4) {
-          const float4 th = ld_shared_f4(t_addr + n * 4);
-          need |= (x[n] > th.x) | (x[n + 1] > th.y) | (x[n + 2] > th.z) | (x[n + 3] > th.w);
+          for (int n = 0; n < HC; n += 4) {
+            const float4 th = ld_shared_f4(t_addr + n * 4);
+            need |= (x[n] > th.x) | (x[n + 1] > th.y) | (x[n + 2] > th.z) | (x[n + 3] > th.w);
+          }
         }
         if (named_bar_red_or(bar_id, 128, need)) {
           // the running max moves by > 2^TAU somewhere: column max over the WG
-          // (in halves of <= 16 columns to bound register pressure)
-          constexpr int HW = CW > 16 ? 16 : CW;
+          // (in pieces of <= 16 columns to bound register pressure)
+          constexpr int HW = HC > 16 ? 16 : HC;
 #pragma unroll
-          for (int h0 = 0; h0 < CW; h0 += HW) {
+          for (int h0 = 0; h0 < HC; h0 += HW) {
             float tmp[HW];
 #pragma unroll
             for (int n = 0; n < HW; ++n) tmp[n] = x[h0 + n];
-            const float cm = warp_col_reduce<HW, true>(tmp, lane);
-            if ((lane & ((1 << col_shift<HW>()) - 1)) == 0)
-              red[(wg * 4 + wq) * 32 + h0 + (lane >> col_shift<HW>())] = cm;
+            const float cm = warp_col_reduce<HW, true, LANES>(tmp, lane);
+            if ((lane & ((1 << col_shift<HW, LANES>()) - 1)) == 0)
+              red[(wg * 4 + wq) * 32 + (cb - c0) + h0 + ((lane & (LANES - 1)) >> col_shift<HW, LANES>())] = cm;
           }
           named_bar_sync(bar_id, 128);
           if (r < CW) {
@@ -739,9 +768,13 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
           bool any_scale = false;
 #pragma unroll
           for (int n = 0; n < CW; n += 4) {
+            const float4 a = ld_shared_f4(ao_addr + n * 4);
+            any_scale |= (a.x != 1.f) | (a.y != 1.f) | (a.z != 1.f) | (a.w != 1.f);
+          }
+#pragma unroll
+          for (int n = 0; n < HC; n += 4) {
             const float4 a = ld_shared_f4(a_addr + n * 4);
             l[n] *= a.x; l[n + 1] *= a.y; l[n + 2] *= a.z; l[n + 3] *= a.w;
-            any_scale |= (a.x != 1.f) | (a.y != 1.f) | (a.z != 1.f) | (a.w != 1.f);
           }
           if (tl > s.t0 && any_scale) {  // rescale this WG's O^T columns in TMEM
             const int j = it - 1;
@@ -755,7 +788,7 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
               tmem_ld_wait();
 #pragma unroll
               for (int n = 0; n < CW; n += 4) {
-                const float4 a = ld_shared_f4(a_addr + n * 4);
+                const float4 a = ld_shared_f4(ao_addr + n * 4);
                 o[n] *= a.x; o[n + 1] *= a.y; o[n + 2] *= a.z; o[n + 3] *= a.w;
               }
               tmem_store_cols<C>(ta, o);
@@ -763,37 +796,54 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
             tmem_st_wait();
           }
         }
-        // p = 2^(s*c - m): bf16 P^T into the tile's (now dead) RoPE chunk,
-        // MN-major no-swizzle [NQ/8][128 tok][8]
+        // p = 2^(s*c - m): bf16 P^T into the tile's (now dead) RoPE chunk.
+        // NQ = 64: MN-major 128B-swizzled rows of 64 queries (token tr at
+        // tr*128, 16-B chunk j at j ^ (tr & 7)); else no-swizzle core
+        // matrices [NQ/8][T tok][8].
         const uint32_t stage_base = sbase + (it % NS) * C::STAGE;
-        // P^T layout: NQ = 64 -> MN-major 128B-swizzled rows of 64 queries
-        // (token r at r*128, 16-B chunk j at j ^ (r & 7)); else no-swizzle
-        // core matrices [NQ/8][128 tok][8].
         const uint32_t pbase = stage_base + C::NCH_V * C::CHUNK;
+        if constexpr (HC >= 8) {
 #pragma unroll
-        for (int g = 0; g < CW / 8; ++g) {
-          const float4 ma = ld_shared_f4(m_addr + g * 32);
-          const float4 mb = ld_shared_f4(m_addr + g * 32 + 16);
-          const float mv[8] = {ma.x, ma.y, ma.z, ma.w, mb.x, mb.y, mb.z, mb.w};
-          uint32_t pk[4];
+          for (int g = 0; g < HC / 8; ++g) {
+            const float4 ma = ld_shared_f4(m_addr + g * 32);
+            const float4 mb = ld_shared_f4(m_addr + g * 32 + 16);
+            const float mv[8] = {ma.x, ma.y, ma.z, ma.w, mb.x, mb.y, mb.z, mb.w};
+            uint32_t pk[4];
 #pragma unroll
-          for (int k = 0; k < 8; k += 2) {
-            const float m0 = mv[k] == -INFINITY ? 0.f : mv[k];
-            const float m1 = mv[k + 1] == -INFINITY ? 0.f : mv[k + 1];
-            const __nv_bfloat162 v =
-                __floats2bfloat162_rn(ex2(fmaf(x[g * 8 + k], sl2, -m0)), ex2(fmaf(x[g * 8 + k + 1], sl2, -m1)));
-            // row sum from the bf16-rounded p the PV multiplies (numerator and
-            // denominator consistent; the fp32 sum failed the peaked parity case)
-            l[g * 8 + k] += __low2float(v);
-            l[g * 8 + k + 1] += __high2float(v);
-            pk[k / 2] = *reinterpret_cast<const uint32_t*>(&v);
+            for (int q2 = 0; q2 < 8; q2 += 2) {
+              const float m0 = mv[q2] == -INFINITY ? 0.f : mv[q2];
+              const float m1 = mv[q2 + 1] == -INFINITY ? 0.f : mv[q2 + 1];
+              const __nv_bfloat162 v = __floats2bfloat162_rn(ex2(fmaf(x[g * 8 + q2], sl2, -m0)),
+                                                             ex2(fmaf(x[g * 8 + q2 + 1], sl2, -m1)));
+              // row sum from the bf16-rounded p the PV multiplies (numerator and
+              // denominator consistent; the fp32 sum failed the peaked parity case)
+              l[g * 8 + q2] += __low2float(v);
+              l[g * 8 + q2 + 1] += __high2float(v);
+              pk[q2 / 2] = *reinterpret_cast<const uint32_t*>(&v);
+            }
+            const int j = cb / 8 + g;
+            const uint32_t pa =
+                C::P_SW128 ? pbase + tr * 128 + ((j ^ (tr & 7)) << 4) : pbase + j * (T * 16) + tr * 16;
+            st_shared_v4(pa, pk[0], pk[1], pk[2], pk[3]);
           }
-          const int j = c0 / 8 + g;
-          const uint32_t pa = C::P_SW128 ? pbase + r * 128 + ((j ^ (r & 7)) << 4) : pbase + j * 2048 + r * 16;
-          st_shared_v4(pa, pk[0], pk[1], pk[2], pk[3]);
+        } else {  // HC == 4 (NQ = 16, T = 64): half a core-matrix row per thread
+          const float4 ma = ld_shared_f4(m_addr);
+          const float mv[4] = {ma.x, ma.y, ma.z, ma.w};
+          uint32_t pk[2];
+#pragma unroll
+          for (int q2 = 0; q2 < 4; q2 += 2) {
+            const float m0 = mv[q2] == -INFINITY ? 0.f : mv[q2];
+            const float m1 = mv[q2 + 1] == -INFINITY ? 0.f : mv[q2 + 1];
+            const __nv_bfloat162 v =
+                __floats2bfloat162_rn(ex2(fmaf(x[q2], sl2, -m0)), ex2(fmaf(x[q2 + 1], sl2, -m1)));
+            l[q2] += __low2float(v);
+            l[q2 + 1] += __high2float(v);
+            pk[q2 / 2] = *reinterpret_cast<const uint32_t*>(&v);
+          }
+          st_shared_v2(pbase + (cb / 8) * (T * 16) + tr * 16 + (cb % 8) * 2, pk[0], pk[1]);
         }
-        if (wg == 0 && tok >= s.kv_end) {  // never-visible rows: zero V so 0 * garbage cannot give NaN
-          const uint32_t kvrow = stage_base + r * 128;
+        if (wg == 0 && half == 0 && tok >= s.kv_end) {  // never-visible rows: zero V (0 * garbage != NaN)
+          const uint32_t kvrow = stage_base + tr * 128;
 #pragma unroll
           for (int ch = 0; ch < C::NCH_V; ++ch)
 #pragma unroll
@@ -808,8 +858,9 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
       }
 
       // ------------------------------------------------------- segment epilogue
-      const float cs = warp_col_reduce<CW, false>(l, lane);
-      if ((lane & ((1 << col_shift<CW>()) - 1)) == 0) red[(wg * 4 + wq) * 32 + (lane >> col_shift<CW>())] = cs;
+      const float cs = warp_col_reduce<HC, false, LANES>(l, lane);
+      if ((lane & ((1 << col_shift<HC, LANES>()) - 1)) == 0)
+        red[(wg * 4 + wq) * 32 + (cb - c0) + ((lane & (LANES - 1)) >> col_shift<HC, LANES>())] = cs;
       named_bar_sync(bar_id, 128);
       const int slot = cta + s.u;  // partial slot of a split unit
       if (r < CW) {  // fold the row sum into alpha_s as 1/l (reused below) and write lse

@@ -12,7 +12,7 @@ namespace glad {
 // Kernel family key: value width, key-from-state width, rope width, query
 // rows per CTA.
 struct DecodeKey {
-  int d_v, d_kn, d_r, nq;
+  int d_v, d_kn, d_r, nq, t;  // t: tokens per KV tile (128, or 64)
 };
 
 // Returns cudaErrorInvalidValue (and does not launch) if no instantiation
@@ -22,7 +22,7 @@ cudaError_t launch_decode(const DecodeKey& key, const CUtensorMap& tmap, const C
 bool decode_supported(const DecodeKey& key);
 int decode_max_nq(int d_v);
 
-cudaError_t launch_plan(const int32_t* seqlens, int32_t* plan, int U, int B, int n_qblk, int nq_blk, int Lq,
+cudaError_t launch_plan(const int32_t* seqlens, int32_t* plan, int U, int B, int tile, int n_qblk, int nq_blk, int Lq,
                         int g_q, int causal, cudaStream_t stream);
 cudaError_t launch_merge_units(const int32_t* plan, const float* o_part, const float* lse_part, int G, int U,
                                int nq_blk, int n_qblk, int B, int n_heads, int head_groups, int g_q, int Lq, int H,

@@ -60,6 +60,7 @@ def _sig(lib):
         "glad_version": ([], ctypes.c_char_p),
         "glad_debug_set_trace": ([_VP], None),
         "glad_debug_set_phase_mask": ([ctypes.c_int32], None),
+        "glad_debug_set_tile": ([ctypes.c_int32], None),
         "glad_pool_bytes": ([L], ctypes.c_size_t),
         "glad_cache_append": ([L, _VP, _VP, ctypes.c_int32, _VP, _VP, ctypes.c_int32, ctypes.c_int32, _VP], S),
         "glad_paged_gather": ([L, _VP, _VP, ctypes.c_int32, _VP, ctypes.c_int32, ctypes.c_int32, _VP, _VP], S),
@@ -91,7 +92,7 @@ def lib():
 
 
 def exported_symbols():
-    return ["glad_last_error", "glad_version", "glad_debug_set_trace", "glad_debug_set_phase_mask", "glad_pool_bytes", "glad_cache_append", "glad_paged_gather",
+    return ["glad_last_error", "glad_version", "glad_debug_set_trace", "glad_debug_set_phase_mask", "glad_debug_set_tile", "glad_pool_bytes", "glad_cache_append", "glad_paged_gather",
             "glad_decode_workspace_bytes", "glad_gla_decode", "glad_mla_decode",
             "glad_gta_decode", "glad_splitkv_combine", "glad_tp_duplication", "glad_tp_shard",
             "glad_kv_bytes_per_token_per_device"]
@@ -241,6 +242,11 @@ def debug_set_trace(buf):
 def debug_set_phase_mask(mask):
     """Debug/benchmark: launch only plan (1) / decode (2) / merge (4)."""
     lib().glad_debug_set_phase_mask(int(mask))
+
+
+def debug_set_tile(tokens):
+    """Debug/benchmark: force 64- or 128-token KV tiles (0 = library choice)."""
+    lib().glad_debug_set_tile(int(tokens))
 
 
 def version():

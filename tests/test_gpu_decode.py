@@ -79,7 +79,7 @@ def run_latent(B, Lq, H, h_c, d_c, d_R, seqlens, page, ctas=0, causal=True, scal
     return out, lse, o_ref, lse_ref
 
 
-def test_c1_gla2_oracle_scale():
+def test_c1_gla2_oracle_scale(tile):
     """BASELINE configs[0]: GLA-2, B=2, ctx 256, Lq=1, 16 q heads, 2 latent
     heads d_c=128 + d_R=32, page 16."""
     sl = np.array([256, 256])
@@ -119,16 +119,24 @@ GLA_SWEEP = [
 ]
 
 
+@pytest.fixture(params=[64, 128], ids=["T64", "T128"])
+def tile(request):
+    """Both KV tile heights (64-token tiles use M=64 QK and 16-lane S^T loads)."""
+    glad.debug_set_tile(request.param)
+    yield request.param
+    glad.debug_set_tile(0)
+
+
 @pytest.mark.parametrize("cfg", GLA_SWEEP, ids=lambda c: "B{}Lq{}H{}hc{}dc{}dr{}p{}s{}c{}".format(
     c[0], c[1], c[2], c[3], c[4], c[5], c[7], c[8], int(c[9])))
-def test_gla_sweep(cfg):
+def test_gla_sweep(cfg, tile):
     B, Lq, H, h_c, d_c, d_R, lens, page, ctas, causal = cfg
     out, lse, o_ref, lse_ref = run_latent(B, Lq, H, h_c, d_c, d_R, np.array(lens), page, ctas=ctas,
                                           causal=causal, seed=GLA_SWEEP.index(cfg))
     check(out, lse, o_ref, lse_ref, what=str(cfg))
 
 
-def test_peaked_and_large_scores():
+def test_peaked_and_large_scores(tile):
     """Peaked regime (q x 4) exercises the lazy-rescale path many times."""
     out, lse, o_ref, lse_ref = run_latent(2, 2, 32, 2, 256, 64, np.array([900, 650]), 64, ctas=1,
                                           seed=17, q_scale=4.0)
@@ -136,12 +144,12 @@ def test_peaked_and_large_scores():
 
 
 @pytest.mark.parametrize("Lq,H", [(1, 16), (2, 16), (1, 128)])
-def test_mla_baseline(Lq, H):
+def test_mla_baseline(Lq, H, tile):
     out, lse, o_ref, lse_ref = run_latent(2, Lq, H, 1, 512, 64, np.array([700, 300]), 64, seed=Lq + H)
     check(out, lse, o_ref, lse_ref, what=f"MLA Lq={Lq} H={H}")
 
 
-def test_empty_and_tiny_sequences():
+def test_empty_and_tiny_sequences(tile):
     out, lse, o_ref, lse_ref = run_latent(4, 2, 16, 2, 128, 32, np.array([0, 1, 2, 3]), 16, ctas=1)
     check(out, lse, o_ref, lse_ref, what="tiny")
     assert torch.all(out[0].float() == 0) and torch.all(torch.isneginf(lse[0]))
@@ -167,7 +175,7 @@ def test_page_size_and_permutation_invariance_bitexact():
 
 
 @pytest.mark.parametrize("ctas", [1, 2, 5, 7, 148, 300])
-def test_cta_count_changes_only_rounding(ctas):
+def test_cta_count_changes_only_rounding(ctas, tile):
     """Any persistent-CTA count (1 = no split at all; 300 > tiles = many
     empty CTAs and units cut into 1-tile segments) matches the oracle."""
     sl = np.array([3000, 2500, 1, 700])
@@ -192,7 +200,7 @@ def run_gta(B, Lq, H, h_kv, seqlens, page, ctas=0, causal=True, seed=0):
 
 @pytest.mark.parametrize("cfg", [(2, 1, 64, 8, [700, 333], 64, 0), (2, 2, 64, 8, [700, 333], 16, 2),
                                  (3, 1, 32, 2, [129, 1, 400], 1, 1), (1, 4, 64, 4, [1500], 64, 3)])
-def test_gta(cfg):
+def test_gta(cfg, tile):
     B, Lq, H, h_kv, lens, page, ctas = cfg
     out, lse, o_ref, lse_ref = run_gta(B, Lq, H, h_kv, np.array(lens), page, ctas=ctas, seed=7)
     check(out, lse, o_ref, lse_ref, what=f"GTA {cfg}")
