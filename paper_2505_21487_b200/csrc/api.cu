@@ -206,6 +206,11 @@ glad_status decode_common(Variant v, const void* q, const void* pool, const glad
   char* wsb = static_cast<char*>(ws);
   glad::DecodeParams p;
   p.q_tma = q_tma ? 1 : 0;
+  p.pool = static_cast<const __nv_bfloat16*>(pool);
+  p.row_stride = L->row_stride;
+  // pages shorter than 16 tokens: one TMA per page run per chunk costs ~100
+  // cycles of issue each; the cooperative cp.async producer wins (measured)
+  p.cp_kv = L->page_size < 16 ? 1 : 0;
   p.head_groups = head_groups;
   p.q_box_h = q_box_h;
   p.q_box_t = q_box_t;

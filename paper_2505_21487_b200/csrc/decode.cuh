@@ -61,6 +61,9 @@ struct DecodeParams {
   int32_t n_qblk, n_units;  // query blocks per head, U = n_heads_kv * B * n_qblk (head-major)
   int32_t causal;
   int32_t head_groups;      // 1: CTAs form n_heads_kv equal groups, one per head (see cta_range)
+  const __nv_bfloat16* pool;  // paged cache (cp.async producer path)
+  int64_t row_stride;       // elements
+  int32_t cp_kv;            // 1: small pages -> cooperative cp.async producer instead of TMA
   int32_t q_tma;            // 1: Q via the 3-D tensor map (box (64, q_box_h, q_box_t)); 0: cp.async
   int32_t q_box_h, q_box_t;
   float scale_log2;         // softmax_scale * log2(e)
@@ -102,7 +105,7 @@ struct DecodeCfg {
   static constexpr int CW = NQ / NWG;
   static constexpr int HC = T == 128 ? CW : CW / 2;  // columns per softmax thread (T=64: a thread pair per token)
   static constexpr int MAXSEG = 128;  // per-CTA segment table entries (aux + 3072)
-  static constexpr int AUX = 3072 + MAXSEG * 16;
+  static constexpr int AUX = 3072 + MAXSEG * 16 + T * 4;  // + row table of the cp.async producer
   static constexpr int AVAIL = 227 * 1024 - 1024 - AUX;
   static constexpr int NS_RAW = (AVAIL - QBYTES) / STAGE;
   static constexpr int NS = NS_RAW > 4 ? 4 : NS_RAW;
@@ -313,6 +316,7 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(aux + 256);
   int* range_s = reinterpret_cast<int*>(aux + 264);        // [4] cta tile range, #segments, overflow unit
   int4* segtab = reinterpret_cast<int4*>(aux + 3072);      // [MAXSEG] (u, t0, t1, L | whole << 30)
+  int* rowtab = reinterpret_cast<int*>(aux + 3072 + C::MAXSEG * 16);  // [T] pool row per tile row (cp path)
   int* vend_s = reinterpret_cast<int*>(aux + 320);         // [NQ] visible-key end per query column
   float* m_run = reinterpret_cast<float*>(aux + 640);      // [NQ] running max (log2 units)
   float* thr_s = reinterpret_cast<float*>(aux + 896);      // [NQ] rescale trigger in raw score units
@@ -378,7 +382,7 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
   }
   if (threadIdx.x == 0) {
     for (int i = 0; i < NS; ++i) {
-      mbar_init(&kv_full[i], 1);
+      mbar_init(&kv_full[i], p.cp_kv ? (p.q_tma ? 64 : 32) : 1);
       mbar_init(&kv_empty[i], 1);
       mbar_init(&p_full[i], 8);
     }
@@ -423,7 +427,88 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
     }
   };
 
-  if (warp == 0) {
+  if (p.cp_kv && (warp == 0 || (warp == 3 && p.q_tma))) {
+    // ============ cooperative cp.async producer for small pages ============
+    // The paper's distributed offset calculation on B200 terms: each lane
+    // resolves the page-table entry of "its" rows (one lookup per token, an
+    // int32 pool row kept in a register); for every row the warp broadcasts
+    // that row index with one shuffle and copies the row's slices with
+    // 16-B cp.async (lanes = consecutive 16-B units, 512 contiguous bytes per
+    // warp instruction) into the same 128B-swizzled layout TMA produces.
+    // Two producer warps (0 and 3) split the rows when Q arrives by TMA.
+    const int npw = p.q_tma ? 2 : 1;
+    const int pw = warp == 0 ? 0 : 1;
+    named_bar_sync(3, 96);
+    constexpr int RPW = T / 32;          // row registers per lane
+    const int row_lo = pw * (T / npw), row_hi = row_lo + T / npw;
+    int k = 0, u = 0, it = 0;
+    Seg s;
+    int pk = 0, pu = 0, ptl = 0, pt1 = 0;  // L2 prefetch cursor NS tiles ahead
+    bool pvalid = false;
+    Seg ps;
+    auto pf_advance = [&]() {
+      if (pvalid && ptl + 1 < pt1) { ++ptl; return; }
+      pvalid = next_seg(pk, pu, ps);
+      if (pvalid) { ptl = ps.t0; pt1 = ps.t1; }
+    };
+    pf_advance();
+    for (int i = 0; i < NS && pvalid; ++i) pf_advance();
+    while (next_seg(k, u, s)) {
+      const int* bt_row = p.block_table + static_cast<size_t>(s.b) * p.bt_stride;
+      const __nv_bfloat16* base_h = p.pool + s.head * p.d_head + lane * 8;  // lane's 16-B unit of the latent slice
+      const __nv_bfloat16* base_r = p.pool + p.rope_col + (lane & 7) * 8;
+      for (int tl = s.t0; tl < s.t1; ++tl, ++it) {
+        const int stage = it % NS;
+        const int p0 = tl * T;
+        int rowreg[RPW];  // pool row of tile row (32 j + lane), -1 if not visible
+#pragma unroll
+        for (int j = 0; j < RPW; ++j) {
+          const int pos = p0 + 32 * j + lane;
+          rowreg[j] = pos < s.kv_end ? __ldg(bt_row + (pos >> p.log2_page)) * p.page_size + (pos & (p.page_size - 1))
+                                     : -1;
+        }
+        mbar_wait(&kv_empty[stage], ((it / NS) & 1) ^ 1);
+        if (trace && pw == 0 && lane == 0 && it < kTraceTiles) trace[13 + 7 * it] = globaltimer();
+        const uint32_t sdst = sbase + stage * C::STAGE;
+#pragma unroll
+        for (int j = 0; j < RPW; ++j) {
+          if (32 * j + 31 < row_lo || 32 * j >= row_hi) continue;
+          for (int rr = 0; rr < 32; ++rr) {
+            const int r = 32 * j + rr;
+            const int row = __shfl_sync(0xffffffffu, rowreg[j], rr);
+            if (r < row_lo || r >= row_hi || row < 0) continue;
+            const int64_t roff = static_cast<int64_t>(row) * p.row_stride;
+            const uint32_t rdst = sdst + r * 128;
+            // latent slice: units lane, lane + 32, ... (NCH_V chunks x 8 units)
+#pragma unroll
+            for (int u0 = 0; u0 < C::NCH_V * 8; u0 += 32) {
+              const int un = u0 + lane;
+              if (un < C::NCH_V * 8)
+                cp_async16(rdst + (un >> 3) * C::CHUNK + (((un & 7) ^ (r & 7)) << 4), base_h + roff + u0 * 8, 16);
+            }
+            if (lane < C::D_R / 8)  // RoPE chunk
+              cp_async16(rdst + C::NCH_V * C::CHUNK + ((lane ^ (r & 7)) << 4), base_r + roff, 16);
+          }
+        }
+        cp_async_mbar_arrive(&kv_full[stage]);
+        if (trace && pw == 0 && lane == 0 && it < kTraceTiles) trace[8 + 7 * it] = globaltimer();
+        if (pvalid) {  // L2 prefetch of tile it + NS: each row's latent slice and RoPE
+          const int* pbt = p.block_table + static_cast<size_t>(ps.b) * p.bt_stride;
+          const int pp0 = ptl * T;
+          for (int r2 = row_lo + lane; r2 < row_hi; r2 += 32) {
+            const int pos = pp0 + r2;
+            if (pos < ps.kv_end) {
+              const int64_t row =
+                  static_cast<int64_t>(__ldg(pbt + (pos >> p.log2_page))) * p.page_size + (pos & (p.page_size - 1));
+              prefetch_l2_bulk(p.pool + row * p.row_stride + ps.head * p.d_head, C::NCH_V * 128);
+              prefetch_l2_bulk(p.pool + row * p.row_stride + p.rope_col, C::D_R * 2);
+            }
+          }
+          pf_advance();
+        }
+      }
+    }
+  } else if (warp == 0) {
     // ========================= TMA producer (all 32 lanes issue) =========================
     named_bar_sync(3, 96);  // the first Q load is issued first: QK needs Q, not a second tile
     const int box_rows = p.box_rows;
@@ -538,6 +623,7 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
         const int stage = next_qk % NS;
         const int sb = next_qk & 1;
         tc_fence_after();
+        if (p.cp_kv) fence_proxy_async_smem();  // cp.async (generic proxy) writes -> UMMA (async proxy) reads
         const uint32_t d = tmem + sb * NQ;
         const uint64_t ad = desc_kmajor_sw128(sbase + stage * C::STAGE);
         const uint64_t bd = desc_kmajor_sw128(sbase + C::OFF_Q + (cq.seg % C::NQB) * C::QBYTES);
@@ -619,7 +705,7 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
       }
       if (trace) trace[3] = cp.seg + 1;
     }
-  } else if (warp < 4) {
+  } else if (warp < 4 && !(warp == 3 && p.cp_kv && p.q_tma)) {
     // ========================= Q loader: TMA (one thread) or cp.async (64 threads) =========================
     const int tid = threadIdx.x - 64;
     int k = 0, u = 0, seg = 0;

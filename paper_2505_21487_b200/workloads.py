@@ -80,6 +80,13 @@ WORKLOADS = {w.name: w for w in [
     Workload("c4_gta", "gta", 256, 1, 64, 8, 128, 64, 4096, page=64, scale=1 / math.sqrt(128), seed=4,
              description="GTA Llama-style: h_q=64, 8 tied KV heads, d_h=128 half-RoPE, B=256, ctx 4K"),
     _c5(1), _c5(2), _c5(4), _c5(8), _c5(8, "skew"),
+    # page-size ablation (page 1 vs 64 for GLA 2x256+64)
+    Workload("c2_gla2_p1", "gla", 128, 1, 128, 2, 256, 64, 8192, page=1, scale=1 / math.sqrt(192), seed=1,
+             description="C2 GLA-2 with page size 1 (prefix caching, P:316)"),
+    Workload("c2_gla2_p16", "gla", 128, 1, 128, 2, 256, 64, 8192, page=16, scale=1 / math.sqrt(192), seed=1,
+             description="C2 GLA-2 with page size 16"),
+    Workload("c3_gla2_q2_p1", "gla", 64, 2, 128, 2, 256, 64, 16384, len_kind="uniform", page=1,
+             scale=1 / math.sqrt(192), seed=3, description="C3 GLA-2 q_len 2 with page size 1 (P:1412 setting)"),
 ]}
 
 
