@@ -182,6 +182,24 @@ glad_status decode_common(Variant v, const void* q, const void* pool, const glad
   CUresult cr = enc(&tmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(pool), dims, strides, box, estr,
                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, pr, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (cr != CUDA_SUCCESS) return fail(GLAD_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", static_cast<int>(cr));
+  // The latent slice of a page run as ONE box: the pool viewed as
+  // [row group of 8][64-col chunk][8 rows][64 cols], box (64, 8, NCH_V,
+  // box_rows / 8) -> smem [group][chunk][8 rows][128 B], the interleaved
+  // K-major atom layout the kernel's descriptors expect.
+  CUtensorMap lmap;
+  std::memset(&lmap, 0, sizeof(lmap));
+  if (L->page_size >= 16) {
+    const cuuint64_t rs = static_cast<cuuint64_t>(L->row_stride) * 2;
+    cuuint64_t ld[4] = {64u, 8u, static_cast<cuuint64_t>(L->n_heads_kv) * L->d_head / 64,
+                        static_cast<cuuint64_t>(L->num_pages) * static_cast<cuuint64_t>(L->page_size) / 8};
+    cuuint64_t ls[3] = {rs, 128u, 8u * rs};
+    cuuint32_t lbx[4] = {64u, 8u, static_cast<cuuint32_t>(g.key.d_v / 64), static_cast<cuuint32_t>(box_rows / 8)};
+    cuuint32_t le[4] = {1u, 1u, 1u, 1u};
+    cr = enc(&lmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(pool), ld, ls, lbx, le,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, pr, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (cr != CUDA_SUCCESS)
+      return fail(GLAD_ERR_CUDA, "cuTensorMapEncodeTiled (latent boxes) failed (%d)", static_cast<int>(cr));
+  }
 
   // Q as a 3-D tensor [B*Lq][H][d_qk]: a unit's NQ query rows are one box
   // (64 cols, g_q heads, NQ/g_q positions) or (64 cols, NQ heads, 1).
@@ -246,7 +264,7 @@ glad_status decode_common(Variant v, const void* q, const void* pool, const glad
     if (e != cudaSuccess) return fail(GLAD_ERR_CUDA, "plan launch failed: %s", cudaGetErrorString(e));
   }
   if (g_phase_mask & 2) {
-    e = glad::launch_decode(g.key, tmap, qmap, p, G, st);
+    e = glad::launch_decode(g.key, tmap, lmap, qmap, p, G, st);
     if (e != cudaSuccess) return fail(GLAD_ERR_CUDA, "decode launch failed: %s", cudaGetErrorString(e));
   }
   if (g_phase_mask & 4) {

@@ -70,12 +70,13 @@ struct DecodeParams {
   uint64_t* trace;          // debug timeline (nullptr = off): [cta][kTraceStride]
 };
 // Debug timeline layout per CTA (globaltimer ns): [0] start, [1] first QK,
-// [2] end, [3] number of segments, then per tile i < kTraceTiles: [8+6i] load
-// issued, [9+7i] QK issued, [10+7i] S seen by softmax, [11+7i] P written (WG0),
-// [12+7i] PV issued, [13+7i] stage free seen by the producer (before load i),
-// [14+7i] P written by the second softmax warpgroup.
-constexpr int kTraceTiles = 64;
-constexpr int kTraceStride = 8 + 7 * kTraceTiles;
+// [2] end, [3] number of segments, then per tile i < kTraceTiles: [8+8i] load
+// issued, [9+8i] QK issued, [10+8i] S seen by softmax, [11+8i] P written (WG0),
+// [12+8i] PV issued, [13+8i] stage free seen by the producer (before load i),
+// [14+8i] P written by the second softmax warpgroup, [15+8i] epilogue done
+// (last tile of a segment only).
+constexpr int kTraceTiles = 128;
+constexpr int kTraceStride = 8 + 8 * kTraceTiles;
 
 template <int D_V_, int D_KN_, int D_R_, int NQ_, int T_ = 128>
 struct DecodeCfg {
@@ -93,6 +94,11 @@ struct DecodeCfg {
   static constexpr int RK = D_R / 16;
   static constexpr int CHUNK = T * 128;  // one [T tokens x 64 cols] bf16 box set
   static constexpr int STAGE = NCH * CHUNK;
+  // Stage layout: latent [T/8 row groups][NCH_V chunks][8 rows][128 B] (one
+  // 1-KB SW128 atom per (group, chunk): a page run's whole latent slice is
+  // one TMA box), then the RoPE chunk [T rows][128 B] (later P^T).
+  static constexpr int LGRP = NCH_V * 1024;  // latent row-group stride
+  static constexpr int OFF_R = NCH_V * CHUNK;
   static constexpr int QCHUNK = NQ * 128;
   static constexpr int QBYTES = NQCH * QCHUNK;
   // P^T (bf16, [NQ/8][128 tok][8]) lives in the stage's RoPE chunk, which is
@@ -295,7 +301,8 @@ __device__ __forceinline__ Seg seg_from_entry(const DecodeParams& p, int4 e) {
 
 template <class C>
 __global__ void __launch_bounds__(C::NTHREADS, 1)
-    decode_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUtensorMap qmap,
+    decode_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUtensorMap lmap,
+                  const __grid_constant__ CUtensorMap qmap,
                   const DecodeParams p) {
   constexpr int T = C::T, NQ = C::NQ, CW = C::CW, NS = C::NS;
   constexpr float TAU = 8.0f;  // lazy-rescale threshold (log2 units)
@@ -319,7 +326,7 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
   int* rowtab = reinterpret_cast<int*>(aux + 3072 + C::MAXSEG * 16);  // [T] pool row per tile row (cp path)
   int* vend_s = reinterpret_cast<int*>(aux + 320);         // [NQ] visible-key end per query column
   float* m_run = reinterpret_cast<float*>(aux + 640);      // [NQ] running max (log2 units)
-  float* thr_s = reinterpret_cast<float*>(aux + 896);      // [NQ] rescale trigger in raw score units
+  float* nm_s = reinterpret_cast<float*>(aux + 896);       // [NQ] -m_run (0 while m_run = -inf)
   float* red = reinterpret_cast<float*>(aux + 1280);       // [2 wg][4 warps][32]
   float* alpha_s = reinterpret_cast<float*>(aux + 2304);   // [NQ] rescale factors / 1/l
 
@@ -398,6 +405,7 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
     }
     fence_barrier_init();
     tma_prefetch_desc(&tmap);
+    if (!p.cp_kv) tma_prefetch_desc(&lmap);
     if (p.q_tma) tma_prefetch_desc(&qmap);
   }
   if (warp == 2) { tmem_alloc(tmem_slot, C::TMEM_COLS); tmem_relinquish(); }
@@ -468,7 +476,7 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
                                      : -1;
         }
         mbar_wait(&kv_empty[stage], ((it / NS) & 1) ^ 1);
-        if (trace && pw == 0 && lane == 0 && it < kTraceTiles) trace[13 + 7 * it] = globaltimer();
+        if (trace && pw == 0 && lane == 0 && it < kTraceTiles) trace[13 + 8 * it] = globaltimer();
         const uint32_t sdst = sbase + stage * C::STAGE;
 #pragma unroll
         for (int j = 0; j < RPW; ++j) {
@@ -478,20 +486,20 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
             const int row = __shfl_sync(0xffffffffu, rowreg[j], rr);
             if (r < row_lo || r >= row_hi || row < 0) continue;
             const int64_t roff = static_cast<int64_t>(row) * p.row_stride;
-            const uint32_t rdst = sdst + r * 128;
+            const uint32_t ldst = sdst + (r >> 3) * C::LGRP + (r & 7) * 128;
             // latent slice: units lane, lane + 32, ... (NCH_V chunks x 8 units)
 #pragma unroll
             for (int u0 = 0; u0 < C::NCH_V * 8; u0 += 32) {
               const int un = u0 + lane;
               if (un < C::NCH_V * 8)
-                cp_async16(rdst + (un >> 3) * C::CHUNK + (((un & 7) ^ (r & 7)) << 4), base_h + roff + u0 * 8, 16);
+                cp_async16(ldst + (un >> 3) * 1024 + (((un & 7) ^ (r & 7)) << 4), base_h + roff + u0 * 8, 16);
             }
             if (lane < C::D_R / 8)  // RoPE chunk
-              cp_async16(rdst + C::NCH_V * C::CHUNK + ((lane ^ (r & 7)) << 4), base_r + roff, 16);
+              cp_async16(sdst + C::OFF_R + r * 128 + ((lane ^ (r & 7)) << 4), base_r + roff, 16);
           }
         }
         cp_async_mbar_arrive(&kv_full[stage]);
-        if (trace && pw == 0 && lane == 0 && it < kTraceTiles) trace[8 + 7 * it] = globaltimer();
+        if (trace && pw == 0 && lane == 0 && it < kTraceTiles) trace[8 + 8 * it] = globaltimer();
         if (pvalid) {  // L2 prefetch of tile it + NS: each row's latent slice and RoPE
           const int* pbt = p.block_table + static_cast<size_t>(ps.b) * p.bt_stride;
           const int pp0 = ptl * T;
@@ -511,28 +519,37 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
   } else if (warp == 0) {
     // ========================= TMA producer (all 32 lanes issue) =========================
     named_bar_sync(3, 96);  // the first Q load is issued first: QK needs Q, not a second tile
+    if (trace && lane == 0) trace[4] = globaltimer();
     const int box_rows = p.box_rows;
     // Issue the TMA boxes of tile `tl` of segment `s`: into smem (prefetch =
     // false, completing on kv_full[stage]) or as an L2 prefetch.  Boxes are
     // spread over the 32 lanes; one int32 block-table lookup per box.
+    // Two boxes per page run of a tile: item 2*box = the latent slice (4-D
+    // map, all NCH_V chunks in one box), item 2*box + 1 = the RoPE chunk
+    // (2-D map).  Issued into smem (completing on kv_full[stage]) or as an
+    // L2 prefetch.  Items are spread over the 32 lanes.
+    auto issue_item = [&](const Seg& s, int row, int box, int item, uint32_t stage_addr, uint64_t* bar) {
+      if (item == 0) {
+        const int c = s.head * (p.d_head >> 6);
+        if (bar) tma_load_4d(stage_addr + box * (box_rows >> 3) * C::LGRP, &lmap, bar, 0, 0, c, row >> 3);
+        else tma_prefetch_4d(&lmap, 0, 0, c, row >> 3);
+      } else {
+        if (bar) tma_load_2d(stage_addr + C::OFF_R + box * box_rows * 128, &tmap, bar, p.rope_col, row);
+        else tma_prefetch_2d(&tmap, p.rope_col, row);
+      }
+    };
+    auto item_row = [&](const int* bt_row, int p0, int box) {
+      const int pos = p0 + box * box_rows;
+      return __ldg(bt_row + (pos >> p.log2_page)) * p.page_size + (pos & (p.page_size - 1));
+    };
     auto issue_tile = [&](const Seg& s, int tl, int stage, bool prefetch, int page0) {
       const int* bt_row = p.block_table + static_cast<size_t>(s.b) * p.bt_stride;
       const int p0 = tl * T;
       const int ntok = min(T, s.kv_end - p0);
       const int nbox = (ntok + box_rows - 1) / box_rows;
-      for (int bx = lane; bx < nbox * C::NCH; bx += 32) {
-        const int box = bx / C::NCH, ch = bx - box * C::NCH;
-        const int pos = p0 + box * box_rows;
-        const int page = (bx == lane && page0 >= 0) ? page0 : __ldg(bt_row + (pos >> p.log2_page));
-        const int row = page * p.page_size + (pos & (p.page_size - 1));
-        const int col = ch < C::NCH_V ? s.head * p.d_head + ch * 64 : p.rope_col;
-        if (prefetch) {
-          tma_prefetch_2d(&tmap, col, row);
-        } else {
-          const uint32_t dst = sbase + stage * C::STAGE + ch * C::CHUNK + box * box_rows * 128;
-          tma_load_2d(dst, &tmap, &kv_full[stage], col, row);
-        }
-      }
+      for (int bx = lane; bx < nbox * 2; bx += 32)
+        issue_item(s, item_row(bt_row, p0, bx >> 1), bx >> 1, bx & 1, sbase + stage * C::STAGE,
+                   prefetch ? nullptr : &kv_full[stage]);
       return nbox;
     };
     // L2 prefetch cursor, PF = NS tiles ahead of the load cursor: the tile
@@ -558,35 +575,20 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
         const int p0 = tl * T;
         const int ntok = min(T, s.kv_end - p0);
         const int nbox = (ntok + box_rows - 1) / box_rows;
-        const int nitem = nbox * C::NCH;
-        // coordinates of this lane's first box (block-table lookup included)
-        // are computed before the stage wait: after the release only the TMA
-        // issue remains on the critical path
-        int col0 = 0, row0 = 0;
-        uint32_t dst0 = 0;
-        if (lane < nitem) {
-          const int box = lane / C::NCH, ch = lane - box * C::NCH;
-          const int pos = p0 + box * box_rows;
-          const int page = __ldg(bt_row + (pos >> p.log2_page));
-          row0 = page * p.page_size + (pos & (p.page_size - 1));
-          col0 = ch < C::NCH_V ? s.head * p.d_head + ch * 64 : p.rope_col;
-          dst0 = sbase + stage * C::STAGE + ch * C::CHUNK + box * box_rows * 128;
-        }
+        const int nitem = nbox * 2;
+        // the page lookup of this lane's first item is done before the stage
+        // wait: after the release only the TMA issue remains on the critical path
+        const int row0 = lane < nitem ? item_row(bt_row, p0, lane >> 1) : 0;
+        if (trace && lane == 0 && it == 0) trace[6] = globaltimer();
         mbar_wait(&kv_empty[stage], ((it / NS) & 1) ^ 1);
-        if (trace && lane == 0 && it < kTraceTiles) trace[13 + 7 * it] = globaltimer();
-        if (lane == 0) mbar_arrive_expect_tx(&kv_full[stage], static_cast<uint32_t>(nitem * box_rows * 128));
+        if (trace && lane == 0 && it < kTraceTiles) trace[13 + 8 * it] = globaltimer();
+        if (lane == 0) mbar_arrive_expect_tx(&kv_full[stage], static_cast<uint32_t>(nbox * box_rows * C::NCH * 128));
         __syncwarp();
-        if (lane < nitem) tma_load_2d(dst0, &tmap, &kv_full[stage], col0, row0);
-        for (int bx = lane + 32; bx < nitem; bx += 32) {  // small pages: more boxes than lanes
-          const int box = bx / C::NCH, ch = bx - box * C::NCH;
-          const int pos = p0 + box * box_rows;
-          const int page = __ldg(bt_row + (pos >> p.log2_page));
-          const int row = page * p.page_size + (pos & (p.page_size - 1));
-          const int col = ch < C::NCH_V ? s.head * p.d_head + ch * 64 : p.rope_col;
-          tma_load_2d(sbase + stage * C::STAGE + ch * C::CHUNK + box * box_rows * 128, &tmap, &kv_full[stage], col,
-                      row);
-        }
-        if (trace && lane == 0 && it < kTraceTiles) trace[8 + 7 * it] = globaltimer();
+        const uint32_t stage_addr = sbase + stage * C::STAGE;
+        if (lane < nitem) issue_item(s, row0, lane >> 1, lane & 1, stage_addr, &kv_full[stage]);
+        for (int bx = lane + 32; bx < nitem; bx += 32)  // small pages: more boxes than lanes
+          issue_item(s, item_row(bt_row, p0, bx >> 1), bx >> 1, bx & 1, stage_addr, &kv_full[stage]);
+        if (trace && lane == 0 && it < kTraceTiles) trace[8 + 8 * it] = globaltimer();
         if (pvalid) {  // L2 prefetch of tile it + NS, after the stage load so it never delays it
           issue_tile(ps, ptl, 0, true, -1);
           pf_advance();
@@ -625,18 +627,19 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
         tc_fence_after();
         if (p.cp_kv) fence_proxy_async_smem();  // cp.async (generic proxy) writes -> UMMA (async proxy) reads
         const uint32_t d = tmem + sb * NQ;
-        const uint64_t ad = desc_kmajor_sw128(sbase + stage * C::STAGE);
+        const uint64_t ad = desc_kmajor_sw128(sbase + stage * C::STAGE, C::LGRP);
+        const uint64_t rd = desc_kmajor_sw128(sbase + stage * C::STAGE + C::OFF_R);
         const uint64_t bd = desc_kmajor_sw128(sbase + C::OFF_Q + (cq.seg % C::NQB) * C::QBYTES);
 #pragma unroll
         for (int c = 0; c < C::NCH_QK; ++c) {
 #pragma unroll
           for (int k = 0; k < 4; ++k)
-            umma_f16_ss(d, ad + static_cast<uint64_t>((c * C::CHUNK + k * 32) >> 4),
+            umma_f16_ss(d, ad + static_cast<uint64_t>((c * 1024 + k * 32) >> 4),
                         bd + static_cast<uint64_t>((c * C::QCHUNK + k * 32) >> 4), idesc_qk, (c | k) != 0);
         }
 #pragma unroll
         for (int k = 0; k < C::RK; ++k)
-          umma_f16_ss(d, ad + static_cast<uint64_t>((C::NCH_V * C::CHUNK + k * 32) >> 4),
+          umma_f16_ss(d, rd + static_cast<uint64_t>((k * 32) >> 4),
                       bd + static_cast<uint64_t>((C::NCH_QK * C::QCHUNK + k * 32) >> 4), idesc_qk, 1u);
         umma_commit(&s_full[sb]);
         if (cq.tl + 1 == cq.t1) umma_commit(&q_empty[cq.seg % C::NQB]);  // last QK of the segment: Q free
@@ -646,16 +649,16 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
         const int j = next_pv;
         const int stage = j % NS;
         const uint32_t kv = sbase + stage * C::STAGE;
-        const uint64_t ad = desc_mnmajor_sw128(kv, C::CHUNK);
-        const uint64_t bd = C::P_SW128 ? desc_mnmajor_sw128(kv + C::NCH_V * C::CHUNK, 0)
-                                       : desc_mnmajor_noswz(kv + C::NCH_V * C::CHUNK, 128, T * 16);
+        const uint64_t ad = desc_mnmajor_sw128(kv, 1024, C::LGRP);
+        const uint64_t bd = C::P_SW128 ? desc_mnmajor_sw128(kv + C::OFF_R, 0)
+                                       : desc_mnmajor_noswz(kv + C::OFF_R, 128, T * 16);
         const uint32_t obuf = tmem + C::TMEM_O + (cp.seg % C::NOB) * C::OCOLS;
         const bool first = (cp.tl == cp.t0);
 #pragma unroll
         for (int blk = 0; blk < C::NBLK_O; ++blk) {
 #pragma unroll
           for (int k = 0; k < T / 16; ++k)
-            umma_f16_ss(obuf + blk * NQ, ad + static_cast<uint64_t>((2 * blk * C::CHUNK + k * 2048) >> 4),
+            umma_f16_ss(obuf + blk * NQ, ad + static_cast<uint64_t>((2 * blk * 1024 + k * 2 * C::LGRP) >> 4),
                         bd + static_cast<uint64_t>((C::P_SW128 ? k * 2048 : k * 256) >> 4), idesc_pv,
                         (!first || k > 0) ? 1u : 0u);
         }
@@ -671,7 +674,7 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
           const bool first = (cp.tl == cp.t0);
           if (!first || cp.seg < C::NOB ||
               mbar_test_wait(smem_u32(&o_empty[cp.seg % C::NOB]), ((cp.seg - C::NOB) / C::NOB) & 1)) {
-            if (trace && next_pv < kTraceTiles) trace[12 + 7 * next_pv] = globaltimer();
+            if (trace && next_pv < kTraceTiles) trace[12 + 8 * next_pv] = globaltimer();
             issue_pv();
             ++next_pv;
             pv_left = advance(cp);
@@ -684,7 +687,7 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
           const bool first = (cq.tl == cq.t0);
           if (!first || mbar_test_wait(smem_u32(&q_full[cq.seg % C::NQB]), (cq.seg / C::NQB) & 1)) {
             if (trace && next_qk == 0) trace[1] = globaltimer();
-            if (trace && next_qk < kTraceTiles) trace[9 + 7 * next_qk] = globaltimer();
+            if (trace && next_qk < kTraceTiles) trace[9 + 8 * next_qk] = globaltimer();
             issue_qk();
             ++next_qk;
             qk_left = advance(cq);
@@ -726,7 +729,11 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
             tma_load_3d(qdst + ch * C::QCHUNK, &qmap, &q_full[qbuf], col, c1, c2);
           }
         }
-        if (seg == 0) { __syncwarp(); named_bar_arrive(3, 96); }
+        if (seg == 0) {
+          if (trace && tid == 0) trace[5] = globaltimer();
+          __syncwarp();
+          named_bar_arrive(3, 96);
+        }
       } else {
         for (int idx = tid; idx < NQ * C::NQCH * 8; idx += 64) {
           const int n = idx / (C::NQCH * 8);
@@ -769,12 +776,10 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
     const int cb = c0 + half * HC;
     const uint32_t lane_addr = static_cast<uint32_t>(wq * 32) << 16;
     const uint32_t bar_id = 1 + wg;
-    const uint32_t m_addr = smem_u32(m_run + cb);
-    const uint32_t t_addr = smem_u32(thr_s + cb);
+    const uint32_t nm_addr = smem_u32(nm_s + cb);
     const uint32_t a_addr = smem_u32(alpha_s + cb);
     const uint32_t ao_addr = smem_u32(alpha_s + c0);  // O^T rescale: all CW columns of the WG
     const float sl2 = p.scale_log2;
-    const float inv_sl2 = 1.f / sl2;
     int k = 0, u = 0, seg = 0, it = 0;
     Seg s;
     while (next_seg(k, u, s)) {
@@ -788,7 +793,7 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
         }
         vend_s[n] = ve;
         m_run[n] = -INFINITY;
-        thr_s[n] = -INFINITY;
+        nm_s[n] = 0.f;
       }
       named_bar_sync(bar_id, 128);
       const int min_vend = p.causal ? max(0, min(s.L, s.L - p.Lq + s.n0 / p.g_q + 1)) : s.L;
@@ -802,34 +807,55 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
         const int sb = it & 1;
         mbar_wait(&s_full[sb], (it >> 1) & 1);
         tc_fence_after();
-        if (trace && threadIdx.x == 128 && it < kTraceTiles) trace[10 + 7 * it] = globaltimer();
-        float x[HC];  // raw scores q.k for this thread's token and columns
-        tmem_load_s<C>(tmem + lane_addr + sb * NQ + c0, x);
-        tmem_ld_wait();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&s_empty[sb]);
-
+        if (trace && threadIdx.x == 128 && it < kTraceTiles) trace[10 + 8 * it] = globaltimer();
         const int p0 = tl * T;
         const int tok = p0 + tr;
-        if (!(p0 + T <= min_vend && all_cols)) {  // masked tile (last tile / causal / padded columns)
+        const bool masked = !(p0 + T <= min_vend && all_cols);  // last tile / causal / padded columns
+        float x[HC];  // raw scores q.k for this thread's token and columns
+        // (re)loaded from TMEM instead of kept live across the vote: S(sb) is
+        // released only after it, so the rare path can read it again
+        auto load_x = [&]() {
+          tmem_load_s<C>(tmem + lane_addr + sb * NQ + c0, x);
+          tmem_ld_wait();
+          if (masked) {
 #pragma unroll
-          for (int n = 0; n < HC; ++n) {
-            const bool ok = (cb + n < s.nq) && tok < vend_s[cb + n];
-            x[n] = ok ? x[n] : -INFINITY;
+            for (int n = 0; n < HC; ++n) {
+              const bool ok = (cb + n < s.nq) && tok < vend_s[cb + n];
+              x[n] = ok ? x[n] : -INFINITY;
+            }
           }
-        }
-        bool need = false;
-        if constexpr (HC >= 4) {
+        };
+        load_x();
+        // p = 2^(s*c - m) with the lagging running max m (nm = -m, 0 while m is
+        // -inf so masked scores give exactly 0 without a select), packed to bf16.
+        // Lazy rescale: the max is only moved when some p exceeds 2^TAU (checked
+        // on the packed bf16 bits, which order like unsigned ints for p >= 0) or
+        // on the first tile of a segment; then p is recomputed.
+        uint32_t pk[HC / 2];
+        auto exp_pack = [&]() {
 #pragma unroll
           for (int n = 0; n < HC; n += 4) {
-            const float4 th = ld_shared_f4(t_addr + n * 4);
-            need |= (x[n] > th.x) | (x[n + 1] > th.y) | (x[n + 2] > th.z) | (x[n + 3] > th.w);
+            const float4 m4 = ld_shared_f4(nm_addr + n * 4);
+            const float2 e0 = ffma2(make_float2(x[n], x[n + 1]), make_float2(sl2, sl2), make_float2(m4.x, m4.y));
+            const float2 e1 =
+                ffma2(make_float2(x[n + 2], x[n + 3]), make_float2(sl2, sl2), make_float2(m4.z, m4.w));
+            const __nv_bfloat162 v0 = __floats2bfloat162_rn(ex2(e0.x), ex2(e0.y));
+            const __nv_bfloat162 v1 = __floats2bfloat162_rn(ex2(e1.x), ex2(e1.y));
+            pk[n / 2] = *reinterpret_cast<const uint32_t*>(&v0);
+            pk[n / 2 + 1] = *reinterpret_cast<const uint32_t*>(&v1);
           }
-        }
+        };
+        exp_pack();
+        uint32_t pmax = pk[0];
+#pragma unroll
+        for (int n = 1; n < HC / 2; ++n) pmax = max_u16x2(pmax, pk[n]);
+        constexpr uint32_t kTrig = 0x4380u;  // bf16 bits of 2^TAU = 256
+        static_assert(TAU == 8.f, "kTrig encodes 2^TAU");
+        const bool need = (tl == s.t0) | ((pmax & 0xffffu) > kTrig) | ((pmax >> 16) > kTrig);
         if (named_bar_red_or(bar_id, 128, need)) {
           // the running max moves by > 2^TAU somewhere: column max over the WG
           // (in pieces of <= 16 columns to bound register pressure)
+          load_x();
           constexpr int HW = HC > 16 ? 16 : HC;
 #pragma unroll
           for (int h0 = 0; h0 < HC; h0 += HW) {
@@ -848,7 +874,7 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
             const float mn = fmaxf(mo, mt);
             alpha_s[c0 + r] = (mn == -INFINITY) ? 1.f : ex2(mo - mn);
             m_run[c0 + r] = mn;
-            thr_s[c0 + r] = (mn == -INFINITY) ? -INFINITY : (mn + TAU) * inv_sl2;
+            nm_s[c0 + r] = (mn == -INFINITY) ? 0.f : -mn;
           }
           named_bar_sync(bar_id, 128);
           bool any_scale = false;
@@ -881,66 +907,50 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
             }
             tmem_st_wait();
           }
+          load_x();  // again: keeps x dead across the O^T rescale (register pressure)
+          exp_pack();
         }
-        // p = 2^(s*c - m): bf16 P^T into the tile's (now dead) RoPE chunk.
-        // NQ = 64: MN-major 128B-swizzled rows of 64 queries (token tr at
-        // tr*128, 16-B chunk j at j ^ (tr & 7)); else no-swizzle core
-        // matrices [NQ/8][T tok][8].
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&s_empty[sb]);
+        // row sum from the bf16-rounded p the PV multiplies (numerator and
+        // denominator consistent; the fp32 sum failed the peaked parity case)
+#pragma unroll
+        for (int n = 0; n < HC; n += 2) {
+          const float2 v = make_float2(__uint_as_float(pk[n / 2] << 16), __uint_as_float(pk[n / 2] & 0xffff0000u));
+          const float2 acc = fadd2(make_float2(l[n], l[n + 1]), v);
+          l[n] = acc.x;
+          l[n + 1] = acc.y;
+        }
+        // bf16 P^T into the tile's (now dead) RoPE chunk.  NQ = 64: MN-major
+        // 128B-swizzled rows of 64 queries (token tr at tr*128, 16-B chunk j at
+        // j ^ (tr & 7)); else no-swizzle core matrices [NQ/8][T tok][8].
         const uint32_t stage_base = sbase + (it % NS) * C::STAGE;
-        const uint32_t pbase = stage_base + C::NCH_V * C::CHUNK;
+        const uint32_t pbase = stage_base + C::OFF_R;
         if constexpr (HC >= 8) {
 #pragma unroll
           for (int g = 0; g < HC / 8; ++g) {
-            const float4 ma = ld_shared_f4(m_addr + g * 32);
-            const float4 mb = ld_shared_f4(m_addr + g * 32 + 16);
-            const float mv[8] = {ma.x, ma.y, ma.z, ma.w, mb.x, mb.y, mb.z, mb.w};
-            uint32_t pk[4];
-#pragma unroll
-            for (int q2 = 0; q2 < 8; q2 += 2) {
-              const float m0 = mv[q2] == -INFINITY ? 0.f : mv[q2];
-              const float m1 = mv[q2 + 1] == -INFINITY ? 0.f : mv[q2 + 1];
-              const __nv_bfloat162 v = __floats2bfloat162_rn(ex2(fmaf(x[g * 8 + q2], sl2, -m0)),
-                                                             ex2(fmaf(x[g * 8 + q2 + 1], sl2, -m1)));
-              // row sum from the bf16-rounded p the PV multiplies (numerator and
-              // denominator consistent; the fp32 sum failed the peaked parity case)
-              l[g * 8 + q2] += __low2float(v);
-              l[g * 8 + q2 + 1] += __high2float(v);
-              pk[q2 / 2] = *reinterpret_cast<const uint32_t*>(&v);
-            }
             const int j = cb / 8 + g;
             const uint32_t pa =
                 C::P_SW128 ? pbase + tr * 128 + ((j ^ (tr & 7)) << 4) : pbase + j * (T * 16) + tr * 16;
-            st_shared_v4(pa, pk[0], pk[1], pk[2], pk[3]);
+            st_shared_v4(pa, pk[g * 4], pk[g * 4 + 1], pk[g * 4 + 2], pk[g * 4 + 3]);
           }
         } else {  // HC == 4 (NQ = 16, T = 64): half a core-matrix row per thread
-          const float4 ma = ld_shared_f4(m_addr);
-          const float mv[4] = {ma.x, ma.y, ma.z, ma.w};
-          uint32_t pk[2];
-#pragma unroll
-          for (int q2 = 0; q2 < 4; q2 += 2) {
-            const float m0 = mv[q2] == -INFINITY ? 0.f : mv[q2];
-            const float m1 = mv[q2 + 1] == -INFINITY ? 0.f : mv[q2 + 1];
-            const __nv_bfloat162 v =
-                __floats2bfloat162_rn(ex2(fmaf(x[q2], sl2, -m0)), ex2(fmaf(x[q2 + 1], sl2, -m1)));
-            l[q2] += __low2float(v);
-            l[q2 + 1] += __high2float(v);
-            pk[q2 / 2] = *reinterpret_cast<const uint32_t*>(&v);
-          }
           st_shared_v2(pbase + (cb / 8) * (T * 16) + tr * 16 + (cb % 8) * 2, pk[0], pk[1]);
         }
         if (wg == 0 && half == 0 && tok >= s.kv_end) {  // never-visible rows: zero V (0 * garbage != NaN)
-          const uint32_t kvrow = stage_base + tr * 128;
+          const uint32_t kvrow = stage_base + (tr >> 3) * C::LGRP + (tr & 7) * 128;
 #pragma unroll
           for (int ch = 0; ch < C::NCH_V; ++ch)
 #pragma unroll
-            for (int uu = 0; uu < 8; ++uu) st_shared_v4(kvrow + ch * C::CHUNK + uu * 16, 0u, 0u, 0u, 0u);
+            for (int uu = 0; uu < 8; ++uu) st_shared_v4(kvrow + ch * 1024 + uu * 16, 0u, 0u, 0u, 0u);
         }
         fence_proxy_async_smem();
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&p_full[it % NS]);
-        if (trace && threadIdx.x == 128 && it < kTraceTiles) trace[11 + 7 * it] = globaltimer();
-        if (trace && threadIdx.x == 256 && it < kTraceTiles) trace[14 + 7 * it] = globaltimer();
+        if (trace && threadIdx.x == 128 && it < kTraceTiles) trace[11 + 8 * it] = globaltimer();
+        if (trace && threadIdx.x == 256 && it < kTraceTiles) trace[14 + 8 * it] = globaltimer();
       }
 
       // ------------------------------------------------------- segment epilogue
@@ -967,6 +977,26 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
       const int j = it - 1;  // last tile of this segment
       mbar_wait(&pv_done[j & 3], (j >> 2) & 1);
       tc_fence_after();
+      // 1/l of this WG's columns, and (whole units) the output row of column
+      // c0: rows advance by one within a query position's g_q heads and jump
+      // to the next position's row block after g_q columns (no per-element
+      // integer division or 64-bit index math: the epilogue is on the
+      // critical path of the next segment)
+      float inv_l[CW];
+#pragma unroll
+      for (int n = 0; n < CW; n += 4) {
+        const float4 a = ld_shared_f4(ao_addr + n * 4);
+        inv_l[n] = a.x; inv_l[n + 1] = a.y; inv_l[n + 2] = a.z; inv_l[n + 3] = a.w;
+      }
+      const int ncols = min(CW, s.nq - c0);
+      int j0 = 0;
+      size_t row0 = 0;
+      if (s.whole) {
+        const int ng = s.n0 + c0, t = ng / p.g_q;
+        j0 = ng - t * p.g_q;
+        row0 = (static_cast<size_t>(s.b) * p.Lq + t) * p.H + s.head * p.g_q + j0;
+      }
+      const int jump = (p.H - p.g_q) * C::D_V;
 #pragma unroll
       for (int blk = 0; blk < C::NBLK_O; ++blk) {
         float o[CW];
@@ -978,20 +1008,24 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
           if (lane == 0) mbar_arrive(&o_empty[seg % C::NOB]);
         }
         const int d = blk * 128 + r;
+        if (s.whole) {
+          __nv_bfloat16* dst = p.out + row0 * C::D_V + d;
+          int j = j0;
 #pragma unroll
-        for (int n = 0; n < CW; ++n) {
-          if (c0 + n < s.nq) {
-            const float val = o[n] * alpha_s[c0 + n];
-            if (s.whole) {
-              const int ng = s.n0 + c0 + n, t = ng / p.g_q, h = s.head * p.g_q + (ng - t * p.g_q);
-              p.out[((static_cast<size_t>(s.b) * p.Lq + t) * p.H + h) * C::D_V + d] = __float2bfloat16(val);
-            } else {
-              p.o_part[(static_cast<size_t>(slot) * NQ + c0 + n) * C::D_V + d] = val;
-            }
+          for (int n = 0; n < CW; ++n) {
+            if (n < ncols) *dst = __float2bfloat16(o[n] * inv_l[n]);
+            dst += C::D_V;
+            if (++j == p.g_q) { j = 0; dst += jump; }
           }
+        } else {
+          float* dst = p.o_part + (static_cast<size_t>(slot) * NQ + c0) * C::D_V + d;
+#pragma unroll
+          for (int n = 0; n < CW; ++n)
+            if (n < ncols) dst[n * C::D_V] = o[n] * inv_l[n];
         }
       }
       named_bar_sync(bar_id, 128);  // alpha_s / m_run reads done before the next segment resets them
+      if (trace && threadIdx.x == 128 && it - 1 < kTraceTiles) trace[15 + 8 * (it - 1)] = globaltimer();
       ++seg;
     }
   }

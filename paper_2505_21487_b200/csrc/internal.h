@@ -17,7 +17,7 @@ struct DecodeKey {
 
 // Returns cudaErrorInvalidValue (and does not launch) if no instantiation
 // matches `key`.
-cudaError_t launch_decode(const DecodeKey& key, const CUtensorMap& tmap, const CUtensorMap& qmap, const DecodeParams& p, int grid,
+cudaError_t launch_decode(const DecodeKey& key, const CUtensorMap& tmap, const CUtensorMap& lmap, const CUtensorMap& qmap, const DecodeParams& p, int grid,
                           cudaStream_t stream);
 bool decode_supported(const DecodeKey& key);
 int decode_max_nq(int d_v);

@@ -231,7 +231,7 @@ def kv_bytes_per_token_per_device(variant, n_kv_heads, d_head, d_rope, N, dtype_
     return lib().glad_kv_bytes_per_token_per_device(variant, n_kv_heads, d_head, d_rope, N, dtype_bytes)
 
 
-TRACE_STRIDE = 8 + 7 * 64
+TRACE_STRIDE = 8 + 8 * 128
 
 
 def debug_set_trace(buf):

@@ -26,3 +26,16 @@ for n in (16, 64, 128):
         cyc, cnt, iss = out.tolist()
         ideal = max(128, 128) * n / 256
         print(f"N={n:3d} {names[w]:34s} {cyc / cnt:7.1f} cycles/MMA (dense-rate floor {ideal:.0f})")
+
+# completion time of a burst of n MMAs into an idle pipe (one commit at the end)
+lib.glad_debug_mma_burst.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_void_p]
+ob = torch.zeros(64, dtype=torch.int64, device="cuda")
+for w in (0, 1):
+    for gap in (-1, 5000):
+        row = []
+        for n in (1, 2, 4, 8, 12, 16, 20, 24, 32):
+            assert lib.glad_debug_mma_burst(w, n, gap, ctypes.c_void_p(ob.data_ptr())) == 0
+            torch.cuda.synchronize()
+            v = ob.tolist()
+            row.append(f"n={n}:{v[0]}/{v[32 + n - 1]}")
+        print(f"burst {'QK' if w == 0 else 'PV'} gap {gap:5d} done/issued: " + " ".join(row))

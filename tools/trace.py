@@ -40,10 +40,14 @@ tr = buf.view(n_ctas, glad.TRACE_STRIDE).cpu().numpy().astype(np.int64)
 tr = tr[tr[:, 0] > 0]
 t0 = tr[:, 0].min()
 print(f"{wl.name}: segments/CTA {np.median(tr[:, 3]):.1f}, {len(tr)} CTAs, kernel span {(tr[:, 2].max() - t0) / 1e3:.1f} us")
+_st = np.sort(tr[:, 0] - t0) / 1e3
+_en = np.sort(tr[:, 2] - t0) / 1e3
+print("CTA start (us, percentiles 0/50/90/100): " + " ".join(f"{np.percentile(_st, q):.1f}" for q in (0, 50, 90, 100)) +
+      "; end: " + " ".join(f"{np.percentile(_en, q):.1f}" for q in (0, 10, 50, 90, 100)))
 print(f"CTA lifetime median {np.median(tr[:, 2] - tr[:, 0]) / 1e3:.1f} us, start->Q ready "
       f"{np.median(tr[:, 1] - tr[:, 0]) / 1e3:.2f} us")
-T = (tr.shape[1] - 8) // 7
-tile = tr[:, 8:].reshape(len(tr), T, 7)  # load, qk, s, p, pv, free, p_wg1
+T = (tr.shape[1] - 8) // 8
+tile = tr[:, 8:].reshape(len(tr), T, 8)  # load, qk, s, p, pv, free, p_wg1, epi
 valid = tile[:, :, 1] > 0
 ntile = valid.sum(1)
 
@@ -74,14 +78,29 @@ print(f"  QK period {med(per, valid[:, 1:] & valid[:, :-1]):8.0f}")
 first = tile[:, 0]
 print(f"  first tile: start->load {np.median(first[:, 0] - tr[:, 0]):.0f}  load->QK {np.median(first[:, 1] - first[:, 0]):.0f}")
 last = np.array([tile[i, ntile[i] - 1, 4] for i in range(len(tr))])
-print(f"  last PV issue -> CTA end {np.median(tr[:, 2] - last):.0f}")
+print(f"  last PV issue -> CTA end {np.median(tr[:, 2] - last):.0f}  (tiles traced/CTA {np.median(ntile):.0f})")
+# time budget of a median CTA: steady tiles vs segment switches vs start / tail
+epi = tile[:, :, 7]
+qk = tile[:, :, 1].astype(np.float64)
+dq = np.where(valid[:, 1:] & valid[:, :-1], qk[:, 1:] - qk[:, :-1], np.nan)
+seg_end = epi[:, :-1] > 0  # tile i ends a segment -> gap to QK(i+1) is a switch
+sw = np.where(seg_end, dq, np.nan)
+st = np.where(~seg_end, dq, np.nan)
+print(f"  per CTA: steady QK->QK sum {np.nanmedian(np.nansum(st, 1)) / 1e3:.1f} us over {np.median(np.sum(~np.isnan(st), 1)):.0f} "
+      f"gaps (mean {np.nanmean(st):.0f} ns), switch gaps sum {np.nanmedian(np.nansum(sw, 1)) / 1e3:.1f} us "
+      f"(mean {np.nanmean(sw):.0f} ns)")
+print(f"  start->first QK {np.median(tr[:, 1] - tr[:, 0]) / 1e3:.1f} us, last QK->end {np.median(tr[:, 2] - np.nanmax(np.where(valid, qk, np.nan), 1)) / 1e3:.1f} us")
+print(f"  start (us): Q issued {np.median(tr[:, 5] - tr[:, 0]) / 1e3:.2f}, producer past Q barrier "
+      f"{np.median(tr[:, 4] - tr[:, 0]) / 1e3:.2f}, first row looked up {np.median(tr[:, 6] - tr[:, 0]) / 1e3:.2f}, "
+      f"first load issued {np.median(tile[:, 0, 0] - tr[:, 0]) / 1e3:.2f}")
+print(f"  epilogue: S(last)->epi done {np.nanmedian(np.where(epi > 0, epi - tile[:, :, 2], np.nan)):.0f} ns")
 
 if os.environ.get("TRACE_RAW"):
     c = int(os.environ.get("TRACE_CTA", "5"))
     base = tr[c, 0]
-    print(f"raw timeline of CTA {c} (us from CTA start): free, load, QK, S, P0, P1, PV")
-    for i in range(8, 24):
+    print(f"raw timeline of CTA {c} (us from CTA start): free, load, QK, S, P0, P1, PV, epi")
+    for i in range(int(os.environ.get("TRACE_FROM", "0")), int(os.environ.get("TRACE_TO", "128"))):
         if tile[c, i, 1] == 0:
             break
         print(f"  tile {i:2d}: " + "  ".join(f"{(tile[c, i, j] - base) / 1e3:8.2f}" if tile[c, i, j] else "       -"
-                                          for j in (5, 0, 1, 2, 3, 6, 4)))
+                                          for j in (5, 0, 1, 2, 3, 6, 4, 7)))
