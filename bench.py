@@ -178,6 +178,8 @@ def run_ours(args, rank, world, local_rank):
         base = name.replace("_tp1", "").replace("_tp2", "").replace("_tp4", "").replace("_tp8", "")
         name = base.replace("c5_gla8", f"c5_gla8_tp{world}")
     wl = workloads.get(name)
+    if args.tile:
+        glad.debug_set_tile(args.tile)
     st = workloads.build_device_state(wl, seed=wl.seed + (0 if is_tp else rank), device=dev, num_ctas=args.ctas)
     sl = st["seqlens_host"]
     stream = torch.cuda.current_stream(dev)
@@ -342,6 +344,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ctas", type=int, default=0, help="persistent CTA count (0 = one per SM)")
+    ap.add_argument("--tile", type=int, default=0, help="debug: force the KV tile height (0 = library choice)")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))

@@ -187,7 +187,7 @@ GLAD_API void glad_debug_set_trace(void* device_buf);
  * 1 = plan, 2 = decode, 4 = merge (default 7).  Used to time the decode
  * kernel alone.  Not thread-safe. */
 GLAD_API void glad_debug_set_phase_mask(int32_t mask);
-/* Debug/benchmark only: force the KV tile height (64 or 128 tokens; 0 =
+/* Debug/benchmark only: force the KV tile height (64, 96 or 128 tokens; 0 =
  * library choice).  Results are identical up to fp32 summation order. */
 GLAD_API void glad_debug_set_tile(int32_t tokens);
 

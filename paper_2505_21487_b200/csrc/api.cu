@@ -78,15 +78,21 @@ int64_t row_width(const glad_cache_layout* L) {
 
 enum Variant { kGLA, kMLA, kGTA };
 
-int g_tile_override = 0;  // debug: force 64 / 128-token tiles (glad_debug_set_tile)
+int g_tile_override = 0;  // debug: force 64 / 96 / 128-token tiles (glad_debug_set_tile)
 
-// KV tile height.  64-token tiles (M = 64 QK) fit twice as many stages, but
-// measured slower on every BASELINE shape (C2 0.47 vs 0.36 ms, GTA 1.06 vs
-// 0.63 ms): QK then re-reads Q from smem per 64 tokens and the SS MMAs are
-// smem-read bound, so the tensor pipe becomes the bottleneck.  128 is the
-// default; 64 stays available (and tested) via glad_debug_set_tile.
-int tile_tokens(const glad::DecodeKey&) {
-  if (g_tile_override == 64 || g_tile_override == 128) return g_tile_override;
+// KV tile height.  Shared memory holds NS stages of T tokens next to the
+// query block; the refill of a stage waits for the PV of the tile it held,
+// so with two stages the pipeline is latency-bound.  Prefer
+// the tallest tile that gives three stages, else the tallest with two.
+int tile_tokens(const glad::DecodeKey& k0) {
+  if (g_tile_override == 64 || g_tile_override == 96 || g_tile_override == 128) return g_tile_override;
+  glad::DecodeKey k = k0;
+  for (int want : {3, 2}) {
+    for (int t : {128, 96, 64}) {
+      k.t = t;
+      if (glad::decode_stages(k) >= want) return t;
+    }
+  }
   return 128;
 }
 
@@ -171,7 +177,10 @@ glad_status decode_common(Variant v, const void* q, const void* pool, const glad
   auto enc = encode_fn();
   if (!enc) return fail(GLAD_ERR_CUDA, "cuTensorMapEncodeTiled entry point unavailable");
   CUtensorMap tmap;
-  const int box_rows = L->page_size < g.key.t ? L->page_size : g.key.t;
+  // page runs inside a tile: a page never crosses a tile edge when T is a
+  // multiple of the page or vice versa; T = 96 with pages >= 32 uses 32-row boxes
+  int box_rows = L->page_size;
+  while (g.key.t % box_rows) box_rows >>= 1;  // gcd(page, T) (pages are powers of two)
   cuuint64_t dims[2] = {static_cast<cuuint64_t>(row_width(L)),
                         static_cast<cuuint64_t>(L->num_pages) * static_cast<cuuint64_t>(L->page_size)};
   cuuint64_t strides[1] = {static_cast<cuuint64_t>(L->row_stride) * 2};

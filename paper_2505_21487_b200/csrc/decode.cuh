@@ -28,12 +28,12 @@
 //    A unit finished inside one CTA is written directly; a unit cut by a
 //    range boundary leaves partials (o/l, lse) in workspace slot c + u and
 //    the combine kernel merges them (split-KV LSE merge).
-//  * Warp roles (384 threads): w0 TMA producer, w1 UMMA issuer (one thread,
-//    non-blocking scheduler), w2-3 Q loader (+ TMEM alloc), w4-7 / w8-11 two
+//  * Warp roles (384 threads): w0 TMA producer, w1 UMMA issuer (warp-uniform
+//    scheduler, one elected lane issues), w2-3 Q loader (+ TMEM alloc), w4-7 / w8-11 two
 //    softmax warpgroups, each owning half of the query columns for all 128
 //    token lanes.
 //  * Online softmax with lazy rescaling: the running max only moves when a
-//    score exceeds it by > 2^8 (vote via barrier.red.or), so the cross-lane
+//    p exceeds 2^8 (vote via barrier.red.or), so the cross-lane
 //    max reduction and the TMEM O rescale run on a handful of tiles per unit.
 #pragma once
 #include <cuda.h>
@@ -74,9 +74,13 @@ struct DecodeParams {
 // issued, [9+8i] QK issued, [10+8i] S seen by softmax, [11+8i] P written (WG0),
 // [12+8i] PV issued, [13+8i] stage free seen by the producer (before load i),
 // [14+8i] P written by the second softmax warpgroup, [15+8i] epilogue done
-// (last tile of a segment only).
+// (last tile of a segment only), [16+10i] QK issue returned, [17+10i] PV
+// issue returned (per-tile stride 10).
+#ifndef GLAD_MMA_BACKOFF_NS
+#define GLAD_MMA_BACKOFF_NS 0
+#endif
 constexpr int kTraceTiles = 128;
-constexpr int kTraceStride = 8 + 8 * kTraceTiles;
+constexpr int kTraceStride = 8 + 12 * kTraceTiles;
 
 template <int D_V_, int D_KN_, int D_R_, int NQ_, int T_ = 128>
 struct DecodeCfg {
@@ -84,8 +88,12 @@ struct DecodeCfg {
   static constexpr int D_KN = D_KN_;  // key part taken from the state
   static constexpr int D_R = D_R_;    // rope width
   static constexpr int NQ = NQ_;      // query rows per unit (UMMA N)
-  static constexpr int T = T_;        // tokens per tile (UMMA M of QK: 128, or 64 = 40 KB GLA-2 stages)
-  static constexpr int LANES = T == 128 ? 32 : 16;  // token lanes per warp quarter in S^T (M=64: 16)
+  // tokens per tile (64 / 96 / 128).  The QK UMMA always has M = 128: with
+  // T < 128 its rows >= T read whatever follows the tile in shared memory and
+  // are discarded by the softmax (a fraction of QK tensor work traded for a
+  // third / fourth KV stage).
+  static constexpr int T = T_;
+  static constexpr int LANES = 32;  // token lanes per warp quarter in S^T
   static constexpr int DQ = D_KN + D_R;
   static constexpr int NCH_V = D_V / 64;
   static constexpr int NCH = NCH_V + 1;  // + rope chunk
@@ -109,18 +117,21 @@ struct DecodeCfg {
   static constexpr int NBLK_O = D_V / 128;
   static constexpr int NWG = 2;
   static constexpr int CW = NQ / NWG;
-  static constexpr int HC = T == 128 ? CW : CW / 2;  // columns per softmax thread (T=64: a thread pair per token)
+  static constexpr int HC = CW;  // columns per softmax thread (one token row)
   static constexpr int MAXSEG = 128;  // per-CTA segment table entries (aux + 3072)
   static constexpr int AUX = 3072 + MAXSEG * 16 + T * 4;  // + row table of the cp.async producer
   static constexpr int AVAIL = 227 * 1024 - 1024 - AUX;
-  static constexpr int NS_RAW = (AVAIL - QBYTES) / STAGE;
+  // bytes the M = 128 QK may read past the end of the last stage (rows >= T)
+  static constexpr int OVER_RAW = (16 * LGRP > OFF_R + 16384 ? 16 * LGRP : OFF_R + 16384) - STAGE;
+  static constexpr int XTRA = OVER_RAW - QBYTES - AUX > 0 ? OVER_RAW - QBYTES - AUX : 0;
+  static constexpr int NS_RAW = (AVAIL - QBYTES - XTRA) / STAGE;
   static constexpr int NS = NS_RAW > 4 ? 4 : NS_RAW;
   // a second Q buffer (next unit's Q prefetched while this one runs) when it
   // costs no KV stage
-  static constexpr int NQB = ((AVAIL - 2 * QBYTES) / STAGE >= NS) ? 2 : 1;
+  static constexpr int NQB = ((AVAIL - 2 * QBYTES - XTRA) / STAGE >= NS) ? 2 : 1;
   static constexpr int OFF_Q = NS * STAGE;
   static constexpr int OFF_AUX = OFF_Q + NQB * QBYTES;
-  static constexpr int SMEM_BYTES = 1024 + OFF_AUX + AUX;
+  static constexpr int SMEM_BYTES = 1024 + OFF_AUX + AUX + XTRA;
   static constexpr int OCOLS = NBLK_O * NQ;      // one O^T accumulator
   static constexpr int TMEM_O = 2 * NQ;          // after the two S^T buffers
   // two O buffers (the next unit's first PV overlaps this unit's epilogue)
@@ -137,7 +148,7 @@ struct DecodeCfg {
   static_assert(NQ == 16 || NQ == 32 || NQ == 64, "NQ must be 16/32/64");
   static_assert(TMEM_USED <= 512, "TMEM budget");
   static_assert(QCHUNK % 1024 == 0, "Q chunk alignment");
-  static_assert(T == 128 || T == 64, "tile height");
+  static_assert(T == 128 || T == 96 || T == 64, "tile height");
 };
 
 // Column reduction over groups of LANES lanes (32, or 16 for the halves of a
@@ -181,19 +192,10 @@ __device__ __forceinline__ void tmem_load_cols(uint32_t taddr, float (&x)[C::CW]
     for (int cc = 0; cc < C::CW; cc += 8) tmem_ld8(taddr + cc, x + cc);
   }
 }
-// S^T columns of this thread: T = 128 -> 32x32b (CW columns); T = 64 -> the
-// two-half 16-lane load (HC = CW/2 columns each, thread pair per token).
+// S^T columns of this thread (its token row, CW columns).
 template <class C>
 __device__ __forceinline__ void tmem_load_s(uint32_t taddr, float (&x)[C::HC]) {
-  if constexpr (C::T == 128) {
-    tmem_load_cols<C>(taddr, x);
-  } else if constexpr (C::HC == 16) {
-    tmem_ld16x2_x16(taddr, x);
-  } else if constexpr (C::HC == 8) {
-    tmem_ld16x2_x8(taddr, x);
-  } else {
-    tmem_ld16x2_x4(taddr, x);
-  }
+  tmem_load_cols<C>(taddr, x);
 }
 template <class C>
 __device__ __forceinline__ void tmem_store_cols(uint32_t taddr, const float (&x)[C::CW]) {
@@ -476,7 +478,7 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
                                      : -1;
         }
         mbar_wait(&kv_empty[stage], ((it / NS) & 1) ^ 1);
-        if (trace && pw == 0 && lane == 0 && it < kTraceTiles) trace[13 + 8 * it] = globaltimer();
+        if (trace && pw == 0 && lane == 0 && it < kTraceTiles) trace[13 + 12 * it] = globaltimer();
         const uint32_t sdst = sbase + stage * C::STAGE;
 #pragma unroll
         for (int j = 0; j < RPW; ++j) {
@@ -499,7 +501,7 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
           }
         }
         cp_async_mbar_arrive(&kv_full[stage]);
-        if (trace && pw == 0 && lane == 0 && it < kTraceTiles) trace[8 + 8 * it] = globaltimer();
+        if (trace && pw == 0 && lane == 0 && it < kTraceTiles) trace[8 + 12 * it] = globaltimer();
         if (pvalid) {  // L2 prefetch of tile it + NS: each row's latent slice and RoPE
           const int* pbt = p.block_table + static_cast<size_t>(ps.b) * p.bt_stride;
           const int pp0 = ptl * T;
@@ -581,14 +583,14 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
         const int row0 = lane < nitem ? item_row(bt_row, p0, lane >> 1) : 0;
         if (trace && lane == 0 && it == 0) trace[6] = globaltimer();
         mbar_wait(&kv_empty[stage], ((it / NS) & 1) ^ 1);
-        if (trace && lane == 0 && it < kTraceTiles) trace[13 + 8 * it] = globaltimer();
+        if (trace && lane == 0 && it < kTraceTiles) trace[13 + 12 * it] = globaltimer();
         if (lane == 0) mbar_arrive_expect_tx(&kv_full[stage], static_cast<uint32_t>(nbox * box_rows * C::NCH * 128));
         __syncwarp();
         const uint32_t stage_addr = sbase + stage * C::STAGE;
         if (lane < nitem) issue_item(s, row0, lane >> 1, lane & 1, stage_addr, &kv_full[stage]);
         for (int bx = lane + 32; bx < nitem; bx += 32)  // small pages: more boxes than lanes
           issue_item(s, item_row(bt_row, p0, bx >> 1), bx >> 1, bx & 1, stage_addr, &kv_full[stage]);
-        if (trace && lane == 0 && it < kTraceTiles) trace[8 + 8 * it] = globaltimer();
+        if (trace && lane == 0 && it < kTraceTiles) trace[8 + 12 * it] = globaltimer();
         if (pvalid) {  // L2 prefetch of tile it + NS, after the stage load so it never delays it
           issue_tile(ps, ptl, 0, true, -1);
           pf_advance();
@@ -596,10 +598,15 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
       }
     }
   } else if (warp == 1) {
-    // ========================= UMMA issuer (one thread) =========================
-    if (lane == 0) {
-      constexpr uint32_t idesc_qk = make_idesc_bf16(T, NQ, false, false);
+    // ========================= UMMA issuer (warp 1, one elected lane issues) =========================
+    // The whole warp runs the scheduler with warp-uniform control flow (every
+    // barrier probe and cursor value is made uniform with a vote / REDUX), so
+    // descriptors live in uniform registers and each tcgen05.mma costs a
+    // couple of uniform adds to issue.
+    {
+      constexpr uint32_t idesc_qk = make_idesc_bf16(128, NQ, false, false);
       constexpr uint32_t idesc_pv = make_idesc_bf16(128, NQ, true, true);
+      const uint32_t tm = static_cast<uint32_t>(warp_uniform(static_cast<int>(tmem)));
       // The QK stream and the PV stream walk the CTA's tiles with separate
       // cursors (segment, tile within unit).
       struct Cursor {
@@ -609,24 +616,26 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
       auto advance = [&](Cursor& c) -> bool {  // move to the next tile; false when done
         if (c.seg >= 0 && c.tl + 1 < c.t1) { ++c.tl; return true; }
         Seg s;
-        if (!next_seg(c.k, c.u, s)) return false;
+        const bool ok = warp_uniform(next_seg(c.k, c.u, s));
+        if (!ok) return false;
+        c.k = warp_uniform(c.k);
+        c.u = warp_uniform(c.u);
         ++c.seg;
-        c.tl = s.t0;
-        c.t0 = s.t0;
-        c.t1 = s.t1;
+        c.tl = c.t0 = warp_uniform(s.t0);
+        c.t1 = warp_uniform(s.t1);
         return true;
       };
+      auto probe = [&](uint64_t* bar, int parity) { return warp_uniform(mbar_test_wait(smem_u32(bar), parity)); };
       bool qk_left = advance(cq), pv_left = advance(cp);
       int next_qk = 0, next_pv = 0;
       // Descriptors are built once per stage / Q buffer; each MMA only adds a
-      // compile-time byte offset (>> 4) to the start-address field, so the
-      // single issuing thread spends ~1 instruction per tcgen05.mma on them.
+      // compile-time byte offset (>> 4) to the start-address field.
       auto issue_qk = [&]() {
         const int stage = next_qk % NS;
         const int sb = next_qk & 1;
         tc_fence_after();
         if (p.cp_kv) fence_proxy_async_smem();  // cp.async (generic proxy) writes -> UMMA (async proxy) reads
-        const uint32_t d = tmem + sb * NQ;
+        const uint32_t d = tm + sb * NQ;
         const uint64_t ad = desc_kmajor_sw128(sbase + stage * C::STAGE, C::LGRP);
         const uint64_t rd = desc_kmajor_sw128(sbase + stage * C::STAGE + C::OFF_R);
         const uint64_t bd = desc_kmajor_sw128(sbase + C::OFF_Q + (cq.seg % C::NQB) * C::QBYTES);
@@ -634,15 +643,15 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
         for (int c = 0; c < C::NCH_QK; ++c) {
 #pragma unroll
           for (int k = 0; k < 4; ++k)
-            umma_f16_ss(d, ad + static_cast<uint64_t>((c * 1024 + k * 32) >> 4),
-                        bd + static_cast<uint64_t>((c * C::QCHUNK + k * 32) >> 4), idesc_qk, (c | k) != 0);
+            umma_f16_ss_warp(d, ad + static_cast<uint64_t>((c * 1024 + k * 32) >> 4),
+                             bd + static_cast<uint64_t>((c * C::QCHUNK + k * 32) >> 4), idesc_qk, (c | k) != 0);
         }
 #pragma unroll
         for (int k = 0; k < C::RK; ++k)
-          umma_f16_ss(d, rd + static_cast<uint64_t>((k * 32) >> 4),
-                      bd + static_cast<uint64_t>((C::NCH_QK * C::QCHUNK + k * 32) >> 4), idesc_qk, 1u);
-        umma_commit(&s_full[sb]);
-        if (cq.tl + 1 == cq.t1) umma_commit(&q_empty[cq.seg % C::NQB]);  // last QK of the segment: Q free
+          umma_f16_ss_warp(d, rd + static_cast<uint64_t>((k * 32) >> 4),
+                           bd + static_cast<uint64_t>((C::NCH_QK * C::QCHUNK + k * 32) >> 4), idesc_qk, 1u);
+        umma_commit_warp(&s_full[sb]);
+        if (cq.tl + 1 == cq.t1) umma_commit_warp(&q_empty[cq.seg % C::NQB]);  // last QK of the segment: Q free
       };
       auto issue_pv = [&]() {
         tc_fence_after();
@@ -652,43 +661,51 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
         const uint64_t ad = desc_mnmajor_sw128(kv, 1024, C::LGRP);
         const uint64_t bd = C::P_SW128 ? desc_mnmajor_sw128(kv + C::OFF_R, 0)
                                        : desc_mnmajor_noswz(kv + C::OFF_R, 128, T * 16);
-        const uint32_t obuf = tmem + C::TMEM_O + (cp.seg % C::NOB) * C::OCOLS;
+        const uint32_t obuf = tm + C::TMEM_O + (cp.seg % C::NOB) * C::OCOLS;
         const bool first = (cp.tl == cp.t0);
 #pragma unroll
         for (int blk = 0; blk < C::NBLK_O; ++blk) {
 #pragma unroll
           for (int k = 0; k < T / 16; ++k)
-            umma_f16_ss(obuf + blk * NQ, ad + static_cast<uint64_t>((2 * blk * 1024 + k * 2 * C::LGRP) >> 4),
-                        bd + static_cast<uint64_t>((C::P_SW128 ? k * 2048 : k * 256) >> 4), idesc_pv,
-                        (!first || k > 0) ? 1u : 0u);
+            umma_f16_ss_warp(obuf + blk * NQ, ad + static_cast<uint64_t>((2 * blk * 1024 + k * 2 * C::LGRP) >> 4),
+                             bd + static_cast<uint64_t>((C::P_SW128 ? k * 2048 : k * 256) >> 4), idesc_pv,
+                             (!first || k > 0) ? 1u : 0u);
         }
-        umma_commit(&kv_empty[stage]);
-        umma_commit(&pv_done[j & 3]);
+        umma_commit_warp(&kv_empty[stage]);
+        umma_commit_warp(&pv_done[j & 3]);
       };
       long long t0 = clock64();
       while (pv_left) {
         bool did = false;
-        if (next_pv < next_qk && mbar_test_wait(smem_u32(&p_full[next_pv % NS]), (next_pv / NS) & 1)) {
+        if (next_pv < next_qk && probe(&p_full[next_pv % NS], (next_pv / NS) & 1)) {
           // first PV of a segment reuses O buffer (seg % NOB): the epilogue of
           // segment seg - NOB must have read it
           const bool first = (cp.tl == cp.t0);
-          if (!first || cp.seg < C::NOB ||
-              mbar_test_wait(smem_u32(&o_empty[cp.seg % C::NOB]), ((cp.seg - C::NOB) / C::NOB) & 1)) {
-            if (trace && next_pv < kTraceTiles) trace[12 + 8 * next_pv] = globaltimer();
+          if (!first || cp.seg < C::NOB || probe(&o_empty[cp.seg % C::NOB], ((cp.seg - C::NOB) / C::NOB) & 1)) {
+            if (trace && lane == 0 && next_pv < kTraceTiles) trace[12 + 12 * next_pv] = globaltimer();
             issue_pv();
+            if (trace && lane == 0 && next_pv < kTraceTiles) trace[17 + 12 * next_pv] = globaltimer();
             ++next_pv;
             pv_left = advance(cp);
             did = true;
           }
         }
-        if (!did && qk_left &&
-            mbar_test_wait(smem_u32(&kv_full[next_qk % NS]), (next_qk / NS) & 1) &&
-            mbar_test_wait(smem_u32(&s_empty[next_qk & 1]), ((next_qk >> 1) & 1) ^ 1)) {
+        // With >= 3 stages the QK stream runs at most one tile ahead of the PV
+        // stream: the tensor pipe then strictly alternates QK(i+1), PV(i) (an
+        // MMA issue blocks until it executes, so a second QK issued ahead
+        // would hold PV(i) back and starve the stage refill).  With two
+        // stages the refill itself needs PV(i) first, and greedy order wins.
+        // (checked right after a PV issue too: PV(i) + QK(i+2) then go out as
+        // one block, one scheduler round trip per tile)
+        if (qk_left && (NS < 3 || next_qk - next_pv <= 1) &&
+            probe(&kv_full[next_qk % NS], (next_qk / NS) & 1) &&
+            probe(&s_empty[next_qk & 1], ((next_qk >> 1) & 1) ^ 1)) {
           const bool first = (cq.tl == cq.t0);
-          if (!first || mbar_test_wait(smem_u32(&q_full[cq.seg % C::NQB]), (cq.seg / C::NQB) & 1)) {
-            if (trace && next_qk == 0) trace[1] = globaltimer();
-            if (trace && next_qk < kTraceTiles) trace[9 + 8 * next_qk] = globaltimer();
+          if (!first || probe(&q_full[cq.seg % C::NQB], (cq.seg / C::NQB) & 1)) {
+            if (trace && lane == 0 && next_qk == 0) trace[1] = globaltimer();
+            if (trace && lane == 0 && next_qk < kTraceTiles) trace[9 + 12 * next_qk] = globaltimer();
             issue_qk();
+            if (trace && lane == 0 && next_qk < kTraceTiles) trace[16 + 12 * next_qk] = globaltimer();
             ++next_qk;
             qk_left = advance(cq);
             did = true;
@@ -697,16 +714,14 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
         if (did) {
           t0 = clock64();
         } else {
-          // back off: this thread shares its SM sub-partition with two softmax
-          // warps; a tight test_wait loop steals their issue slots
-          __nanosleep(40);
-          if (clock64() - t0 > (1ll << 34)) {
-            printf("glad: MMA scheduler watchdog (cta %d qk %d pv %d)\n", cta, next_qk, next_pv);
+          if (GLAD_MMA_BACKOFF_NS > 0) __nanosleep(GLAD_MMA_BACKOFF_NS);
+          if (warp_uniform(clock64() - t0 > (1ll << 34))) {
+            if (lane == 0) printf("glad: MMA scheduler watchdog (cta %d qk %d pv %d)\n", cta, next_qk, next_pv);
             __trap();
           }
         }
       }
-      if (trace) trace[3] = cp.seg + 1;
+      if (trace && lane == 0) trace[3] = cp.seg + 1;
     }
   } else if (warp < 4 && !(warp == 3 && p.cp_kv && p.q_tma)) {
     // ========================= Q loader: TMA (one thread) or cp.async (64 threads) =========================
@@ -762,18 +777,17 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
     if (seg == 0) named_bar_arrive(3, 96);  // no work: release the producer
   } else {
     // ========================= softmax / correction / epilogue =========================
-    // Thread -> data: T = 128: token tr = 32*wq + lane, columns [c0, c0 + CW).
-    // T = 64 (M = 64 S^T: 16 lanes per quarter): token tr = 16*wq + lane % 16,
-    // columns [cb, cb + HC) with cb = c0 + (lane / 16) * HC.  O^T (M = 128) is
-    // always one d row per TMEM lane r = 32*wq + lane.
+    // Thread -> data: token row tr = 32*wq + lane of S^T (rows >= T carry no
+    // token: warp-uniform, they only join the barriers), columns [c0, c0 + CW);
+    // O^T: one d row per TMEM lane r = tr.
     constexpr int HC = C::HC, LANES = C::LANES;
     const int wg = (warp - 4) >> 2;
     const int wq = warp & 3;
     const int r = wq * 32 + lane;  // TMEM lane of O^T (d row)
-    const int half = T == 128 ? 0 : (lane >> 4);
-    const int tr = T == 128 ? r : wq * 16 + (lane & 15);  // token row of S^T within the tile
+    const int tr = r;              // token row of S^T within the tile
+    const bool row_ok = (T == 128) || (wq * 32 < T);
     const int c0 = wg * CW;
-    const int cb = c0 + half * HC;
+    const int cb = c0;
     const uint32_t lane_addr = static_cast<uint32_t>(wq * 32) << 16;
     const uint32_t bar_id = 1 + wg;
     const uint32_t nm_addr = smem_u32(nm_s + cb);
@@ -807,32 +821,35 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
         const int sb = it & 1;
         mbar_wait(&s_full[sb], (it >> 1) & 1);
         tc_fence_after();
-        if (trace && threadIdx.x == 128 && it < kTraceTiles) trace[10 + 8 * it] = globaltimer();
+        if (trace && threadIdx.x == 128 && it < kTraceTiles) trace[10 + 12 * it] = globaltimer();
         const int p0 = tl * T;
         const int tok = p0 + tr;
         const bool masked = !(p0 + T <= min_vend && all_cols);  // last tile / causal / padded columns
-        float x[HC];  // raw scores q.k for this thread's token and columns
-        // (re)loaded from TMEM instead of kept live across the vote: S(sb) is
-        // released only after it, so the rare path can read it again
-        auto load_x = [&]() {
+        // Raw scores q.k of this thread's token row, re-read from TMEM where
+        // needed instead of kept live across the vote (S(sb) is released only
+        // after it).  Rows >= T (warp-uniform) carry no token and skip it.
+        const uint32_t vend_addr = smem_u32(vend_s + cb);
+        auto load_x = [&](float (&x)[HC]) {
           tmem_load_s<C>(tmem + lane_addr + sb * NQ + c0, x);
           tmem_ld_wait();
-          if (masked) {
+          if (masked) {  // vend = 0 for padded columns
 #pragma unroll
-            for (int n = 0; n < HC; ++n) {
-              const bool ok = (cb + n < s.nq) && tok < vend_s[cb + n];
-              x[n] = ok ? x[n] : -INFINITY;
+            for (int n = 0; n < HC; n += 4) {
+              const float4 v = ld_shared_f4(vend_addr + n * 4);
+              x[n] = tok < __float_as_int(v.x) ? x[n] : -INFINITY;
+              x[n + 1] = tok < __float_as_int(v.y) ? x[n + 1] : -INFINITY;
+              x[n + 2] = tok < __float_as_int(v.z) ? x[n + 2] : -INFINITY;
+              x[n + 3] = tok < __float_as_int(v.w) ? x[n + 3] : -INFINITY;
             }
           }
         };
-        load_x();
         // p = 2^(s*c - m) with the lagging running max m (nm = -m, 0 while m is
         // -inf so masked scores give exactly 0 without a select), packed to bf16.
         // Lazy rescale: the max is only moved when some p exceeds 2^TAU (checked
         // on the packed bf16 bits, which order like unsigned ints for p >= 0) or
         // on the first tile of a segment; then p is recomputed.
         uint32_t pk[HC / 2];
-        auto exp_pack = [&]() {
+        auto exp_pack = [&](const float (&x)[HC]) {
 #pragma unroll
           for (int n = 0; n < HC; n += 4) {
             const float4 m4 = ld_shared_f4(nm_addr + n * 4);
@@ -845,17 +862,28 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
             pk[n / 2 + 1] = *reinterpret_cast<const uint32_t*>(&v1);
           }
         };
-        exp_pack();
-        uint32_t pmax = pk[0];
-#pragma unroll
-        for (int n = 1; n < HC / 2; ++n) pmax = max_u16x2(pmax, pk[n]);
         constexpr uint32_t kTrig = 0x4380u;  // bf16 bits of 2^TAU = 256
         static_assert(TAU == 8.f, "kTrig encodes 2^TAU");
-        const bool need = (tl == s.t0) | ((pmax & 0xffffu) > kTrig) | ((pmax >> 16) > kTrig);
+        bool need = (tl == s.t0);
+        if (row_ok) {
+          float x[HC];
+          load_x(x);
+          exp_pack(x);
+          uint32_t pmax = pk[0];
+#pragma unroll
+          for (int n = 1; n < HC / 2; ++n) pmax = max_u16x2(pmax, pk[n]);
+          need |= ((pmax & 0xffffu) > kTrig) | ((pmax >> 16) > kTrig);
+        }
         if (named_bar_red_or(bar_id, 128, need)) {
           // the running max moves by > 2^TAU somewhere: column max over the WG
           // (in pieces of <= 16 columns to bound register pressure)
-          load_x();
+          float x[HC];
+          if (row_ok) {
+            load_x(x);
+          } else {
+#pragma unroll
+            for (int n = 0; n < HC; ++n) x[n] = -INFINITY;
+          }
           constexpr int HW = HC > 16 ? 16 : HC;
 #pragma unroll
           for (int h0 = 0; h0 < HC; h0 += HW) {
@@ -907,27 +935,34 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
             }
             tmem_st_wait();
           }
-          load_x();  // again: keeps x dead across the O^T rescale (register pressure)
-          exp_pack();
+          if (row_ok) {  // again: keeps x dead across the O^T rescale (register pressure)
+            float x2[HC];
+            load_x(x2);
+            exp_pack(x2);
+          }
         }
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&s_empty[sb]);
         // row sum from the bf16-rounded p the PV multiplies (numerator and
         // denominator consistent; the fp32 sum failed the peaked parity case)
+        if (row_ok) {
 #pragma unroll
-        for (int n = 0; n < HC; n += 2) {
-          const float2 v = make_float2(__uint_as_float(pk[n / 2] << 16), __uint_as_float(pk[n / 2] & 0xffff0000u));
-          const float2 acc = fadd2(make_float2(l[n], l[n + 1]), v);
-          l[n] = acc.x;
-          l[n + 1] = acc.y;
+          for (int n = 0; n < HC; n += 2) {
+            const float2 v =
+                make_float2(__uint_as_float(pk[n / 2] << 16), __uint_as_float(pk[n / 2] & 0xffff0000u));
+            const float2 acc = fadd2(make_float2(l[n], l[n + 1]), v);
+            l[n] = acc.x;
+            l[n + 1] = acc.y;
+          }
         }
         // bf16 P^T into the tile's (now dead) RoPE chunk.  NQ = 64: MN-major
         // 128B-swizzled rows of 64 queries (token tr at tr*128, 16-B chunk j at
         // j ^ (tr & 7)); else no-swizzle core matrices [NQ/8][T tok][8].
         const uint32_t stage_base = sbase + (it % NS) * C::STAGE;
         const uint32_t pbase = stage_base + C::OFF_R;
-        if constexpr (HC >= 8) {
+        static_assert(HC % 8 == 0, "P^T rows are stored in 16-B pieces");
+        if (row_ok) {
 #pragma unroll
           for (int g = 0; g < HC / 8; ++g) {
             const int j = cb / 8 + g;
@@ -935,10 +970,8 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
                 C::P_SW128 ? pbase + tr * 128 + ((j ^ (tr & 7)) << 4) : pbase + j * (T * 16) + tr * 16;
             st_shared_v4(pa, pk[g * 4], pk[g * 4 + 1], pk[g * 4 + 2], pk[g * 4 + 3]);
           }
-        } else {  // HC == 4 (NQ = 16, T = 64): half a core-matrix row per thread
-          st_shared_v2(pbase + (cb / 8) * (T * 16) + tr * 16 + (cb % 8) * 2, pk[0], pk[1]);
         }
-        if (wg == 0 && half == 0 && tok >= s.kv_end) {  // never-visible rows: zero V (0 * garbage != NaN)
+        if (wg == 0 && row_ok && tok >= s.kv_end) {  // never-visible rows: zero V (0 * garbage != NaN)
           const uint32_t kvrow = stage_base + (tr >> 3) * C::LGRP + (tr & 7) * 128;
 #pragma unroll
           for (int ch = 0; ch < C::NCH_V; ++ch)
@@ -949,8 +982,8 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&p_full[it % NS]);
-        if (trace && threadIdx.x == 128 && it < kTraceTiles) trace[11 + 8 * it] = globaltimer();
-        if (trace && threadIdx.x == 256 && it < kTraceTiles) trace[14 + 8 * it] = globaltimer();
+        if (trace && threadIdx.x == 128 && it < kTraceTiles) trace[11 + 12 * it] = globaltimer();
+        if (trace && threadIdx.x == 256 && it < kTraceTiles) trace[14 + 12 * it] = globaltimer();
       }
 
       // ------------------------------------------------------- segment epilogue
@@ -1025,7 +1058,7 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
         }
       }
       named_bar_sync(bar_id, 128);  // alpha_s / m_run reads done before the next segment resets them
-      if (trace && threadIdx.x == 128 && it - 1 < kTraceTiles) trace[15 + 8 * (it - 1)] = globaltimer();
+      if (trace && threadIdx.x == 128 && it - 1 < kTraceTiles) trace[15 + 12 * (it - 1)] = globaltimer();
       ++seg;
     }
   }

@@ -1,0 +1,85 @@
+// Instantiation helpers shared by the decode_inst_t*.cu translation units
+// (one per tile height, compiled in parallel).
+#pragma once
+#include "internal.h"
+
+namespace glad {
+
+template <int DV, int DKN, int DR, int NQ, int T>
+cudaError_t launch_one(const CUtensorMap& tmap, const CUtensorMap& lmap, const CUtensorMap& qmap,
+                       const DecodeParams& p, int grid, cudaStream_t stream) {
+  using C = DecodeCfg<DV, DKN, DR, NQ, T>;
+  static bool attr_set = false;  // benign race: idempotent attribute set
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(decode_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         C::SMEM_BYTES);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  decode_kernel<C><<<grid, C::NTHREADS, C::SMEM_BYTES, stream>>>(tmap, lmap, qmap, p);
+  return cudaGetLastError();
+}
+
+// Calls f.template run<C>() for the DecodeCfg matching (key, T); returns
+// cudaErrorInvalidValue for an unsupported key.
+template <int T, class F>
+cudaError_t with_cfg(const DecodeKey& k, F&& f) {
+#define GLAD_NQ(DV, DKN, DR)                                                  \
+  switch (k.nq) {                                                             \
+    case 16: return f.template run<DecodeCfg<DV, DKN, DR, 16, T>>();          \
+    case 32: return f.template run<DecodeCfg<DV, DKN, DR, 32, T>>();          \
+    case 64: return f.template run<DecodeCfg<DV, DKN, DR, 64, T>>();          \
+    default: return cudaErrorInvalidValue;                                    \
+  }
+  if (k.d_kn == k.d_v) {
+    if (k.d_v == 128 && k.d_r == 32) { GLAD_NQ(128, 128, 32) }
+    if (k.d_v == 128 && k.d_r == 64) { GLAD_NQ(128, 128, 64) }
+    if (k.d_v == 256 && k.d_r == 32) { GLAD_NQ(256, 256, 32) }
+    if (k.d_v == 256 && k.d_r == 64) { GLAD_NQ(256, 256, 64) }
+    if (k.d_v == 512 && k.d_r == 64) { GLAD_NQ(512, 512, 64) }
+  } else if (k.d_v == 128 && k.d_kn == 64 && k.d_r == 64) {
+    GLAD_NQ(128, 64, 64)
+  }
+#undef GLAD_NQ
+  return cudaErrorInvalidValue;
+}
+
+struct LaunchF {
+  const CUtensorMap &tmap, &lmap, &qmap;
+  const DecodeParams& p;
+  int grid;
+  cudaStream_t s;
+  template <class C>
+  cudaError_t run() {
+    return launch_one<C::D_V, C::D_KN, C::D_R, C::NQ, C::T>(tmap, lmap, qmap, p, grid, s);
+  }
+};
+
+struct StagesF {
+  int* ns;
+  template <class C>
+  cudaError_t run() {
+    *ns = C::NS;
+    return cudaSuccess;
+  }
+};
+
+template <int T>
+cudaError_t launch_decode_t(const DecodeKey& k, const CUtensorMap& tmap, const CUtensorMap& lmap,
+                            const CUtensorMap& qmap, const DecodeParams& p, int grid, cudaStream_t s);
+template <int T>
+int decode_stages_t(const DecodeKey& k);
+
+#define GLAD_INSTANTIATE_T(T)                                                                              \
+  template <>                                                                                              \
+  cudaError_t launch_decode_t<T>(const DecodeKey& k, const CUtensorMap& tmap, const CUtensorMap& lmap,     \
+                                 const CUtensorMap& qmap, const DecodeParams& p, int grid, cudaStream_t s) { \
+    return with_cfg<T>(k, LaunchF{tmap, lmap, qmap, p, grid, s});                                          \
+  }                                                                                                        \
+  template <>                                                                                              \
+  int decode_stages_t<T>(const DecodeKey& k) {                                                             \
+    int ns = 0;                                                                                            \
+    return with_cfg<T>(k, StagesF{&ns}) == cudaSuccess ? ns : 0;                                           \
+  }
+
+}  // namespace glad

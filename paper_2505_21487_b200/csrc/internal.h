@@ -12,7 +12,7 @@ namespace glad {
 // Kernel family key: value width, key-from-state width, rope width, query
 // rows per CTA.
 struct DecodeKey {
-  int d_v, d_kn, d_r, nq, t;  // t: tokens per KV tile (128, or 64)
+  int d_v, d_kn, d_r, nq, t;  // t: tokens per KV tile (64 / 96 / 128)
 };
 
 // Returns cudaErrorInvalidValue (and does not launch) if no instantiation
@@ -20,6 +20,7 @@ struct DecodeKey {
 cudaError_t launch_decode(const DecodeKey& key, const CUtensorMap& tmap, const CUtensorMap& lmap, const CUtensorMap& qmap, const DecodeParams& p, int grid,
                           cudaStream_t stream);
 bool decode_supported(const DecodeKey& key);
+int decode_stages(const DecodeKey& key);  // KV pipeline stages of the instantiation (0: unsupported)
 int decode_max_nq(int d_v);
 
 cudaError_t launch_plan(const int32_t* seqlens, int32_t* plan, int U, int B, int tile, int n_qblk, int nq_blk, int Lq,

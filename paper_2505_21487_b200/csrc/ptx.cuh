@@ -179,6 +179,30 @@ __device__ __forceinline__ void umma_f16_ss(uint32_t d_tmem, uint64_t adesc, uin
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+// Warp-collective forms: the whole (converged) warp executes them, one
+// elected lane issues.  Keeping the MMA warp's control flow uniform lets
+// ptxas hold the descriptors in uniform registers (no R2UR + waterfall loop
+// per tcgen05.mma, which made the issue slower than the tensor pipe).
+__device__ __forceinline__ void umma_f16_ss_warp(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                                 uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred e, p;\n\telect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void umma_commit_warp(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(smem_u32(bar))
+      : "memory");
+}
+// Warp-uniform copies of per-lane values (REDUX / VOTE results are uniform).
+__device__ __forceinline__ int warp_uniform(int v) {
+  return static_cast<int>(__reduce_max_sync(0xffffffffu, static_cast<unsigned>(v)));
+}
+__device__ __forceinline__ bool warp_uniform(bool v) { return __all_sync(0xffffffffu, v); }
+
 // Arrive (once) on an mbarrier when all previously issued tcgen05 async ops of
 // this thread complete.  Implies tcgen05.fence::before_thread_sync.
 __device__ __forceinline__ void umma_commit(uint64_t* bar) {

@@ -231,7 +231,7 @@ def kv_bytes_per_token_per_device(variant, n_kv_heads, d_head, d_rope, N, dtype_
     return lib().glad_kv_bytes_per_token_per_device(variant, n_kv_heads, d_head, d_rope, N, dtype_bytes)
 
 
-TRACE_STRIDE = 8 + 8 * 128
+TRACE_STRIDE = 8 + 12 * 128
 
 
 def debug_set_trace(buf):
@@ -245,7 +245,7 @@ def debug_set_phase_mask(mask):
 
 
 def debug_set_tile(tokens):
-    """Debug/benchmark: force 64- or 128-token KV tiles (0 = library choice)."""
+    """Debug/benchmark: force 64-, 96- or 128-token KV tiles (0 = library choice)."""
     lib().glad_debug_set_tile(int(tokens))
 
 

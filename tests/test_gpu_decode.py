@@ -119,9 +119,10 @@ GLA_SWEEP = [
 ]
 
 
-@pytest.fixture(params=[64, 128], ids=["T64", "T128"])
+@pytest.fixture(params=[64, 96, 128], ids=["T64", "T96", "T128"])
 def tile(request):
-    """Both KV tile heights (64-token tiles use M=64 QK and 16-lane S^T loads)."""
+    """Every KV tile height (T < 128: the M=128 QK rows >= T read past the
+    tile and must be discarded; T = 96 with pages >= 32 uses 32-row boxes)."""
     glad.debug_set_tile(request.param)
     yield request.param
     glad.debug_set_tile(0)

@@ -23,9 +23,12 @@ from paper_2505_21487_b200 import glad, workloads  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--workload", default="c2_gla2")
 ap.add_argument("--ctas", type=int, default=0)
+ap.add_argument("--tile", type=int, default=0)
 ap.add_argument("--ns", type=int, default=2, help="KV stages of the instantiation (for PV->load)")
 a = ap.parse_args()
 wl = workloads.get(a.workload)
+if a.tile:
+    glad.debug_set_tile(a.tile)
 st = workloads.build_device_state(wl, num_ctas=a.ctas)
 for _ in range(3):
     workloads.run(wl, st)
@@ -46,8 +49,8 @@ print("CTA start (us, percentiles 0/50/90/100): " + " ".join(f"{np.percentile(_s
       "; end: " + " ".join(f"{np.percentile(_en, q):.1f}" for q in (0, 10, 50, 90, 100)))
 print(f"CTA lifetime median {np.median(tr[:, 2] - tr[:, 0]) / 1e3:.1f} us, start->Q ready "
       f"{np.median(tr[:, 1] - tr[:, 0]) / 1e3:.2f} us")
-T = (tr.shape[1] - 8) // 8
-tile = tr[:, 8:].reshape(len(tr), T, 8)  # load, qk, s, p, pv, free, p_wg1, epi
+T = (tr.shape[1] - 8) // 12
+tile = tr[:, 8:].reshape(len(tr), T, 12)  # load, qk, s, p, pv, free, p_wg1, epi, qk_ret, pv_ret, landed, -
 valid = tile[:, :, 1] > 0
 ntile = valid.sum(1)
 
@@ -98,9 +101,9 @@ print(f"  epilogue: S(last)->epi done {np.nanmedian(np.where(epi > 0, epi - tile
 if os.environ.get("TRACE_RAW"):
     c = int(os.environ.get("TRACE_CTA", "5"))
     base = tr[c, 0]
-    print(f"raw timeline of CTA {c} (us from CTA start): free, load, QK, S, P0, P1, PV, epi")
+    print(f"raw timeline of CTA {c} (us from CTA start): free, load, landed, QK, QKret, S, P0, P1, PV, PVret, epi")
     for i in range(int(os.environ.get("TRACE_FROM", "0")), int(os.environ.get("TRACE_TO", "128"))):
         if tile[c, i, 1] == 0:
             break
         print(f"  tile {i:2d}: " + "  ".join(f"{(tile[c, i, j] - base) / 1e3:8.2f}" if tile[c, i, j] else "       -"
-                                          for j in (5, 0, 1, 2, 3, 6, 4, 7)))
+                                          for j in (5, 0, 10, 1, 8, 2, 3, 6, 4, 9, 7)))
