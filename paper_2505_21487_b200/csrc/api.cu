@@ -265,11 +265,13 @@ glad_status decode_common(Variant v, const void* q, const void* pool, const glad
   p.causal = causal ? 1 : 0;
   p.scale_log2 = scale * 1.4426950408889634f;
   p.trace = g_trace;
+
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   int32_t* plan = reinterpret_cast<int32_t*>(wsb + wl.plan);
   cudaError_t e = cudaSuccess;
   if (g_phase_mask & 1) {
-    e = glad::launch_plan(seqlens, plan, p.n_units, B, g.key.t, g.n_qblk, g.key.nq, Lq, g.g_q, p.causal, st);
+    e = glad::launch_plan(seqlens, plan, p.n_units, B, g.key.t, g.n_qblk, g.key.nq, Lq, g.g_q, p.causal, H,
+                          L->d_head, out, lse, nullptr, st);
     if (e != cudaSuccess) return fail(GLAD_ERR_CUDA, "plan launch failed: %s", cudaGetErrorString(e));
   }
   if (g_phase_mask & 2) {
@@ -277,9 +279,8 @@ glad_status decode_common(Variant v, const void* q, const void* pool, const glad
     if (e != cudaSuccess) return fail(GLAD_ERR_CUDA, "decode launch failed: %s", cudaGetErrorString(e));
   }
   if (g_phase_mask & 4) {
-    e = glad::launch_merge_units(plan, p.o_part, p.lse_part, G, p.n_units, g.key.nq, g.n_qblk, B, L->n_heads_kv,
-                                 head_groups, g.g_q, Lq, H, static_cast<int64_t>(B) * Lq * H, L->d_head, out, lse,
-                                 st);
+    e = glad::launch_merge_split(plan, p.o_part, p.lse_part, G, p.n_units, g.key.nq, g.n_qblk, B, L->n_heads_kv,
+                                 head_groups, g.g_q, Lq, H, L->d_head, out, lse, st);
     if (e != cudaSuccess) return fail(GLAD_ERR_CUDA, "merge launch failed: %s", cudaGetErrorString(e));
   }
   return GLAD_OK;

@@ -86,9 +86,14 @@ __global__ void combine_kernel(const float* __restrict__ o_part, const float* __
 }
 
 // Decode schedule plan (one CTA): tiles per unit u = (b, head, query block)
-// -> exclusive prefix sum plan[0..U]; plan[U] = total tiles.
-__global__ void plan_kernel(const int32_t* __restrict__ seqlens, int32_t* __restrict__ plan, int U, int B, int tile,
-                            int n_qblk, int nq_blk, int Lq, int g_q, int causal) {
+// -> exclusive prefix sum plan[0..U]; plan[U] = total tiles.  Also writes
+// the output of units with no visible key (zeros, lse = -inf), which no
+// decode CTA visits.
+__global__ void plan_kernel(const int32_t* __restrict__ seqlens, int32_t* __restrict__ plan, int U, int B,
+                            int tile, int n_qblk, int nq_blk, int Lq, int g_q,
+                            int causal, int H, int d_v, __nv_bfloat16* __restrict__ out, float* __restrict__ lse,
+                            uint64_t* trace) {
+  if (trace && threadIdx.x == 0) trace[0] = globaltimer();
   __shared__ int warp_sums[32];
   __shared__ int carry;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
@@ -106,6 +111,16 @@ __global__ void plan_kernel(const int32_t* __restrict__ seqlens, int32_t* __rest
       int kv_end = L;
       if (causal) kv_end = max(0, min(L, L - Lq + (n0 + nq - 1) / g_q + 1));
       tiles = (kv_end + tile - 1) / tile;
+      if (tiles == 0) {  // no visible key: no decode CTA visits the unit (rare; one thread per unit)
+        const int head = (u / n_qblk) / B;
+        for (int n = 0; n < nq; ++n) {
+          const int ng = n0 + n, t = ng / g_q, h = head * g_q + (ng - t * g_q);
+          const int64_t row = (static_cast<int64_t>(b) * Lq + t) * H + h;
+          uint4* o = reinterpret_cast<uint4*>(out + row * d_v);
+          for (int d = 0; d < d_v / 8; ++d) o[d] = make_uint4(0u, 0u, 0u, 0u);
+          lse[row] = -INFINITY;
+        }
+      }
     }
     int v = tiles;  // inclusive warp scan
 #pragma unroll
@@ -132,87 +147,127 @@ __global__ void plan_kernel(const int32_t* __restrict__ seqlens, int32_t* __rest
     __syncthreads();
   }
   if (threadIdx.x == 0) plan[U] = carry;
+  __syncthreads();
+  if (trace && threadIdx.x == 0) trace[1] = globaltimer();
 }
 
-// Merge the partial segments of units that a CTA range boundary cut (the
-// split-KV LSE merge); write zeros / -inf for units with no visible key.
-// One warp per output row (b, t, h).  Units finished inside one CTA were
-// written by the decode kernel and are skipped.
-__global__ void merge_units_kernel(const int32_t* __restrict__ plan, const float* __restrict__ o_part,
-                                   const float* __restrict__ lse_part, int G, int U, int nq_blk, int n_qblk,
-                                   int B, int n_heads, int head_groups, int g_q, int Lq, int H, int64_t rows, int d_v,
-                                   __nv_bfloat16* __restrict__ out, float* __restrict__ lse) {
-  const int64_t row = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (row >= rows) return;
-  const int h = static_cast<int>(row % H);
-  const int64_t bt = row / H;
-  const int t = static_cast<int>(bt % Lq);
-  const int b = static_cast<int>(bt / Lq);
-  const int head = h / g_q, j = h - head * g_q;
-  const int ng = t * g_q + j;
-  const int qb = ng / nq_blk, n = ng - qb * nq_blk;
-  const int u = (head * B + b) * n_qblk + qb;
-  const int pu0 = plan[u], pu1 = plan[u + 1], total = plan[U];
-  if (pu1 == pu0) {  // no visible key
-    for (int d = lane * 8; d < d_v; d += 256)
-      *reinterpret_cast<uint4*>(out + row * d_v + d) = make_uint4(0u, 0u, 0u, 0u);
-    if (lane == 0) lse[row] = -INFINITY;
-    return;
-  }
-  const int c_first = cta_of_tile(pu0, G, total, n_heads, head_groups);
-  const int c_last = cta_of_tile(pu1 - 1, G, total, n_heads, head_groups);
-  if (c_first == c_last) return;
-  float mx = -INFINITY;
-  for (int c = c_first + lane; c <= c_last; c += 32)
-    mx = fmaxf(mx, lse_part[static_cast<int64_t>(c + u) * nq_blk + n]);
-#pragma unroll
-  for (int o = 16; o >= 1; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-  float z = 0.f;
-  for (int c = c_first + lane; c <= c_last; c += 32) {
-    const float ls = lse_part[static_cast<int64_t>(c + u) * nq_blk + n];
-    if (ls != -INFINITY) z += __expf(ls - mx);
-  }
-#pragma unroll
-  for (int o = 16; o >= 1; o >>= 1) z += __shfl_xor_sync(0xffffffffu, z, o);
-  if (lane == 0) lse[row] = (z > 0.f) ? mx + __logf(z) : -INFINITY;
-  const float inv_z = (z > 0.f) ? 1.f / z : 0.f;
-  for (int d0 = lane * 8; d0 < d_v; d0 += 256) {
-    float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-    for (int c = c_first; c <= c_last; ++c) {
-      const int64_t slot = static_cast<int64_t>(c + u) * nq_blk + n;
-      const float ls = lse_part[slot];
-      if (ls == -INFINITY) continue;
-      const float w = __expf(ls - mx) * inv_z;
-      const float4* src = reinterpret_cast<const float4*>(o_part + slot * d_v + d0);
-      const float4 a = __ldg(src), c4 = __ldg(src + 1);
-      acc[0] += w * a.x; acc[1] += w * a.y; acc[2] += w * a.z; acc[3] += w * a.w;
-      acc[4] += w * c4.x; acc[5] += w * c4.y; acc[6] += w * c4.z; acc[7] += w * c4.w;
-    }
-    uint4 v;
-    v.x = pack_bf16x2(acc[0], acc[1]);
-    v.y = pack_bf16x2(acc[2], acc[3]);
-    v.z = pack_bf16x2(acc[4], acc[5]);
-    v.w = pack_bf16x2(acc[6], acc[7]);
-    *reinterpret_cast<uint4*>(out + row * d_v + d0) = v;
-  }
-}
-
-cudaError_t launch_plan(const int32_t* seqlens, int32_t* plan, int U, int B, int tile, int n_qblk, int nq_blk, int Lq,
-                        int g_q, int causal, cudaStream_t stream) {
-  plan_kernel<<<1, 1024, 0, stream>>>(seqlens, plan, U, B, tile, n_qblk, nq_blk, Lq, g_q, causal);
+cudaError_t launch_plan(const int32_t* seqlens, int32_t* plan, int U, int B, int tile, int n_qblk, int nq_blk,
+                        int Lq, int g_q, int causal, int H, int d_v, void* out, float* lse, uint64_t* trace,
+                        cudaStream_t stream) {
+  plan_kernel<<<1, 1024, 0, stream>>>(seqlens, plan, U, B, tile, n_qblk, nq_blk, Lq, g_q, causal, H, d_v,
+                                      static_cast<__nv_bfloat16*>(out), lse, trace);
   return cudaGetLastError();
 }
 
-cudaError_t launch_merge_units(const int32_t* plan, const float* o_part, const float* lse_part, int G, int U,
+// Split-KV LSE merge of the units that CTA range boundaries cut (
+// oracle.attention.merge_partials).  Block b looks at the boundary between
+// decode CTAs b-1 and b: if it cuts a unit and is that unit's first cut, the
+// block merges the partials (workspace slots c + u, c = first..last CTA of
+// the unit) into out / lse.  All other blocks exit at once.
+constexpr int kMergeThreads = 256;
+constexpr int kMergeMaxParts = 8;  // weights staged per pass
+__global__ void __launch_bounds__(kMergeThreads) merge_split_kernel(
+    const int32_t* __restrict__ plan, const float* __restrict__ o_part, const float* __restrict__ lse_part, int G,
+    int U, int nq_blk, int n_qblk, int B, int n_heads, int head_groups, int g_q, int Lq, int H, int d_v,
+    __nv_bfloat16* __restrict__ out, float* __restrict__ lse) {
+  __shared__ int u_s;
+  __shared__ float w_s[kMergeMaxParts][64];
+  __shared__ float mx_s[64], iz_s[64];
+  const int b_cta = blockIdx.x + 1;  // boundary between CTAs b-1 and b
+  const int total = __ldg(plan + U);
+  const CtaRange rg = cta_range(b_cta, G, total, n_heads, head_groups);
+  if (rg.t0 >= rg.t1) return;
+  const int t = rg.t0;
+  // unit containing tile t: 32-ary search by warp 0 (last u with plan[u] <= t)
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    int lo = 0, hi = U - 1;
+    while (lo < hi) {
+      const int step = (hi - lo + 32) / 32;
+      const int idx = lo + lane * step;
+      const bool ok = idx <= hi && __ldg(plan + idx) <= t;
+      const unsigned m = __ballot_sync(0xffffffffu, ok);
+      lo = lo + (31 - __clz(m)) * step;
+      hi = min(hi, lo + step - 1);
+    }
+    if (lane == 0) u_s = lo;
+  }
+  __syncthreads();
+  const int u = u_s;
+  const int pu0 = __ldg(plan + u), pu1 = __ldg(plan + u + 1);
+  if (pu0 == t) return;  // the unit starts at this boundary: not cut here
+  const int cf = cta_of_tile(pu0, G, total, n_heads, head_groups);
+  if (cf != b_cta - 1) return;  // an earlier boundary cuts it: that block merges
+  const int cl = cta_of_tile(pu1 - 1, G, total, n_heads, head_groups);
+  const int qb = u % n_qblk, hb = u / n_qblk, b = hb % B, head = hb / B;
+  const int n0 = qb * nq_blk;
+  const int nq = min(nq_blk, Lq * g_q - n0);
+  const float* lp = lse_part + static_cast<int64_t>(u) * nq_blk;  // slot c: + c * nq_blk
+  for (int n = threadIdx.x; n < nq; n += kMergeThreads) {
+    float mx = -INFINITY;
+    for (int c = cf; c <= cl; ++c) mx = fmaxf(mx, lp[static_cast<int64_t>(c) * nq_blk + n]);
+    float z = 0.f;
+    if (mx != -INFINITY)
+      for (int c = cf; c <= cl; ++c) z += __expf(lp[static_cast<int64_t>(c) * nq_blk + n] - mx);
+    const int ng = n0 + n, tq = ng / g_q, h = head * g_q + (ng - tq * g_q);
+    lse[(static_cast<int64_t>(b) * Lq + tq) * H + h] = z > 0.f ? mx + __logf(z) : -INFINITY;
+    mx_s[n] = mx;
+    iz_s[n] = z > 0.f ? 1.f / z : 0.f;
+  }
+  // items (column n, 4 consecutive d): thread-strided, weights staged per
+  // pass of <= kMergeMaxParts partials
+  const int d4n = d_v / 4;
+  const int items = nq * d4n;
+  constexpr int kPer = 8;  // items per thread per sweep (loads in flight)
+  for (int base = 0; base < items; base += kMergeThreads * kPer) {
+    float4 acc[kPer];
+#pragma unroll
+    for (int i = 0; i < kPer; ++i) acc[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int c0 = cf; c0 <= cl; c0 += kMergeMaxParts) {
+      const int np = min(kMergeMaxParts, cl + 1 - c0);
+      __syncthreads();
+      for (int k = threadIdx.x; k < np * nq; k += kMergeThreads) {
+        const int cc = k / nq, n = k - cc * nq;
+        const float mx = mx_s[n];
+        w_s[cc][n] = mx == -INFINITY ? 0.f : __expf(lp[static_cast<int64_t>(c0 + cc) * nq_blk + n] - mx) * iz_s[n];
+      }
+      __syncthreads();
+      for (int cc = 0; cc < np; ++cc) {
+        const float4* src = reinterpret_cast<const float4*>(o_part + static_cast<int64_t>(c0 + cc + u) * nq_blk * d_v);
+        float4 v[kPer];
+#pragma unroll
+        for (int i = 0; i < kPer; ++i) {
+          const int it = base + i * kMergeThreads + threadIdx.x;
+          v[i] = it < items ? __ldg(src + (it / d4n) * d4n + (it % d4n)) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+        for (int i = 0; i < kPer; ++i) {
+          const int it = base + i * kMergeThreads + threadIdx.x;
+          const float w = it < items ? w_s[cc][it / d4n] : 0.f;
+          acc[i].x += w * v[i].x; acc[i].y += w * v[i].y; acc[i].z += w * v[i].z; acc[i].w += w * v[i].w;
+        }
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < kPer; ++i) {
+      const int it = base + i * kMergeThreads + threadIdx.x;
+      if (it < items) {
+        const int n = it / d4n, d = (it % d4n) * 4;
+        const int ng = n0 + n, tq = ng / g_q, h = head * g_q + (ng - tq * g_q);
+        *reinterpret_cast<uint2*>(out + ((static_cast<int64_t>(b) * Lq + tq) * H + h) * d_v + d) =
+            make_uint2(pack_bf16x2(acc[i].x, acc[i].y), pack_bf16x2(acc[i].z, acc[i].w));
+      }
+    }
+  }
+}
+
+cudaError_t launch_merge_split(const int32_t* plan, const float* o_part, const float* lse_part, int G, int U,
                                int nq_blk, int n_qblk, int B, int n_heads, int head_groups, int g_q, int Lq, int H,
-                               int64_t rows, int d_v, void* out, float* lse, cudaStream_t stream) {
-  if (rows == 0) return cudaSuccess;
-  const int threads = 128;
-  const int64_t blocks = (rows * 32 + threads - 1) / threads;
-  merge_units_kernel<<<static_cast<unsigned>(blocks), threads, 0, stream>>>(
-      plan, o_part, lse_part, G, U, nq_blk, n_qblk, B, n_heads, head_groups, g_q, Lq, H, rows, d_v,
-      static_cast<__nv_bfloat16*>(out), lse);
+                               int d_v, void* out, float* lse, cudaStream_t stream) {
+  if (G < 2) return cudaSuccess;
+  merge_split_kernel<<<G - 1, kMergeThreads, 0, stream>>>(plan, o_part, lse_part, G, U, nq_blk, n_qblk, B, n_heads,
+                                                          head_groups, g_q, Lq, H, d_v,
+                                                          static_cast<__nv_bfloat16*>(out), lse);
   return cudaGetLastError();
 }
 

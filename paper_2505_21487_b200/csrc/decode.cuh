@@ -334,6 +334,7 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int cta = blockIdx.x;
+  if (p.trace && threadIdx.x == 0) p.trace[static_cast<size_t>(cta) * kTraceStride + 7] = globaltimer();
 
   // ------------------------------------------------------------- setup
   if (warp == 0) {

@@ -23,11 +23,12 @@ bool decode_supported(const DecodeKey& key);
 int decode_stages(const DecodeKey& key);  // KV pipeline stages of the instantiation (0: unsupported)
 int decode_max_nq(int d_v);
 
-cudaError_t launch_plan(const int32_t* seqlens, int32_t* plan, int U, int B, int tile, int n_qblk, int nq_blk, int Lq,
-                        int g_q, int causal, cudaStream_t stream);
-cudaError_t launch_merge_units(const int32_t* plan, const float* o_part, const float* lse_part, int G, int U,
+cudaError_t launch_plan(const int32_t* seqlens, int32_t* plan, int U, int B, int tile, int n_qblk, int nq_blk,
+                        int Lq, int g_q, int causal, int H, int d_v, void* out, float* lse, uint64_t* trace,
+                        cudaStream_t stream);
+cudaError_t launch_merge_split(const int32_t* plan, const float* o_part, const float* lse_part, int G, int U,
                                int nq_blk, int n_qblk, int B, int n_heads, int head_groups, int g_q, int Lq, int H,
-                               int64_t rows, int d_v, void* out, float* lse, cudaStream_t stream);
+                               int d_v, void* out, float* lse, cudaStream_t stream);
 cudaError_t launch_append(void* pool, int64_t row_stride, int page_size, const int32_t* block_table,
                           int32_t bt_stride, const int32_t* seqlens_before, const void* rows, int32_t B,
                           int32_t n_new, int32_t width, cudaStream_t stream);

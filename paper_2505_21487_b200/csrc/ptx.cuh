@@ -78,14 +78,21 @@ __device__ __forceinline__ void tc_fence_after() {
 }
 
 // ---------------------------------------------------------------- barriers
+// bar.sync / bar.arrive / bar.red are warp-aligned: a warp that reaches one
+// while diverged is counted whole as soon as its first threads arrive, and
+// the barrier can release before the rest of the warp gets there.  Every
+// named barrier therefore reconverges its warp first.
 __device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t nthreads) {
+  __syncwarp();
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 __device__ __forceinline__ void named_bar_arrive(uint32_t id, uint32_t nthreads) {
+  __syncwarp();
   asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 __device__ __forceinline__ bool named_bar_red_or(uint32_t id, uint32_t nthreads, bool v) {
   uint32_t r;
+  __syncwarp();
   asm volatile(
       "{\n\t.reg .pred pi, po;\n\tsetp.ne.u32 pi, %1, 0;\n\tbarrier.cta.red.or.pred po, %2, %3, pi;\n\tselp.u32 %0, 1, "
       "0, po;\n\t}"
@@ -361,7 +368,7 @@ __device__ __forceinline__ uint32_t max_u16x2(uint32_t a, uint32_t b) {
 // --------------------------------------------------------------- misc
 __device__ __forceinline__ uint64_t globaltimer() {
   uint64_t t;
-  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t) : : "memory");  // not hoisted across barriers
   return t;
 }
 __device__ __forceinline__ float ex2(float x) {

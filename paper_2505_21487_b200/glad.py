@@ -10,7 +10,8 @@ import os
 
 import torch
 
-_LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libglad.so")
+# GLAD_LIB: debug/A-B override of the library file (default: the in-tree build)
+_LIB_PATH = os.environ.get("GLAD_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libglad.so")
 _lib = None
 
 GLAD_OK, GLAD_ERR_INVALID_ARG, GLAD_ERR_UNSUPPORTED, GLAD_ERR_WORKSPACE, GLAD_ERR_CUDA = range(5)

@@ -47,6 +47,8 @@ _st = np.sort(tr[:, 0] - t0) / 1e3
 _en = np.sort(tr[:, 2] - t0) / 1e3
 print("CTA start (us, percentiles 0/50/90/100): " + " ".join(f"{np.percentile(_st, q):.1f}" for q in (0, 50, 90, 100)) +
       "; end: " + " ".join(f"{np.percentile(_en, q):.1f}" for q in (0, 10, 50, 90, 100)))
+print(f"kernel entry -> CTA start (setup) us: median {np.median(tr[:, 0] - tr[:, 7]) / 1e3:.1f} max {np.max(tr[:, 0] - tr[:, 7]) / 1e3:.1f}; "
+      f"entry spread {(tr[:, 7].max() - tr[:, 7].min()) / 1e3:.1f}")
 print(f"CTA lifetime median {np.median(tr[:, 2] - tr[:, 0]) / 1e3:.1f} us, start->Q ready "
       f"{np.median(tr[:, 1] - tr[:, 0]) / 1e3:.2f} us")
 T = (tr.shape[1] - 8) // 12
