@@ -80,19 +80,14 @@ enum Variant { kGLA, kMLA, kGTA };
 
 int g_tile_override = 0;  // debug: force 64 / 96 / 128-token tiles (glad_debug_set_tile)
 
-// KV tile height.  Shared memory holds NS stages of T tokens next to the
-// query block; the refill of a stage waits for the PV of the tile it held,
-// so with two stages the pipeline is latency-bound.  Prefer
-// the tallest tile that gives three stages, else the tallest with two.
-int tile_tokens(const glad::DecodeKey& k0) {
+// KV tile height.  128 is the default: 96-token tiles (three GLA-2 stages)
+// and 64-token tiles (four) shorten the refill chain but spend more QK tensor
+// work and per-tile softmax overhead per token, and measured no faster on any
+// BASELINE shape (C2 0.300 / 0.287 ms at T = 96 / 128, C5 equal, MLA 0.62 /
+// 0.61 ms at T = 64 / 128).  The others stay available (and tested) through
+// glad_debug_set_tile.
+int tile_tokens(const glad::DecodeKey&) {
   if (g_tile_override == 64 || g_tile_override == 96 || g_tile_override == 128) return g_tile_override;
-  glad::DecodeKey k = k0;
-  for (int want : {3, 2}) {
-    for (int t : {128, 96, 64}) {
-      k.t = t;
-      if (glad::decode_stages(k) >= want) return t;
-    }
-  }
   return 128;
 }
 

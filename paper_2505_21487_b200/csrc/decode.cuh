@@ -412,6 +412,17 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
     if (p.q_tma) tma_prefetch_desc(&qmap);
   }
   if (warp == 2) { tmem_alloc(tmem_slot, C::TMEM_COLS); tmem_relinquish(); }
+  if (warp == 3) {
+    // While warp 0 searches the plan: touch the block table, Q and the plan
+    // so this SM's address translations are warm when the producer and the
+    // Q loader start (their first accesses otherwise pay TLB misses, all
+    // 148 SMs at once: measured ~5 us before the first KV load).
+    if (lane == 0) prefetch_l2(p.block_table);
+    if (lane == 1) prefetch_l2(p.q);
+    if (lane == 2) prefetch_l2(p.seqlens);
+    if (lane == 3) prefetch_l2(p.o_part);
+    if (lane == 4) prefetch_l2(p.out);
+  }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -524,9 +535,6 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
     named_bar_sync(3, 96);  // the first Q load is issued first: QK needs Q, not a second tile
     if (trace && lane == 0) trace[4] = globaltimer();
     const int box_rows = p.box_rows;
-    // Issue the TMA boxes of tile `tl` of segment `s`: into smem (prefetch =
-    // false, completing on kv_full[stage]) or as an L2 prefetch.  Boxes are
-    // spread over the 32 lanes; one int32 block-table lookup per box.
     // Two boxes per page run of a tile: item 2*box = the latent slice (4-D
     // map, all NCH_V chunks in one box), item 2*box + 1 = the RoPE chunk
     // (2-D map).  Issued into smem (completing on kv_full[stage]) or as an
@@ -569,6 +577,7 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
     };
     pf_advance();
     for (int i = 0; i < NS && pvalid; ++i) pf_advance();
+    if (trace && lane == 0) trace[kTraceStride - 6] = globaltimer();  // debug: prefetch cursor ready
     int k = 0, u = 0, it = 0;
     Seg s;
     while (next_seg(k, u, s)) {
@@ -582,7 +591,10 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
         // the page lookup of this lane's first item is done before the stage
         // wait: after the release only the TMA issue remains on the critical path
         const int row0 = lane < nitem ? item_row(bt_row, p0, lane >> 1) : 0;
-        if (trace && lane == 0 && it == 0) trace[6] = globaltimer();
+        if (trace && lane == 0 && it == 0) {
+          if (row0 == 0x7fffffff) __nanosleep(1);  // debug: wait for the lookup itself
+          trace[6] = globaltimer();
+        }
         mbar_wait(&kv_empty[stage], ((it / NS) & 1) ^ 1);
         if (trace && lane == 0 && it < kTraceTiles) trace[13 + 12 * it] = globaltimer();
         if (lane == 0) mbar_arrive_expect_tx(&kv_full[stage], static_cast<uint32_t>(nbox * box_rows * C::NCH * 128));

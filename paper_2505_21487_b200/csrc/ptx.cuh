@@ -366,6 +366,9 @@ __device__ __forceinline__ uint32_t max_u16x2(uint32_t a, uint32_t b) {
 }
 
 // --------------------------------------------------------------- misc
+__device__ __forceinline__ void prefetch_l2(const void* ptr) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(ptr));
+}
 __device__ __forceinline__ uint64_t globaltimer() {
   uint64_t t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t) : : "memory");  // not hoisted across barriers

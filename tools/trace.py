@@ -95,6 +95,7 @@ print(f"  per CTA: steady QK->QK sum {np.nanmedian(np.nansum(st, 1)) / 1e3:.1f} 
       f"gaps (mean {np.nanmean(st):.0f} ns), switch gaps sum {np.nanmedian(np.nansum(sw, 1)) / 1e3:.1f} us "
       f"(mean {np.nanmean(sw):.0f} ns)")
 print(f"  start->first QK {np.median(tr[:, 1] - tr[:, 0]) / 1e3:.1f} us, last QK->end {np.median(tr[:, 2] - np.nanmax(np.where(valid, qk, np.nan), 1)) / 1e3:.1f} us")
+print(f"  producer: prefetch cursor ready {np.median(tr[:, -6] - tr[:, 0]) / 1e3:.2f} us after start")
 print(f"  start (us): Q issued {np.median(tr[:, 5] - tr[:, 0]) / 1e3:.2f}, producer past Q barrier "
       f"{np.median(tr[:, 4] - tr[:, 0]) / 1e3:.2f}, first row looked up {np.median(tr[:, 6] - tr[:, 0]) / 1e3:.2f}, "
       f"first load issued {np.median(tile[:, 0, 0] - tr[:, 0]) / 1e3:.2f}")
