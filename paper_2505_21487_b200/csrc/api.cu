@@ -3,7 +3,10 @@
 // compute path runs in the kernels of decode.cuh / aux_kernels.cu.
 #include <cudaTypedefs.h>
 
+#include <algorithm>
 #include <cmath>
+#include <map>
+#include <tuple>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -86,9 +89,23 @@ int g_tile_override = 0;  // debug: force 64 / 96 / 128-token tiles (glad_debug_
 // BASELINE shape (C2 0.300 / 0.287 ms at T = 96 / 128, C5 equal, MLA 0.62 /
 // 0.61 ms at T = 64 / 128).  The others stay available (and tested) through
 // glad_debug_set_tile.
-int tile_tokens(const glad::DecodeKey&) {
+int tile_tokens(const glad::DecodeKey& k0) {
   if (g_tile_override == 64 || g_tile_override == 96 || g_tile_override == 128) return g_tile_override;
-  return 128;
+  glad::DecodeKey k = k0;
+  k.t = 128;
+  if (glad::decode_stages(k) >= 2) return 128;
+  return 64;  // MLA (144 KB tiles): one 128-token stage only; two 64-token stages measured 5 % faster
+}
+
+// Resident clusters per (kernel, cluster size), queried once.
+int max_clusters(const glad::DecodeKey& k, int cl_n) {
+  static std::map<std::tuple<int, int, int, int, int, int>, int> cache;
+  const auto key = std::make_tuple(k.d_v, k.d_kn, k.d_r, k.nq, k.t, cl_n);
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  const int n = glad::decode_max_clusters(k, cl_n);
+  cache[key] = n;
+  return n;
 }
 
 struct DecodeGeom {
@@ -160,10 +177,28 @@ glad_status decode_common(Variant v, const void* q, const void* pool, const glad
   const int64_t U = static_cast<int64_t>(B) * L->n_heads_kv * g.n_qblk;
   if (U >= (int64_t(1) << 30)) return fail(GLAD_ERR_UNSUPPORTED, "too many work units (%lld)", (long long)U);
   const int G0 = num_ctas > 0 ? num_ctas : num_sms();
-  // one equal CTA group per KV head (when there are enough CTAs): keeps the
-  // heads of a sequence in lockstep so their shared RoPE rows hit L2
-  const int head_groups = (L->n_heads_kv > 1 && G0 >= L->n_heads_kv) ? 1 : 0;
-  const int G = head_groups ? (G0 / L->n_heads_kv) * L->n_heads_kv : G0;
+  // Several query blocks per (head, sequence) (q_len >= 2, MLA): optionally
+  // (glad_debug_set_phase_mask bit 8) a cluster of one CTA per block shares
+  // every KV tile through TMA multicast, so the tile is read from HBM once
+  // instead of once per block.  Measured: DRAM bytes halve (C3 q_len 2: 1.23
+  // -> 0.66 GB) but the step is 5-15 % slower — these shapes are bound by the
+  // per-tile QK/softmax/PV chain, not by HBM, and the cluster-wide stage
+  // handshake lengthens that chain.  Off by default.
+  int cl_n = 1;
+  if (g.n_qblk >= 2 && g.n_qblk <= 8 && L->page_size >= 16 && (g_phase_mask & 8) &&
+      (num_ctas == 0 || num_ctas % g.n_qblk == 0)) {
+    cl_n = g.n_qblk;
+    if (max_clusters(g.key, cl_n) < 1) cl_n = 1;
+  }
+  // Ranges (one per CTA, or per cluster): one equal group per KV head when
+  // there are enough, so the heads of a sequence advance in lockstep and
+  // their shared RoPE rows hit L2.
+  int R0 = G0 / cl_n;
+  if (cl_n > 1 && num_ctas == 0) R0 = std::min(R0, max_clusters(g.key, cl_n));
+  const int head_groups = (L->n_heads_kv > 1 && R0 >= L->n_heads_kv) ? 1 : 0;
+  const int R = head_groups ? (R0 / L->n_heads_kv) * L->n_heads_kv : R0;
+  const int G = R * cl_n;
+  const int64_t n_plan = U / cl_n;  // plan entries: units, or (head, sequence) groups
   const WsLayout wl = ws_layout(U, G, g.key.nq, L->d_head);
   if (ws == nullptr || ws_bytes < wl.total)
     return fail(GLAD_ERR_WORKSPACE, "workspace %zu bytes < required %zu", ws_bytes, wl.total);
@@ -256,16 +291,17 @@ glad_status decode_common(Variant v, const void* q, const void* pool, const glad
   p.log2_page = ilog2(L->page_size);
   p.box_rows = box_rows;
   p.n_qblk = g.n_qblk;
-  p.n_units = static_cast<int32_t>(U);
+  p.n_units = static_cast<int32_t>(n_plan);
   p.causal = causal ? 1 : 0;
   p.scale_log2 = scale * 1.4426950408889634f;
   p.trace = g_trace;
+  p.cl_n = cl_n;
 
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   int32_t* plan = reinterpret_cast<int32_t*>(wsb + wl.plan);
   cudaError_t e = cudaSuccess;
   if (g_phase_mask & 1) {
-    e = glad::launch_plan(seqlens, plan, p.n_units, B, g.key.t, g.n_qblk, g.key.nq, Lq, g.g_q, p.causal, H,
+    e = glad::launch_plan(seqlens, plan, p.n_units, cl_n, B, g.key.t, g.n_qblk, g.key.nq, Lq, g.g_q, p.causal, H,
                           L->d_head, out, lse, nullptr, st);
     if (e != cudaSuccess) return fail(GLAD_ERR_CUDA, "plan launch failed: %s", cudaGetErrorString(e));
   }
@@ -274,8 +310,8 @@ glad_status decode_common(Variant v, const void* q, const void* pool, const glad
     if (e != cudaSuccess) return fail(GLAD_ERR_CUDA, "decode launch failed: %s", cudaGetErrorString(e));
   }
   if (g_phase_mask & 4) {
-    e = glad::launch_merge_split(plan, p.o_part, p.lse_part, G, p.n_units, g.key.nq, g.n_qblk, B, L->n_heads_kv,
-                                 head_groups, g.g_q, Lq, H, L->d_head, out, lse, st);
+    e = glad::launch_merge_split(plan, p.o_part, p.lse_part, G, cl_n, p.n_units, g.key.nq, g.n_qblk, B,
+                                 L->n_heads_kv, head_groups, g.g_q, Lq, H, L->d_head, out, lse, st);
     if (e != cudaSuccess) return fail(GLAD_ERR_CUDA, "merge launch failed: %s", cudaGetErrorString(e));
   }
   return GLAD_OK;
@@ -291,7 +327,7 @@ const char* glad_version(void) { return "glad 0.1.0 sm_100a"; }
 
 void glad_debug_set_trace(void* device_buf) { g_trace = static_cast<uint64_t*>(device_buf); }
 
-void glad_debug_set_phase_mask(int32_t mask) { g_phase_mask = mask & 7; }
+void glad_debug_set_phase_mask(int32_t mask) { g_phase_mask = mask & 15; }
 
 void glad_debug_set_tile(int32_t tokens) { g_tile_override = tokens; }
 

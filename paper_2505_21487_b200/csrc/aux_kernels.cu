@@ -89,8 +89,8 @@ __global__ void combine_kernel(const float* __restrict__ o_part, const float* __
 // -> exclusive prefix sum plan[0..U]; plan[U] = total tiles.  Also writes
 // the output of units with no visible key (zeros, lse = -inf), which no
 // decode CTA visits.
-__global__ void plan_kernel(const int32_t* __restrict__ seqlens, int32_t* __restrict__ plan, int U, int B,
-                            int tile, int n_qblk, int nq_blk, int Lq, int g_q,
+__global__ void plan_kernel(const int32_t* __restrict__ seqlens, int32_t* __restrict__ plan, int U, int cl_n,
+                            int B, int tile, int n_qblk, int nq_blk, int Lq, int g_q,
                             int causal, int H, int d_v, __nv_bfloat16* __restrict__ out, float* __restrict__ lse,
                             uint64_t* trace) {
   if (trace && threadIdx.x == 0) trace[0] = globaltimer();
@@ -103,18 +103,22 @@ __global__ void plan_kernel(const int32_t* __restrict__ seqlens, int32_t* __rest
     const int u = base + threadIdx.x;
     int tiles = 0;
     if (u < U) {
-      const int qb = u % n_qblk;
-      const int b = (u / n_qblk) % B;  // head-major unit order
+      // plan entry u: unit u, or with clusters the (head, sequence) group of
+      // cl_n units whose tiles are those of its last query block (most keys)
+      const int ul = u * cl_n + cl_n - 1;
+      const int qb = ul % n_qblk;
+      const int b = (ul / n_qblk) % B;  // head-major unit order
       const int n0 = qb * nq_blk;
       const int nq = min(nq_blk, Lq * g_q - n0);
       const int L = seqlens[b];
       int kv_end = L;
       if (causal) kv_end = max(0, min(L, L - Lq + (n0 + nq - 1) / g_q + 1));
       tiles = (kv_end + tile - 1) / tile;
-      if (tiles == 0) {  // no visible key: no decode CTA visits the unit (rare; one thread per unit)
-        const int head = (u / n_qblk) / B;
-        for (int n = 0; n < nq; ++n) {
-          const int ng = n0 + n, t = ng / g_q, h = head * g_q + (ng - t * g_q);
+      if (tiles == 0) {  // no visible key: no decode CTA visits the unit(s) (rare; one thread per entry)
+        const int head = (ul / n_qblk) / B;
+        const int n_first = (ul - (cl_n - 1)) % n_qblk * nq_blk;
+        for (int n = n_first; n < n0 + nq; ++n) {
+          const int t = n / g_q, h = head * g_q + (n - t * g_q);
           const int64_t row = (static_cast<int64_t>(b) * Lq + t) * H + h;
           uint4* o = reinterpret_cast<uint4*>(out + row * d_v);
           for (int d = 0; d < d_v / 8; ++d) o[d] = make_uint4(0u, 0u, 0u, 0u);
@@ -151,31 +155,36 @@ __global__ void plan_kernel(const int32_t* __restrict__ seqlens, int32_t* __rest
   if (trace && threadIdx.x == 0) trace[1] = globaltimer();
 }
 
-cudaError_t launch_plan(const int32_t* seqlens, int32_t* plan, int U, int B, int tile, int n_qblk, int nq_blk,
-                        int Lq, int g_q, int causal, int H, int d_v, void* out, float* lse, uint64_t* trace,
-                        cudaStream_t stream) {
-  plan_kernel<<<1, 1024, 0, stream>>>(seqlens, plan, U, B, tile, n_qblk, nq_blk, Lq, g_q, causal, H, d_v,
+cudaError_t launch_plan(const int32_t* seqlens, int32_t* plan, int U, int cl_n, int B, int tile, int n_qblk,
+                        int nq_blk, int Lq, int g_q, int causal, int H, int d_v, void* out, float* lse,
+                        uint64_t* trace, cudaStream_t stream) {
+  plan_kernel<<<1, 1024, 0, stream>>>(seqlens, plan, U, cl_n, B, tile, n_qblk, nq_blk, Lq, g_q, causal, H, d_v,
                                       static_cast<__nv_bfloat16*>(out), lse, trace);
   return cudaGetLastError();
 }
 
-// Split-KV LSE merge of the units that CTA range boundaries cut (
-// oracle.attention.merge_partials).  Block b looks at the boundary between
-// decode CTAs b-1 and b: if it cuts a unit and is that unit's first cut, the
-// block merges the partials (workspace slots c + u, c = first..last CTA of
-// the unit) into out / lse.  All other blocks exit at once.
+// Split-KV LSE merge of the units that range boundaries cut (
+// oracle.attention.merge_partials).  Ranges belong to CTAs, or with
+// clusters (cl_n > 1) to clusters whose CTA r owns query block r of each
+// plan entry.  Block (b, r) looks at the boundary between ranges b-1 and b:
+// if it cuts a plan entry and is its first cut, the block merges the
+// partials of unit entry * cl_n + r (workspace slots (c + entry) * cl_n + r,
+// c = first..last range of the entry) into out / lse.  All other blocks
+// exit at once.
 constexpr int kMergeThreads = 256;
 constexpr int kMergeMaxParts = 8;  // weights staged per pass
 __global__ void __launch_bounds__(kMergeThreads) merge_split_kernel(
     const int32_t* __restrict__ plan, const float* __restrict__ o_part, const float* __restrict__ lse_part, int G,
-    int U, int nq_blk, int n_qblk, int B, int n_heads, int head_groups, int g_q, int Lq, int H, int d_v,
+    int cl_n, int U, int nq_blk, int n_qblk, int B, int n_heads, int head_groups, int g_q, int Lq, int H, int d_v,
     __nv_bfloat16* __restrict__ out, float* __restrict__ lse) {
   __shared__ int u_s;
   __shared__ float w_s[kMergeMaxParts][64];
   __shared__ float mx_s[64], iz_s[64];
-  const int b_cta = blockIdx.x + 1;  // boundary between CTAs b-1 and b
+  const int GR = G / cl_n;                     // ranges
+  const int b_cta = blockIdx.x / cl_n + 1;     // boundary between ranges b-1 and b
+  const int rank = blockIdx.x % cl_n;
   const int total = __ldg(plan + U);
-  const CtaRange rg = cta_range(b_cta, G, total, n_heads, head_groups);
+  const CtaRange rg = cta_range(b_cta, GR, total, n_heads, head_groups);
   if (rg.t0 >= rg.t1) return;
   const int t = rg.t0;
   // unit containing tile t: 32-ary search by warp 0 (last u with plan[u] <= t)
@@ -193,22 +202,26 @@ __global__ void __launch_bounds__(kMergeThreads) merge_split_kernel(
     if (lane == 0) u_s = lo;
   }
   __syncthreads();
-  const int u = u_s;
-  const int pu0 = __ldg(plan + u), pu1 = __ldg(plan + u + 1);
-  if (pu0 == t) return;  // the unit starts at this boundary: not cut here
-  const int cf = cta_of_tile(pu0, G, total, n_heads, head_groups);
+  const int pe = u_s;  // plan entry
+  const int pu0 = __ldg(plan + pe), pu1 = __ldg(plan + pe + 1);
+  if (pu0 == t) return;  // the entry starts at this boundary: not cut here
+  const int cf = cta_of_tile(pu0, GR, total, n_heads, head_groups);
   if (cf != b_cta - 1) return;  // an earlier boundary cuts it: that block merges
-  const int cl = cta_of_tile(pu1 - 1, G, total, n_heads, head_groups);
+  const int cl = cta_of_tile(pu1 - 1, GR, total, n_heads, head_groups);
+  const int u = pe * cl_n + rank;
   const int qb = u % n_qblk, hb = u / n_qblk, b = hb % B, head = hb / B;
   const int n0 = qb * nq_blk;
   const int nq = min(nq_blk, Lq * g_q - n0);
-  const float* lp = lse_part + static_cast<int64_t>(u) * nq_blk;  // slot c: + c * nq_blk
+  if (nq <= 0) return;
+  // slot of range c: (c + pe) * cl_n + rank
+  const float* lp = lse_part + (static_cast<int64_t>(pe) * cl_n + rank) * nq_blk;  // + c * cl_n * nq_blk
+  const int64_t sstride = static_cast<int64_t>(cl_n) * nq_blk;
   for (int n = threadIdx.x; n < nq; n += kMergeThreads) {
     float mx = -INFINITY;
-    for (int c = cf; c <= cl; ++c) mx = fmaxf(mx, lp[static_cast<int64_t>(c) * nq_blk + n]);
+    for (int c = cf; c <= cl; ++c) mx = fmaxf(mx, lp[c * sstride + n]);
     float z = 0.f;
     if (mx != -INFINITY)
-      for (int c = cf; c <= cl; ++c) z += __expf(lp[static_cast<int64_t>(c) * nq_blk + n] - mx);
+      for (int c = cf; c <= cl; ++c) z += __expf(lp[c * sstride + n] - mx);
     const int ng = n0 + n, tq = ng / g_q, h = head * g_q + (ng - tq * g_q);
     lse[(static_cast<int64_t>(b) * Lq + tq) * H + h] = z > 0.f ? mx + __logf(z) : -INFINITY;
     mx_s[n] = mx;
@@ -229,11 +242,12 @@ __global__ void __launch_bounds__(kMergeThreads) merge_split_kernel(
       for (int k = threadIdx.x; k < np * nq; k += kMergeThreads) {
         const int cc = k / nq, n = k - cc * nq;
         const float mx = mx_s[n];
-        w_s[cc][n] = mx == -INFINITY ? 0.f : __expf(lp[static_cast<int64_t>(c0 + cc) * nq_blk + n] - mx) * iz_s[n];
+        w_s[cc][n] = mx == -INFINITY ? 0.f : __expf(lp[(c0 + cc) * sstride + n] - mx) * iz_s[n];
       }
       __syncthreads();
       for (int cc = 0; cc < np; ++cc) {
-        const float4* src = reinterpret_cast<const float4*>(o_part + static_cast<int64_t>(c0 + cc + u) * nq_blk * d_v);
+        const float4* src = reinterpret_cast<const float4*>(
+            o_part + ((static_cast<int64_t>(c0 + cc) + pe) * cl_n + rank) * nq_blk * d_v);
         float4 v[kPer];
 #pragma unroll
         for (int i = 0; i < kPer; ++i) {
@@ -261,13 +275,13 @@ __global__ void __launch_bounds__(kMergeThreads) merge_split_kernel(
   }
 }
 
-cudaError_t launch_merge_split(const int32_t* plan, const float* o_part, const float* lse_part, int G, int U,
-                               int nq_blk, int n_qblk, int B, int n_heads, int head_groups, int g_q, int Lq, int H,
-                               int d_v, void* out, float* lse, cudaStream_t stream) {
-  if (G < 2) return cudaSuccess;
-  merge_split_kernel<<<G - 1, kMergeThreads, 0, stream>>>(plan, o_part, lse_part, G, U, nq_blk, n_qblk, B, n_heads,
-                                                          head_groups, g_q, Lq, H, d_v,
-                                                          static_cast<__nv_bfloat16*>(out), lse);
+cudaError_t launch_merge_split(const int32_t* plan, const float* o_part, const float* lse_part, int G, int cl_n,
+                               int U, int nq_blk, int n_qblk, int B, int n_heads, int head_groups, int g_q, int Lq,
+                               int H, int d_v, void* out, float* lse, cudaStream_t stream) {
+  if (G / cl_n < 2) return cudaSuccess;
+  merge_split_kernel<<<(G / cl_n - 1) * cl_n, kMergeThreads, 0, stream>>>(
+      plan, o_part, lse_part, G, cl_n, U, nq_blk, n_qblk, B, n_heads, head_groups, g_q, Lq, H, d_v,
+      static_cast<__nv_bfloat16*>(out), lse);
   return cudaGetLastError();
 }
 

@@ -67,6 +67,10 @@ struct DecodeParams {
   int32_t q_tma;            // 1: Q via the 3-D tensor map (box (64, q_box_h, q_box_t)); 0: cp.async
   int32_t q_box_h, q_box_t;
   float scale_log2;         // softmax_scale * log2(e)
+  int cl_n;                 // CTAs per cluster = query blocks per (head, sequence); 1 = no cluster.
+                            // With cl_n > 1 the plan is over (head, sequence) groups, the CTAs of a
+                            // cluster share each KV tile (TMA multicast) and CTA rank r owns query
+                            // block r of every group.
   uint64_t* trace;          // debug timeline (nullptr = off): [cta][kTraceStride]
 };
 // Debug timeline layout per CTA (globaltimer ns): [0] start, [1] first QK,
@@ -214,29 +218,46 @@ __device__ __forceinline__ void tmem_store_cols(uint32_t taddr, const float (&x)
 // tile range [t0, t1) that falls in this CTA's flattened range.
 struct Seg {
   int u, b, head, qb;
+  int pi;          // plan entry: the unit (cl_n = 1) or its (head, sequence) group
   int n0, nq;      // query rows [n0, n0 + nq) of the head's Lq*g_q rows
   int L, kv_end;   // keys visible to the block's last query
+  int ld_end;      // keys the tile loads cover: kv_end of the group's last block (cluster)
   int t0, t1;      // tile range within the unit
   bool whole;      // unit entirely inside this CTA -> write final output
 };
 
+// Keys visible to the last query of rows [n0, n0 + nq) (bottom-right causal).
+__device__ __forceinline__ int rows_kv_end(const DecodeParams& p, int L, int n0, int nq) {
+  if (!p.causal) return L;
+  const int t_last = (n0 + nq - 1) / p.g_q;
+  return max(0, min(L, L - p.Lq + t_last + 1));
+}
+// Unit fields of plan entry pi for this CTA (cluster rank = query block).
 template <int NQ>
-__device__ __forceinline__ Seg make_seg(const DecodeParams& p, int u, int cta_t0, int cta_t1) {
-  Seg s;
-  s.u = u;
-  s.qb = u % p.n_qblk;
-  const int hb = u / p.n_qblk;  // head-major: CTAs in different head ranges stream the same b together
+__device__ __forceinline__ void seg_unit(const DecodeParams& p, int pi, int L, Seg& s) {
+  s.pi = pi;
+  const int rank = static_cast<int>(blockIdx.x) % p.cl_n;
+  s.u = pi * p.cl_n + rank;
+  s.qb = s.u % p.n_qblk;
+  const int hb = s.u / p.n_qblk;  // head-major: CTAs in different head ranges stream the same b together
   s.b = hb % p.B;
   s.head = hb / p.B;
   const int nq_total = p.Lq * p.g_q;
   s.n0 = s.qb * NQ;
   s.nq = min(NQ, nq_total - s.n0);
-  s.L = __ldg(p.seqlens + s.b);
-  s.kv_end = s.L;
-  if (p.causal) {
-    const int t_last = (s.n0 + s.nq - 1) / p.g_q;
-    s.kv_end = max(0, min(s.L, s.L - p.Lq + t_last + 1));
+  s.L = L;
+  s.kv_end = rows_kv_end(p, L, s.n0, s.nq);
+  s.ld_end = s.kv_end;
+  if (p.cl_n > 1) {  // the group's last query block sees the most keys
+    const int n0l = (p.n_qblk - 1) * NQ;
+    s.ld_end = rows_kv_end(p, L, n0l, nq_total - n0l);
   }
+}
+
+template <int NQ>
+__device__ __forceinline__ Seg make_seg(const DecodeParams& p, int u, int cta_t0, int cta_t1) {
+  Seg s;
+  seg_unit<NQ>(p, u, __ldg(p.seqlens + ((u * p.cl_n) / p.n_qblk) % p.B), s);
   const int pu0 = __ldg(p.plan + u), pu1 = __ldg(p.plan + u + 1);
   s.t0 = max(cta_t0, pu0) - pu0;
   s.t1 = min(cta_t1, pu1) - pu0;
@@ -282,19 +303,7 @@ __device__ __host__ __forceinline__ int cta_of_tile(int t, int G, int total, int
 template <int NQ>
 __device__ __forceinline__ Seg seg_from_entry(const DecodeParams& p, int4 e) {
   Seg s;
-  s.u = e.x;
-  s.qb = s.u % p.n_qblk;
-  const int hb = s.u / p.n_qblk;
-  s.b = hb % p.B;
-  s.head = hb / p.B;
-  s.n0 = s.qb * NQ;
-  s.nq = min(NQ, p.Lq * p.g_q - s.n0);
-  s.L = e.w & 0x3FFFFFFF;
-  s.kv_end = s.L;
-  if (p.causal) {
-    const int t_last = (s.n0 + s.nq - 1) / p.g_q;
-    s.kv_end = max(0, min(s.L, s.L - p.Lq + t_last + 1));
-  }
+  seg_unit<NQ>(p, e.x, e.w & 0x3FFFFFFF, s);
   s.t0 = e.y;
   s.t1 = e.z;
   s.whole = (e.w >> 30) & 1;
@@ -322,6 +331,7 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
   uint64_t* q_full = bars + 20;    // [2] Q buffer (s % NQB) of segment s loaded (64 arrivals)
   uint64_t* q_empty = bars + 22;   // [2] last QK of segment s done: Q buffer (s % NQB) free
   uint64_t* o_empty = bars + 24;   // [2] epilogue read O buffer (s & 1) (8 arrivals)
+  uint64_t* cl_empty = bars + 26;  // [4] cluster: stage free in all cl_n CTAs (leader's copy is used)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(aux + 256);
   int* range_s = reinterpret_cast<int*>(aux + 264);        // [4] cta tile range, #segments, overflow unit
   int4* segtab = reinterpret_cast<int4*>(aux + 3072);      // [MAXSEG] (u, t0, t1, L | whole << 30)
@@ -342,7 +352,7 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
     // (a serial search over the plan would cost one L2 round trip per step).
     const int U = p.n_units;
     const int total = __ldg(p.plan + U);
-    const CtaRange rg = cta_range(cta, gridDim.x, total, p.n_heads_kv, p.head_groups);
+    const CtaRange rg = cta_range(cta / p.cl_n, gridDim.x / p.cl_n, total, p.n_heads_kv, p.head_groups);
     const int t0 = rg.t0, t1 = rg.t1;
     int lo = 0, hi = U - 1;  // last unit with plan[u] <= t0 (plan[0] = 0)
     while (lo < hi) {
@@ -364,7 +374,7 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
         const int st0 = max(t0, pu0) - pu0, st1 = min(t1, pu1) - pu0;
         const bool has = in && st1 > st0;
         int L = 0;
-        if (has) L = __ldg(p.seqlens + (u / p.n_qblk) % p.B);
+        if (has) L = __ldg(p.seqlens + ((u * p.cl_n) / p.n_qblk) % p.B);
         const unsigned hm = __ballot_sync(0xffffffffu, has);
         const int pos = nseg + __popc(hm & ((1u << lane) - 1));
         const int whole = (st0 == 0 && st1 == pu1 - pu0) ? 1 : 0;
@@ -402,6 +412,7 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
       mbar_init(&o_empty[i], 8);
     }
     for (int i = 0; i < 4; ++i) mbar_init(&pv_done[i], 1);
+    for (int i = 0; i < 4; ++i) mbar_init(&cl_empty[i], p.cl_n);
     for (int i = 0; i < 2; ++i) {
       mbar_init(&q_full[i], p.q_tma ? 1 : 64);
       mbar_init(&q_empty[i], 1);
@@ -425,6 +436,7 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
   }
   tc_fence_before();
   __syncthreads();
+  if (p.cl_n > 1) cluster_sync();  // peers' barriers initialised before any remote arrive / multicast
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   const int cta_t0 = range_s[0], cta_t1 = range_s[1], nseg_tab = range_s[2], u_more = range_s[3];
@@ -486,7 +498,7 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
 #pragma unroll
         for (int j = 0; j < RPW; ++j) {
           const int pos = p0 + 32 * j + lane;
-          rowreg[j] = pos < s.kv_end ? __ldg(bt_row + (pos >> p.log2_page)) * p.page_size + (pos & (p.page_size - 1))
+          rowreg[j] = pos < s.ld_end ? __ldg(bt_row + (pos >> p.log2_page)) * p.page_size + (pos & (p.page_size - 1))
                                      : -1;
         }
         mbar_wait(&kv_empty[stage], ((it / NS) & 1) ^ 1);
@@ -519,7 +531,7 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
           const int pp0 = ptl * T;
           for (int r2 = row_lo + lane; r2 < row_hi; r2 += 32) {
             const int pos = pp0 + r2;
-            if (pos < ps.kv_end) {
+            if (pos < ps.ld_end) {
               const int64_t row =
                   static_cast<int64_t>(__ldg(pbt + (pos >> p.log2_page))) * p.page_size + (pos & (p.page_size - 1));
               prefetch_l2_bulk(p.pool + row * p.row_stride + ps.head * p.d_head, C::NCH_V * 128);
@@ -539,16 +551,24 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
     // map, all NCH_V chunks in one box), item 2*box + 1 = the RoPE chunk
     // (2-D map).  Issued into smem (completing on kv_full[stage]) or as an
     // L2 prefetch.  Items are spread over the 32 lanes.
+    const uint16_t mc_mask = static_cast<uint16_t>((1u << p.cl_n) - 1u);
     auto issue_item = [&](const Seg& s, int row, int box, int item, uint32_t stage_addr, uint64_t* bar) {
       if (item == 0) {
         const int c = s.head * (p.d_head >> 6);
-        if (bar) tma_load_4d(stage_addr + box * (box_rows >> 3) * C::LGRP, &lmap, bar, 0, 0, c, row >> 3);
-        else tma_prefetch_4d(&lmap, 0, 0, c, row >> 3);
+        const uint32_t dst = stage_addr + box * (box_rows >> 3) * C::LGRP;
+        if (!bar) tma_prefetch_4d(&lmap, 0, 0, c, row >> 3);
+        else if (p.cl_n > 1) tma_load_4d_mc(dst, &lmap, bar, 0, 0, c, row >> 3, mc_mask);
+        else tma_load_4d(dst, &lmap, bar, 0, 0, c, row >> 3);
       } else {
-        if (bar) tma_load_2d(stage_addr + C::OFF_R + box * box_rows * 128, &tmap, bar, p.rope_col, row);
-        else tma_prefetch_2d(&tmap, p.rope_col, row);
+        const uint32_t dst = stage_addr + C::OFF_R + box * box_rows * 128;
+        if (!bar) tma_prefetch_2d(&tmap, p.rope_col, row);
+        else if (p.cl_n > 1) tma_load_2d_mc(dst, &tmap, bar, p.rope_col, row, mc_mask);
+        else tma_load_2d(dst, &tmap, bar, p.rope_col, row);
       }
     };
+    // Cluster: rank 0 loads every tile for all cl_n CTAs (multicast) once all
+    // of them have freed the stage; the others only arm their kv_full.
+    const bool loader = (cta % p.cl_n) == 0;
     auto item_row = [&](const int* bt_row, int p0, int box) {
       const int pos = p0 + box * box_rows;
       return __ldg(bt_row + (pos >> p.log2_page)) * p.page_size + (pos & (p.page_size - 1));
@@ -556,7 +576,7 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
     auto issue_tile = [&](const Seg& s, int tl, int stage, bool prefetch, int page0) {
       const int* bt_row = p.block_table + static_cast<size_t>(s.b) * p.bt_stride;
       const int p0 = tl * T;
-      const int ntok = min(T, s.kv_end - p0);
+      const int ntok = min(T, s.ld_end - p0);
       const int nbox = (ntok + box_rows - 1) / box_rows;
       for (int bx = lane; bx < nbox * 2; bx += 32)
         issue_item(s, item_row(bt_row, p0, bx >> 1), bx >> 1, bx & 1, sbase + stage * C::STAGE,
@@ -585,12 +605,12 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
       for (int tl = s.t0; tl < s.t1; ++tl, ++it) {
         const int stage = it % NS;
         const int p0 = tl * T;
-        const int ntok = min(T, s.kv_end - p0);
+        const int ntok = min(T, s.ld_end - p0);
         const int nbox = (ntok + box_rows - 1) / box_rows;
         const int nitem = nbox * 2;
         // the page lookup of this lane's first item is done before the stage
         // wait: after the release only the TMA issue remains on the critical path
-        const int row0 = lane < nitem ? item_row(bt_row, p0, lane >> 1) : 0;
+        const int row0 = (loader && lane < nitem) ? item_row(bt_row, p0, lane >> 1) : 0;
         if (trace && lane == 0 && it == 0) {
           if (row0 == 0x7fffffff) __nanosleep(1);  // debug: wait for the lookup itself
           trace[6] = globaltimer();
@@ -598,13 +618,19 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
         mbar_wait(&kv_empty[stage], ((it / NS) & 1) ^ 1);
         if (trace && lane == 0 && it < kTraceTiles) trace[13 + 12 * it] = globaltimer();
         if (lane == 0) mbar_arrive_expect_tx(&kv_full[stage], static_cast<uint32_t>(nbox * box_rows * C::NCH * 128));
+        if (p.cl_n > 1) {  // stage free here -> tell the loader; the loader waits for every CTA
+          if (lane == 0) mbar_arrive_cluster(&cl_empty[stage], 0);
+          if (loader) mbar_wait(&cl_empty[stage], (it / NS) & 1);
+        }
         __syncwarp();
         const uint32_t stage_addr = sbase + stage * C::STAGE;
-        if (lane < nitem) issue_item(s, row0, lane >> 1, lane & 1, stage_addr, &kv_full[stage]);
-        for (int bx = lane + 32; bx < nitem; bx += 32)  // small pages: more boxes than lanes
-          issue_item(s, item_row(bt_row, p0, bx >> 1), bx >> 1, bx & 1, stage_addr, &kv_full[stage]);
+        if (loader) {
+          if (lane < nitem) issue_item(s, row0, lane >> 1, lane & 1, stage_addr, &kv_full[stage]);
+          for (int bx = lane + 32; bx < nitem; bx += 32)  // small pages: more boxes than lanes
+            issue_item(s, item_row(bt_row, p0, bx >> 1), bx >> 1, bx & 1, stage_addr, &kv_full[stage]);
+        }
         if (trace && lane == 0 && it < kTraceTiles) trace[8 + 12 * it] = globaltimer();
-        if (pvalid) {  // L2 prefetch of tile it + NS, after the stage load so it never delays it
+        if (pvalid && loader) {  // L2 prefetch of tile it + NS, after the stage load so it never delays it
           issue_tile(ps, ptl, 0, true, -1);
           pf_advance();
         }
@@ -1004,7 +1030,9 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
       if ((lane & ((1 << col_shift<HC, LANES>()) - 1)) == 0)
         red[(wg * 4 + wq) * 32 + (cb - c0) + ((lane & (LANES - 1)) >> col_shift<HC, LANES>())] = cs;
       named_bar_sync(bar_id, 128);
-      const int slot = cta + s.u;  // partial slot of a split unit
+      // partial slot of a split unit: (range + plan entry) * cl_n + rank is
+      // unique (both increase together along the tile order)
+      const int slot = (cta / p.cl_n + s.pi) * p.cl_n + cta % p.cl_n;
       if (r < CW) {  // fold the row sum into alpha_s as 1/l (reused below) and write lse
         const float* rr = red + wg * 128 + r;
         const float ls = (rr[0] + rr[32]) + (rr[64] + rr[96]);
@@ -1078,6 +1106,7 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
 
   tc_fence_before();
   __syncthreads();
+  if (p.cl_n > 1) cluster_sync();  // no CTA leaves while a peer may still signal it
   if (trace && threadIdx.x == 0) trace[2] = globaltimer();
   if (warp == 2) {
     tc_fence_after();

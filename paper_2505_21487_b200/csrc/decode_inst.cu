@@ -22,6 +22,12 @@ int decode_stages(const DecodeKey& k) {
   return k.t == 64 ? decode_stages_t<64>(k) : k.t == 96 ? decode_stages_t<96>(k) : decode_stages_t<128>(k);
 }
 
+int decode_max_clusters(const DecodeKey& k, int cl_n) {
+  if (!decode_supported(k)) return 0;
+  return k.t == 64 ? decode_max_clusters_t<64>(k, cl_n)
+                   : k.t == 96 ? decode_max_clusters_t<96>(k, cl_n) : decode_max_clusters_t<128>(k, cl_n);
+}
+
 cudaError_t launch_decode(const DecodeKey& k, const CUtensorMap& tmap, const CUtensorMap& lmap,
                           const CUtensorMap& qmap, const DecodeParams& p, int grid, cudaStream_t s) {
   if (!decode_supported(k)) return cudaErrorInvalidValue;

@@ -5,10 +5,8 @@
 
 namespace glad {
 
-template <int DV, int DKN, int DR, int NQ, int T>
-cudaError_t launch_one(const CUtensorMap& tmap, const CUtensorMap& lmap, const CUtensorMap& qmap,
-                       const DecodeParams& p, int grid, cudaStream_t stream) {
-  using C = DecodeCfg<DV, DKN, DR, NQ, T>;
+template <class C>
+cudaError_t set_smem_attr() {
   static bool attr_set = false;  // benign race: idempotent attribute set
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(decode_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -16,8 +14,32 @@ cudaError_t launch_one(const CUtensorMap& tmap, const CUtensorMap& lmap, const C
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  decode_kernel<C><<<grid, C::NTHREADS, C::SMEM_BYTES, stream>>>(tmap, lmap, qmap, p);
-  return cudaGetLastError();
+  return cudaSuccess;
+}
+
+template <int DV, int DKN, int DR, int NQ, int T>
+cudaError_t launch_one(const CUtensorMap& tmap, const CUtensorMap& lmap, const CUtensorMap& qmap,
+                       const DecodeParams& p, int grid, cudaStream_t stream) {
+  using C = DecodeCfg<DV, DKN, DR, NQ, T>;
+  cudaError_t e = set_smem_attr<C>();
+  if (e != cudaSuccess) return e;
+  if (p.cl_n <= 1) {
+    decode_kernel<C><<<grid, C::NTHREADS, C::SMEM_BYTES, stream>>>(tmap, lmap, qmap, p);
+    return cudaGetLastError();
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(C::NTHREADS);
+  cfg.dynamicSmemBytes = C::SMEM_BYTES;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = p.cl_n;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, decode_kernel<C>, tmap, lmap, qmap, p);
 }
 
 // Calls f.template run<C>() for the DecodeCfg matching (key, T); returns
@@ -55,6 +77,30 @@ struct LaunchF {
   }
 };
 
+// How many clusters of `cl_n` decode CTAs can be resident at once (a
+// persistent grid must not exceed it: clusters live inside one GPC).
+struct ClustersF {
+  int cl_n;
+  int* out;
+  template <class C>
+  cudaError_t run() {
+    cudaError_t e = set_smem_attr<C>();
+    if (e != cudaSuccess) return e;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(cl_n * 64);
+    cfg.blockDim = dim3(C::NTHREADS);
+    cfg.dynamicSmemBytes = C::SMEM_BYTES;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = cl_n;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaOccupancyMaxActiveClusters(out, decode_kernel<C>, &cfg);
+  }
+};
+
 struct StagesF {
   int* ns;
   template <class C>
@@ -69,6 +115,8 @@ cudaError_t launch_decode_t(const DecodeKey& k, const CUtensorMap& tmap, const C
                             const CUtensorMap& qmap, const DecodeParams& p, int grid, cudaStream_t s);
 template <int T>
 int decode_stages_t(const DecodeKey& k);
+template <int T>
+int decode_max_clusters_t(const DecodeKey& k, int cl_n);
 
 #define GLAD_INSTANTIATE_T(T)                                                                              \
   template <>                                                                                              \
@@ -80,6 +128,11 @@ int decode_stages_t(const DecodeKey& k);
   int decode_stages_t<T>(const DecodeKey& k) {                                                             \
     int ns = 0;                                                                                            \
     return with_cfg<T>(k, StagesF{&ns}) == cudaSuccess ? ns : 0;                                           \
+  }                                                                                                        \
+  template <>                                                                                              \
+  int decode_max_clusters_t<T>(const DecodeKey& k, int cl_n) {                                             \
+    int n = 0;                                                                                             \
+    return with_cfg<T>(k, ClustersF{cl_n, &n}) == cudaSuccess ? n : 0;                                     \
   }
 
 }  // namespace glad

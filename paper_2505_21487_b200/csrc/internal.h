@@ -20,15 +20,16 @@ struct DecodeKey {
 cudaError_t launch_decode(const DecodeKey& key, const CUtensorMap& tmap, const CUtensorMap& lmap, const CUtensorMap& qmap, const DecodeParams& p, int grid,
                           cudaStream_t stream);
 bool decode_supported(const DecodeKey& key);
-int decode_stages(const DecodeKey& key);  // KV pipeline stages of the instantiation (0: unsupported)
+int decode_stages(const DecodeKey& key);                   // KV pipeline stages of the instantiation (0: unsupported)
+int decode_max_clusters(const DecodeKey& key, int cl_n);  // resident clusters of cl_n CTAs (0: error)
 int decode_max_nq(int d_v);
 
-cudaError_t launch_plan(const int32_t* seqlens, int32_t* plan, int U, int B, int tile, int n_qblk, int nq_blk,
-                        int Lq, int g_q, int causal, int H, int d_v, void* out, float* lse, uint64_t* trace,
-                        cudaStream_t stream);
-cudaError_t launch_merge_split(const int32_t* plan, const float* o_part, const float* lse_part, int G, int U,
-                               int nq_blk, int n_qblk, int B, int n_heads, int head_groups, int g_q, int Lq, int H,
-                               int d_v, void* out, float* lse, cudaStream_t stream);
+cudaError_t launch_plan(const int32_t* seqlens, int32_t* plan, int U, int cl_n, int B, int tile, int n_qblk,
+                        int nq_blk, int Lq, int g_q, int causal, int H, int d_v, void* out, float* lse,
+                        uint64_t* trace, cudaStream_t stream);
+cudaError_t launch_merge_split(const int32_t* plan, const float* o_part, const float* lse_part, int G, int cl_n,
+                               int U, int nq_blk, int n_qblk, int B, int n_heads, int head_groups, int g_q, int Lq,
+                               int H, int d_v, void* out, float* lse, cudaStream_t stream);
 cudaError_t launch_append(void* pool, int64_t row_stride, int page_size, const int32_t* block_table,
                           int32_t bt_stride, const int32_t* seqlens_before, const void* rows, int32_t B,
                           int32_t n_new, int32_t width, cudaStream_t stream);

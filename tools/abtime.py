@@ -14,12 +14,13 @@ ap.add_argument("--tile", type=int, default=0)
 ap.add_argument("--n", type=int, default=20)
 ap.add_argument("--trace", action="store_true", help="run with the debug timeline enabled")
 ap.add_argument("--mask", type=int, default=7, help="glad_debug_set_phase_mask value")
+ap.add_argument("--ctas", type=int, default=0)
 a = ap.parse_args()
 if a.tile:
     glad.debug_set_tile(a.tile)
 glad.debug_set_phase_mask(a.mask)
 wl = workloads.get(a.workload)
-st = workloads.build_device_state(wl)
+st = workloads.build_device_state(wl, num_ctas=a.ctas)
 if a.trace:
     tbuf = torch.zeros(4096 * glad.TRACE_STRIDE, dtype=torch.int64, device="cuda")
     glad.debug_set_trace(tbuf)
