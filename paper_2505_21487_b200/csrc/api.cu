@@ -90,8 +90,16 @@ int g_tile_override = 0;  // debug: force 64 / 96 / 128-token tiles (glad_debug_
 // 0.61 ms at T = 64 / 128).  The others stay available (and tested) through
 // glad_debug_set_tile.
 int tile_tokens(const glad::DecodeKey& k0) {
+  if (k0.nq == 128 && g_tile_override == 128) return 96;  // rows mode has no 128-token tiles
   if (g_tile_override == 64 || g_tile_override == 96 || g_tile_override == 128) return g_tile_override;
   glad::DecodeKey k = k0;
+  if (k.nq == 128) {  // rows mode: the largest tile that leaves three KV stages next to the 128-row Q
+    for (int t : {96, 64}) {
+      k.t = t;
+      if (glad::decode_stages(k) >= 3) return t;
+    }
+    return 64;
+  }
   k.t = 128;
   if (glad::decode_stages(k) >= 2) return 128;
   return 64;  // MLA (144 KB tiles): one 128-token stage only; two 64-token stages measured 5 % faster
@@ -131,6 +139,12 @@ glad_status decode_geom(Variant v, const glad_cache_layout* L, int32_t Lq, int32
   const int64_t nq_total = static_cast<int64_t>(Lq) * g->g_q;
   const int maxnq = glad::decode_max_nq(L->d_head);
   g->key.nq = nq_total <= 16 ? 16 : nq_total <= 32 ? 32 : maxnq;
+  // More than 64 query rows per head (q_len >= 2 with g_q = 64):
+  // rows mode, one CTA per 128 rows reads each KV tile once for all of them
+  // (glad_debug_set_phase_mask bit 16 turns it off for A/B runs).
+  glad::DecodeKey kr = g->key;
+  kr.nq = 128;
+  if (nq_total > 64 && !(g_phase_mask & 16) && glad::decode_rows_supported(kr)) g->key.nq = 128;
   g->key.t = tile_tokens(g->key);
   g->n_qblk = static_cast<int>((nq_total + g->key.nq - 1) / g->key.nq);
   if (!glad::decode_supported(g->key))
@@ -327,7 +341,7 @@ const char* glad_version(void) { return "glad 0.1.0 sm_100a"; }
 
 void glad_debug_set_trace(void* device_buf) { g_trace = static_cast<uint64_t*>(device_buf); }
 
-void glad_debug_set_phase_mask(int32_t mask) { g_phase_mask = mask & 15; }
+void glad_debug_set_phase_mask(int32_t mask) { g_phase_mask = mask & 31; }
 
 void glad_debug_set_tile(int32_t tokens) { g_tile_override = tokens; }
 

@@ -178,8 +178,8 @@ __global__ void __launch_bounds__(kMergeThreads) merge_split_kernel(
     int cl_n, int U, int nq_blk, int n_qblk, int B, int n_heads, int head_groups, int g_q, int Lq, int H, int d_v,
     __nv_bfloat16* __restrict__ out, float* __restrict__ lse) {
   __shared__ int u_s;
-  __shared__ float w_s[kMergeMaxParts][64];
-  __shared__ float mx_s[64], iz_s[64];
+  __shared__ float w_s[kMergeMaxParts][128];  // nq_blk <= 128 (rows mode)
+  __shared__ float mx_s[128], iz_s[128];
   const int GR = G / cl_n;                     // ranges
   const int b_cta = blockIdx.x / cl_n + 1;     // boundary between ranges b-1 and b
   const int rank = blockIdx.x % cl_n;

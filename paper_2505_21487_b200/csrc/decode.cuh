@@ -91,11 +91,18 @@ struct DecodeCfg {
   static constexpr int D_V = D_V_;    // value width (= state width)
   static constexpr int D_KN = D_KN_;  // key part taken from the state
   static constexpr int D_R = D_R_;    // rope width
-  static constexpr int NQ = NQ_;      // query rows per unit (UMMA N)
-  // tokens per tile (64 / 96 / 128).  The QK UMMA always has M = 128: with
-  // T < 128 its rows >= T read whatever follows the tile in shared memory and
-  // are discarded by the softmax (a fraction of QK tensor work traded for a
-  // third / fourth KV stage).
+  static constexpr int NQ = NQ_;      // query rows per unit (UMMA N; UMMA M in rows mode)
+  // Rows mode (NQ = 128): query rows on UMMA M, tokens on N (S = Q K^T,
+  // O = P V with P kept in TMEM as the A operand of a "TS" MMA).  One CTA
+  // then serves 128 query rows of a head (q_len >= 2 speculative decode,
+  // P:278) from one read of each KV tile, and a QK MMA reads a 128-row A and
+  // a T-row B from shared memory (balanced against the smem operand
+  // bandwidth, instead of 6 KB per 32 tensor cycles at N = 64).
+  static constexpr bool ROWS = (NQ_ == 128);
+  // tokens per tile (64 / 96 / 128).  Swap-AB: the QK UMMA always has
+  // M = 128: with T < 128 its rows >= T read whatever follows the tile in
+  // shared memory and are discarded by the softmax (a fraction of QK tensor
+  // work traded for a third / fourth KV stage).  Rows: N = T.
   static constexpr int T = T_;
   static constexpr int LANES = 32;  // token lanes per warp quarter in S^T
   static constexpr int DQ = D_KN + D_R;
@@ -116,17 +123,18 @@ struct DecodeCfg {
   // P^T (bf16, [NQ/8][128 tok][8]) lives in the stage's RoPE chunk, which is
   // dead once QK of that tile has completed: P is thereby multi-buffered with
   // the KV stages at zero extra shared memory.
-  static constexpr int PBYTES = T * NQ * 2;
+  // (Rows mode: P lives in TMEM.)
+  static constexpr int PBYTES = ROWS ? 0 : T * NQ * 2;
   static constexpr bool P_SW128 = (NQ == 64);  // MN-major SW128 P^T: PV MMA 70 vs 81 cycles (microbench)
   static constexpr int NBLK_O = D_V / 128;
   static constexpr int NWG = 2;
-  static constexpr int CW = NQ / NWG;
+  static constexpr int CW = ROWS ? 32 : NQ / NWG;
   static constexpr int HC = CW;  // columns per softmax thread (one token row)
   static constexpr int MAXSEG = 128;  // per-CTA segment table entries (aux + 3072)
-  static constexpr int AUX = 3072 + MAXSEG * 16 + T * 4;  // + row table of the cp.async producer
+  static constexpr int AUX = 3072 + MAXSEG * 16 + T * 4 + (ROWS ? 1024 : 0);  // + cp.async row table (+ rows: row-sum exchange)
   static constexpr int AVAIL = 227 * 1024 - 1024 - AUX;
   // bytes the M = 128 QK may read past the end of the last stage (rows >= T)
-  static constexpr int OVER_RAW = (16 * LGRP > OFF_R + 16384 ? 16 * LGRP : OFF_R + 16384) - STAGE;
+  static constexpr int OVER_RAW = ROWS ? 0 : (16 * LGRP > OFF_R + 16384 ? 16 * LGRP : OFF_R + 16384) - STAGE;
   static constexpr int XTRA = OVER_RAW - QBYTES - AUX > 0 ? OVER_RAW - QBYTES - AUX : 0;
   static constexpr int NS_RAW = (AVAIL - QBYTES - XTRA) / STAGE;
   static constexpr int NS = NS_RAW > 4 ? 4 : NS_RAW;
@@ -136,12 +144,17 @@ struct DecodeCfg {
   static constexpr int OFF_Q = NS * STAGE;
   static constexpr int OFF_AUX = OFF_Q + NQB * QBYTES;
   static constexpr int SMEM_BYTES = 1024 + OFF_AUX + AUX + XTRA;
-  static constexpr int OCOLS = NBLK_O * NQ;      // one O^T accumulator
-  static constexpr int TMEM_O = 2 * NQ;          // after the two S^T buffers
+  // TMEM columns.  Swap-AB: two S^T buffers [128 tok x NQ], then O^T [128 d
+  // lanes x NBLK_O*NQ].  Rows mode: two S buffers [128 rows x T] (a tile's
+  // bf16 P is written over the upper half of its S buffer), then O [128 rows
+  // x D_V].
+  static constexpr int SCOLS = ROWS ? T : NQ;             // one S buffer
+  static constexpr int OCOLS = ROWS ? D_V : NBLK_O * NQ;  // one O accumulator
+  static constexpr int TMEM_O = 2 * SCOLS;                // after the two S buffers
   // two O buffers (the next unit's first PV overlaps this unit's epilogue)
-  // when TMEM allows, else one (MLA d_c = 512 with 64 rows)
-  static constexpr int NOB = (2 * NQ + 2 * OCOLS <= 512) ? 2 : 1;
-  static constexpr int TMEM_USED = 2 * NQ + NOB * OCOLS;
+  // when TMEM allows, else one (MLA d_c = 512 with 64 rows; rows mode d_c = 256)
+  static constexpr int NOB = (2 * SCOLS + 2 * OCOLS <= 512) ? 2 : 1;
+  static constexpr int TMEM_USED = 2 * SCOLS + NOB * OCOLS;
   static constexpr int TMEM_COLS =
       TMEM_USED <= 32 ? 32 : TMEM_USED <= 64 ? 64 : TMEM_USED <= 128 ? 128 : TMEM_USED <= 256 ? 256 : 512;
   static constexpr int NTHREADS = 384;
@@ -149,7 +162,8 @@ struct DecodeCfg {
   static_assert(PBYTES <= CHUNK, "P^T must fit in the RoPE chunk");
   static_assert(D_V % 128 == 0 && D_KN % 64 == 0 && D_KN <= D_V, "unsupported head dims");
   static_assert(D_R % 16 == 0 && D_R >= 16 && D_R <= 64, "unsupported rope dim");
-  static_assert(NQ == 16 || NQ == 32 || NQ == 64, "NQ must be 16/32/64");
+  static_assert(NQ == 16 || NQ == 32 || NQ == 64 || NQ == 128, "NQ must be 16/32/64/128");
+  static_assert(!ROWS || D_V <= 256, "rows mode: O [128 x D_V] needs D_V <= 256 (one UMMA N)");
   static_assert(TMEM_USED <= 512, "TMEM budget");
   static_assert(QCHUNK % 1024 == 0, "Q chunk alignment");
   static_assert(T == 128 || T == 96 || T == 64, "tile height");
@@ -404,7 +418,7 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
     for (int i = 0; i < NS; ++i) {
       mbar_init(&kv_full[i], p.cp_kv ? (p.q_tma ? 64 : 32) : 1);
       mbar_init(&kv_empty[i], 1);
-      mbar_init(&p_full[i], 8);
+      mbar_init(&p_full[i], 8);  // softmax warps
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&s_full[i], 1);
@@ -642,7 +656,96 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
     // barrier probe and cursor value is made uniform with a vote / REDUX), so
     // descriptors live in uniform registers and each tcgen05.mma costs a
     // couple of uniform adds to issue.
-    {
+    if constexpr (C::ROWS) {
+      // Rows mode: S[128 rows x T] = Q . K_tile^T (A = Q, B = the KV tile,
+      // both K-major SW128 as TMA wrote them); O[128 x D_V] += P . V (A = the
+      // bf16 P the softmax wrote into the upper half of S's TMEM buffer,
+      // B = the same KV tile read MN-major).  S buffer sb is reused by
+      // QK(i + 2) only after PV(i) (which reads P from it) has completed.
+      constexpr uint32_t idesc_qk = make_idesc_bf16(128, T, false, false);
+      constexpr uint32_t idesc_pv = make_idesc_bf16(128, C::D_V, false, true);
+      const uint32_t tm = static_cast<uint32_t>(warp_uniform(static_cast<int>(tmem)));
+      struct Cursor {
+        int k, u, seg, tl, t1, t0;
+      };
+      Cursor cq{0, 0, -1, 0, 0, 0}, cp{0, 0, -1, 0, 0, 0};
+      auto advance = [&](Cursor& c) -> bool {
+        if (c.seg >= 0 && c.tl + 1 < c.t1) { ++c.tl; return true; }
+        Seg s;
+        const bool ok = warp_uniform(next_seg(c.k, c.u, s));
+        if (!ok) return false;
+        c.k = warp_uniform(c.k);
+        c.u = warp_uniform(c.u);
+        ++c.seg;
+        c.tl = c.t0 = warp_uniform(s.t0);
+        c.t1 = warp_uniform(s.t1);
+        return true;
+      };
+      auto probe = [&](uint64_t* bar, int parity) { return warp_uniform(mbar_test_wait(smem_u32(bar), parity)); };
+      bool qk_left = advance(cq), pv_left = advance(cp);
+      int next_qk = 0, next_pv = 0;
+      long long t0 = clock64();
+      while (pv_left) {
+        bool did = false;
+        if (next_pv < next_qk && probe(&p_full[next_pv & 1], (next_pv >> 1) & 1)) {
+          const bool first = (cp.tl == cp.t0);
+          if (!first || cp.seg < C::NOB || probe(&o_empty[cp.seg % C::NOB], ((cp.seg - C::NOB) / C::NOB) & 1)) {
+            tc_fence_after();
+            const int j = next_pv;
+            const int stage = j % NS;
+            const uint64_t bd = desc_mnmajor_sw128(sbase + stage * C::STAGE, 1024, C::LGRP);
+            const uint32_t obuf = tm + C::TMEM_O + (cp.seg % C::NOB) * C::OCOLS;
+            const uint32_t pa = tm + (j & 1) * C::SCOLS + T / 2;
+#pragma unroll
+            for (int k = 0; k < T / 16; ++k)
+              umma_f16_ts_warp(obuf, pa + k * 8, bd + static_cast<uint64_t>((k * 2 * C::LGRP) >> 4), idesc_pv,
+                               (!first || k > 0) ? 1u : 0u);
+            umma_commit_warp(&kv_empty[stage]);
+            umma_commit_warp(&pv_done[j & 3]);
+            ++next_pv;
+            pv_left = advance(cp);
+            did = true;
+          }
+        }
+        if (qk_left && next_qk - next_pv <= 1 && probe(&kv_full[next_qk % NS], (next_qk / NS) & 1) &&
+            (next_qk < 2 || probe(&pv_done[(next_qk - 2) & 3], ((next_qk - 2) >> 2) & 1))) {
+          const bool first = (cq.tl == cq.t0);
+          if (!first || probe(&q_full[cq.seg % C::NQB], (cq.seg / C::NQB) & 1)) {
+            if (trace && lane == 0 && next_qk == 0) trace[1] = globaltimer();
+            tc_fence_after();
+            if (p.cp_kv) fence_proxy_async_smem();
+            const int stage = next_qk % NS;
+            const uint32_t d = tm + (next_qk & 1) * C::SCOLS;
+            const uint64_t qd = desc_kmajor_sw128(sbase + C::OFF_Q + (cq.seg % C::NQB) * C::QBYTES);
+            const uint64_t kd = desc_kmajor_sw128(sbase + stage * C::STAGE, C::LGRP);
+            const uint64_t rd = desc_kmajor_sw128(sbase + stage * C::STAGE + C::OFF_R);
+#pragma unroll
+            for (int c = 0; c < C::NCH_QK; ++c) {
+#pragma unroll
+              for (int k = 0; k < 4; ++k)
+                umma_f16_ss_warp(d, qd + static_cast<uint64_t>((c * C::QCHUNK + k * 32) >> 4),
+                                 kd + static_cast<uint64_t>((c * 1024 + k * 32) >> 4), idesc_qk, (c | k) != 0);
+            }
+#pragma unroll
+            for (int k = 0; k < C::RK; ++k)
+              umma_f16_ss_warp(d, qd + static_cast<uint64_t>((C::NCH_QK * C::QCHUNK + k * 32) >> 4),
+                               rd + static_cast<uint64_t>((k * 32) >> 4), idesc_qk, 1u);
+            umma_commit_warp(&s_full[next_qk & 1]);
+            if (cq.tl + 1 == cq.t1) umma_commit_warp(&q_empty[cq.seg % C::NQB]);
+            ++next_qk;
+            qk_left = advance(cq);
+            did = true;
+          }
+        }
+        if (did) {
+          t0 = clock64();
+        } else if (warp_uniform(clock64() - t0 > (1ll << 34))) {
+          if (lane == 0) printf("glad: MMA scheduler watchdog (rows, cta %d qk %d pv %d)\n", cta, next_qk, next_pv);
+          __trap();
+        }
+      }
+      if (trace && lane == 0) trace[3] = cp.seg + 1;
+    } else {
       constexpr uint32_t idesc_qk = make_idesc_bf16(128, NQ, false, false);
       constexpr uint32_t idesc_pv = make_idesc_bf16(128, NQ, true, true);
       const uint32_t tm = static_cast<uint32_t>(warp_uniform(static_cast<int>(tmem)));
@@ -814,6 +917,170 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
       ++seg;
     }
     if (seg == 0) named_bar_arrive(3, 96);  // no work: release the producer
+  } else if constexpr (C::ROWS) {
+    // ============ rows mode: softmax / correction / epilogue (two warpgroups) ============
+    // Thread = query row n = TMEM lane (32 wq + lane) of S and O.  Warpgroup
+    // wg owns S columns [wg T/2, (wg+1) T/2) of every tile and O columns
+    // [wg D_V/2, (wg+1) D_V/2).  Warps 4 + wq and 8 + wq hold the same rows:
+    // they keep identical copies of the row's running max (both compute it
+    // from the same exchanged values), vote the lazy rescale together
+    // (bar.red.or over the pair, barrier 4 + wq) and each keeps a partial
+    // row sum, combined in the epilogue.
+    constexpr int TH = T / 2;            // S columns per thread
+    constexpr int NP = TH / 2;           // bf16 pairs of them (TMEM columns of P)
+    constexpr int DH = C::D_V / 2;       // O columns per thread
+    constexpr uint32_t kTrig = 0x4380u;  // bf16 bits of 2^TAU = 256
+    static_assert(TAU == 8.f, "kTrig encodes 2^TAU");
+    static_assert(TH % 16 == 0 && NP % 8 == 0 && DH % 32 == 0, "rows mode tile split");
+    const int wg = (warp - 4) >> 2;
+    const int wq = warp & 3;
+    const int n = wq * 32 + lane;
+    const uint32_t lane_addr = static_cast<uint32_t>(wq * 32) << 16;
+    const uint32_t pair_bar = 4 + wq;
+    float* mx_x = red;                                                   // [2 wg][128] partial row max
+    float* l_x = reinterpret_cast<float*>(aux + 3072 + C::MAXSEG * 16 + T * 4);  // [2 wg][128] partial row sums
+    const float sl2 = p.scale_log2;
+    int k = 0, u = 0, seg = 0, it = 0;
+    Seg s;
+    while (next_seg(k, u, s)) {
+      int vend = 0, t_row = 0, h_row = 0;
+      if (n < s.nq) {
+        const int ng = s.n0 + n;
+        t_row = ng / p.g_q;
+        h_row = s.head * p.g_q + (ng - t_row * p.g_q);
+        vend = p.causal ? max(0, min(s.L, s.L - p.Lq + t_row + 1)) : s.L;
+      }
+      float m = -INFINITY, nm = 0.f;  // running max (log2 units), -m (0 while m = -inf)
+      float2 l2 = make_float2(0.f, 0.f);
+      const uint32_t obuf = tmem + lane_addr + C::TMEM_O + (seg % C::NOB) * C::OCOLS + wg * DH;
+      for (int tl = s.t0; tl < s.t1; ++tl, ++it) {
+        const int sb = it & 1;
+        const uint32_t sbuf = tmem + lane_addr + sb * C::SCOLS;
+        mbar_wait(&s_full[sb], (it >> 1) & 1);
+        tc_fence_after();
+        const int c0 = tl * T + wg * TH;  // first token of this thread's columns
+        float x[TH];
+#pragma unroll
+        for (int c = 0; c < TH; c += 16) tmem_ld16(sbuf + wg * TH + c, x + c);
+        tmem_ld_wait();
+        if (c0 + TH > vend) {
+#pragma unroll
+          for (int j = 0; j < TH; ++j) x[j] = (c0 + j < vend) ? x[j] : -INFINITY;
+        }
+        uint32_t pk[NP];
+        auto exp_pack = [&]() {
+#pragma unroll
+          for (int j = 0; j < TH; j += 2) {
+            const float2 e = ffma2(make_float2(x[j], x[j + 1]), make_float2(sl2, sl2), make_float2(nm, nm));
+            pk[j / 2] = pack_bf16x2(ex2(e.x), ex2(e.y));
+          }
+        };
+        exp_pack();
+        uint32_t pmax = pk[0];
+#pragma unroll
+        for (int j = 1; j < NP; ++j) pmax = max_u16x2(pmax, pk[j]);
+        const bool need = (tl == s.t0) || ((pmax & 0xffffu) > kTrig) || ((pmax >> 16) > kTrig);
+        if (named_bar_red_or(pair_bar, 64, need)) {
+          float mt = x[0];
+#pragma unroll
+          for (int j = 1; j < TH; ++j) mt = fmaxf(mt, x[j]);
+          mx_x[wg * 128 + n] = mt;
+          named_bar_sync(pair_bar, 64);
+          mt = fmaxf(mt, mx_x[(wg ^ 1) * 128 + n]);
+          const float mn = fmaxf(m, mt * sl2);
+          const float alpha = (mn == -INFINITY) ? 1.f : ex2(m - mn);
+          m = mn;
+          nm = (mn == -INFINITY) ? 0.f : -mn;
+          l2.x *= alpha;
+          l2.y *= alpha;
+          if (tl > s.t0 && __any_sync(0xffffffffu, alpha != 1.f)) {  // rescale this thread's O half-row
+            const int j = it - 1;
+            mbar_wait(&pv_done[j & 3], (j >> 2) & 1);
+            tc_fence_after();
+#pragma unroll 1
+            for (int c = 0; c < DH; c += 32) {
+              float o[32];
+              tmem_ld32(obuf + c, o);
+              tmem_ld_wait();
+#pragma unroll
+              for (int q = 0; q < 32; ++q) o[q] *= alpha;
+              tmem_st16(obuf + c, o);
+              tmem_st16(obuf + c + 16, o + 16);
+            }
+            tmem_st_wait();
+          }
+          exp_pack();
+        }
+        // row sum of the bf16-rounded p the PV multiplies
+#pragma unroll
+        for (int j = 0; j < NP; ++j)
+          l2 = fadd2(l2, make_float2(__uint_as_float(pk[j] << 16), __uint_as_float(pk[j] & 0xffff0000u)));
+        // bf16 P over the upper half of this tile's S buffer (A of the TS PV)
+#pragma unroll
+        for (int c = 0; c < NP; c += 8) tmem_st8(sbuf + T / 2 + wg * NP + c, reinterpret_cast<const float*>(pk + c));
+        tmem_st_wait();
+        const int p0 = tl * T;
+        if (p0 + T > s.kv_end) {  // never-loaded tile rows: zero V (0 * stale smem != NaN)
+          const uint32_t stage_base = sbase + (it % NS) * C::STAGE;
+          for (int idx = wg * 128 + n; idx < T * C::NCH_V; idx += 256) {
+            const int tr = idx / C::NCH_V, ch = idx - tr * C::NCH_V;
+            if (p0 + tr >= s.kv_end) {
+              const uint32_t a = stage_base + (tr >> 3) * C::LGRP + ch * 1024 + (tr & 7) * 128;
+#pragma unroll
+              for (int uu = 0; uu < 8; ++uu) st_shared_v4(a + uu * 16, 0u, 0u, 0u, 0u);
+            }
+          }
+          fence_proxy_async_smem();
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&p_full[sb]);
+      }
+      // ---- segment epilogue: O / l, lse (natural log); each WG writes its O half
+      l_x[wg * 128 + n] = l2.x + l2.y;
+      named_bar_sync(pair_bar, 64);
+      const float ls = l_x[n] + l_x[128 + n];  // same order in both WGs
+      const float inv_l = ls > 0.f ? 1.f / ls : 0.f;
+      const int j = it - 1;
+      mbar_wait(&pv_done[j & 3], (j >> 2) & 1);
+      tc_fence_after();
+      const int slot = (cta / p.cl_n + s.pi) * p.cl_n + cta % p.cl_n;
+      const bool valid = n < s.nq;
+      if (valid && wg == 0) {
+        const float lse = ls > 0.f ? (m + __log2f(ls)) * 0.69314718055994531f : -INFINITY;
+        if (s.whole) p.lse[(static_cast<size_t>(s.b) * p.Lq + t_row) * p.H + h_row] = lse;
+        else p.lse_part[static_cast<size_t>(slot) * NQ + n] = lse;
+      }
+      __nv_bfloat16* orow = p.out + ((static_cast<size_t>(s.b) * p.Lq + t_row) * p.H + h_row) * C::D_V + wg * DH;
+      float* prow = p.o_part + (static_cast<size_t>(slot) * NQ + n) * C::D_V + wg * DH;
+#pragma unroll 1
+      for (int c = 0; c < DH; c += 32) {
+        float o[32];
+        tmem_ld32(obuf + c, o);
+        tmem_ld_wait();
+        if (c + 32 == DH) {  // O consumed: the segment after next may reuse the buffer
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&o_empty[seg % C::NOB]);
+        }
+        if (valid) {
+          if (s.whole) {
+#pragma unroll
+            for (int q = 0; q < 32; q += 8)
+              *reinterpret_cast<uint4*>(orow + c + q) =
+                  make_uint4(pack_bf16x2(o[q] * inv_l, o[q + 1] * inv_l), pack_bf16x2(o[q + 2] * inv_l, o[q + 3] * inv_l),
+                             pack_bf16x2(o[q + 4] * inv_l, o[q + 5] * inv_l), pack_bf16x2(o[q + 6] * inv_l, o[q + 7] * inv_l));
+          } else {
+#pragma unroll
+            for (int q = 0; q < 32; q += 4)
+              *reinterpret_cast<float4*>(prow + c + q) =
+                  make_float4(o[q] * inv_l, o[q + 1] * inv_l, o[q + 2] * inv_l, o[q + 3] * inv_l);
+          }
+        }
+      }
+      named_bar_sync(pair_bar, 64);  // l_x read by both WGs before the next segment rewrites it
+      ++seg;
+    }
   } else {
     // ========================= softmax / correction / epilogue =========================
     // Thread -> data: token row tr = 32*wq + lane of S^T (rows >= T carry no

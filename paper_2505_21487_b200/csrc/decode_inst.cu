@@ -6,9 +6,16 @@ namespace glad {
 
 int decode_max_nq(int) { return 64; }
 
+bool decode_rows_supported(const DecodeKey& k) {
+  return k.d_kn == k.d_v && (k.d_v == 128 || k.d_v == 256) && (k.d_r == 32 || k.d_r == 64);
+}
+
 bool decode_supported(const DecodeKey& k) {
-  if (k.nq != 16 && k.nq != 32 && k.nq != 64) return false;
   if (k.t != 64 && k.t != 96 && k.t != 128) return false;
+  // rows mode: 64- and 96-token tiles (128: S + P + O fill all of TMEM and
+  // the 128-column S row of a thread spills; it faulted on the second tile)
+  if (k.nq == 128) return k.t <= 96 && decode_rows_supported(k);
+  if (k.nq != 16 && k.nq != 32 && k.nq != 64) return false;
   if (k.nq > decode_max_nq(k.d_v)) return false;
   if (k.d_kn == k.d_v) {  // GLA / MLA: key state == value state
     return (k.d_v == 128 && (k.d_r == 32 || k.d_r == 64)) || (k.d_v == 256 && (k.d_r == 32 || k.d_r == 64)) ||

@@ -53,16 +53,28 @@ cudaError_t with_cfg(const DecodeKey& k, F&& f) {
     case 64: return f.template run<DecodeCfg<DV, DKN, DR, 64, T>>();          \
     default: return cudaErrorInvalidValue;                                    \
   }
+  // rows mode (128 query rows per CTA on UMMA M): GLA / MLA with d_c <= 256
+#define GLAD_NQ_R(DV, DR)                                                     \
+  switch (k.nq) {                                                             \
+    case 16: return f.template run<DecodeCfg<DV, DV, DR, 16, T>>();           \
+    case 32: return f.template run<DecodeCfg<DV, DV, DR, 32, T>>();           \
+    case 64: return f.template run<DecodeCfg<DV, DV, DR, 64, T>>();           \
+    case 128:                                                                 \
+      if constexpr (T <= 96) return f.template run<DecodeCfg<DV, DV, DR, 128, T>>(); \
+      else return cudaErrorInvalidValue;                                      \
+    default: return cudaErrorInvalidValue;                                    \
+  }
   if (k.d_kn == k.d_v) {
-    if (k.d_v == 128 && k.d_r == 32) { GLAD_NQ(128, 128, 32) }
-    if (k.d_v == 128 && k.d_r == 64) { GLAD_NQ(128, 128, 64) }
-    if (k.d_v == 256 && k.d_r == 32) { GLAD_NQ(256, 256, 32) }
-    if (k.d_v == 256 && k.d_r == 64) { GLAD_NQ(256, 256, 64) }
+    if (k.d_v == 128 && k.d_r == 32) { GLAD_NQ_R(128, 32) }
+    if (k.d_v == 128 && k.d_r == 64) { GLAD_NQ_R(128, 64) }
+    if (k.d_v == 256 && k.d_r == 32) { GLAD_NQ_R(256, 32) }
+    if (k.d_v == 256 && k.d_r == 64) { GLAD_NQ_R(256, 64) }
     if (k.d_v == 512 && k.d_r == 64) { GLAD_NQ(512, 512, 64) }
   } else if (k.d_v == 128 && k.d_kn == 64 && k.d_r == 64) {
     GLAD_NQ(128, 64, 64)
   }
 #undef GLAD_NQ
+#undef GLAD_NQ_R
   return cudaErrorInvalidValue;
 }
 

@@ -23,6 +23,7 @@ bool decode_supported(const DecodeKey& key);
 int decode_stages(const DecodeKey& key);                   // KV pipeline stages of the instantiation (0: unsupported)
 int decode_max_clusters(const DecodeKey& key, int cl_n);  // resident clusters of cl_n CTAs (0: error)
 int decode_max_nq(int d_v);
+bool decode_rows_supported(const DecodeKey& key);  // rows mode (nq = 128) exists for these dims (any t)
 
 cudaError_t launch_plan(const int32_t* seqlens, int32_t* plan, int U, int cl_n, int B, int tile, int n_qblk,
                         int nq_blk, int Lq, int g_q, int causal, int H, int d_v, void* out, float* lse,

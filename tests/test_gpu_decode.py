@@ -308,3 +308,67 @@ def test_tp_sharded_gla8_emulated(N):
     y_ref = OS.tp_oproj_allreduce(o_ref.reshape(B * Lq, H, d_c), f64(w_vo).reshape(H, d_c, D), N, h_c)
     rel = float(np.linalg.norm(y.numpy() - y_ref) / np.linalg.norm(y_ref))
     assert rel < 5e-3, rel
+
+
+# ------------------------------------------- rows mode (128 query rows / CTA)
+# More than 64 query rows per latent head (speculative q_len >= 2 with
+# g_q = 64): query rows sit on UMMA M, P stays in TMEM.  Each case runs
+# with rows mode on (library default) and off (phase-mask bit 16: the 64-row
+# swap-AB blocks), both against the oracle.
+ROWS_SWEEP = [
+    # B, Lq, H, h_c, d_c, d_R, lens, page, num_ctas, causal, q_scale
+    (2, 2, 128, 2, 256, 64, [1024, 777], 64, 0, True, 1.0),      # C3 shape, q_len 2
+    (3, 2, 128, 2, 256, 64, [1500, 63, 640], 64, 7, True, 1.0),  # ragged, split units
+    (2, 4, 128, 2, 256, 64, [900, 1201], 16, 5, True, 1.0),      # q_len 4: two 128-row blocks
+    (2, 2, 128, 2, 256, 64, [513, 700], 1, 3, True, 1.0),        # page 1 (cp.async producer)
+    (2, 2, 128, 2, 256, 64, [800, 333], 64, 1, False, 1.0),      # non-causal, one CTA
+    (2, 2, 128, 2, 256, 64, [900, 650], 64, 2, True, 4.0),       # peaked: lazy rescale
+    (2, 3, 64, 2, 128, 32, [300, 129], 16, 2, True, 1.0),        # 96 rows: padded block
+    (1, 2, 64, 1, 256, 64, [2000], 128, 0, True, 1.0),           # one latent head (MLA-like, d_c 256)
+    (4, 2, 128, 2, 256, 64, [0, 1, 2, 130], 16, 1, True, 1.0),   # empty / tiny
+]
+
+
+@pytest.fixture(params=[True, False], ids=["rows", "blocks64"])
+def rows_mode(request):
+    glad.debug_set_phase_mask(7 if request.param else 7 | 16)
+    yield request.param
+    glad.debug_set_phase_mask(7)
+
+
+@pytest.mark.parametrize("cfg", ROWS_SWEEP, ids=lambda c: "B{}Lq{}H{}hc{}dc{}p{}s{}c{}q{}".format(
+    c[0], c[1], c[2], c[3], c[4], c[7], c[8], int(c[9]), c[10]))
+def test_rows_mode(cfg, tile, rows_mode):
+    B, Lq, H, h_c, d_c, d_R, lens, page, ctas, causal, qs = cfg
+    out, lse, o_ref, lse_ref = run_latent(B, Lq, H, h_c, d_c, d_R, np.array(lens), page, ctas=ctas,
+                                          causal=causal, seed=40 + ROWS_SWEEP.index(cfg), q_scale=qs)
+    check(out, lse, o_ref, lse_ref, what=f"rows={rows_mode} {cfg}")
+    if min(lens) == 0:
+        assert torch.all(out[0].float() == 0) and torch.all(torch.isneginf(lse[0]))
+        assert torch.all(torch.isneginf(lse[1, 0]))  # causal Lq=2, L=1: the first query sees nothing
+
+
+def test_rows_mode_cta_count_changes_only_rounding():
+    """Rows mode under different persistent grids (different split points)."""
+    sl = np.array([3000, 1234, 77])
+    res = []
+    for ctas in [1, 3, 148, 400]:
+        out, lse, o_ref, lse_ref = run_latent(3, 2, 128, 2, 256, 64, sl, 64, ctas=ctas, seed=61)
+        check(out, lse, o_ref, lse_ref, what=f"rows ctas={ctas}")
+        res.append(out.float())
+    for r in res[1:]:
+        assert float((r - res[0]).abs().max()) < 1e-2
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("name", ["c3_gla2_q2", "c3_gla2_q4"])
+def test_c3_full_size_sampled(name):
+    """BASELINE configs[2] (GLA-2 speculative q_len 2 / 4, B=64, ctx
+    U[2K,16K]) at full size in bench.py's launch configuration (rows mode);
+    sampled (b, latent head) units recomputed by the oracle."""
+    from paper_2505_21487_b200 import workloads
+    wl = workloads.get(name)
+    st = workloads.build_device_state(wl, seed=3)
+    out, lse = workloads.run(wl, st)
+    torch.cuda.synchronize()
+    _sampled_latent_check(wl, st, out, lse, samples=[(0, 0), (21, 1), (63, 0), (63, 1)])
