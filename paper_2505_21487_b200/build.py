@@ -9,6 +9,7 @@ linked into paper_2505_21487_b200/libglad.so.  Rebuilds only what changed
 
 import concurrent.futures as cf
 import glob
+import hashlib
 import os
 import subprocess
 import sys
@@ -16,8 +17,11 @@ import sys
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
-BUILD = os.path.join(ROOT, "build", "glad")
-LIB = os.path.join(PKG, "libglad.so")
+# A/B builds: GLAD_EXTRA_FLAGS (e.g. "-DGLAD_ROWS_QK_CHUNK=32") and GLAD_LIB_OUT
+# (another .so path, loaded with GLAD_LIB=...) build a variant next to the default.
+EXTRA = os.environ.get("GLAD_EXTRA_FLAGS", "").split()
+LIB = os.environ.get("GLAD_LIB_OUT", os.path.join(PKG, "libglad.so"))
+BUILD = os.path.join(ROOT, "build", "glad" if not EXTRA else "glad_" + hashlib.md5(" ".join(EXTRA).encode()).hexdigest()[:8])
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-fvisibility=hidden", "--expt-relaxed-constexpr",
@@ -37,7 +41,7 @@ def _stale(target, deps):
 
 
 def _compile(src, obj, verbose):
-    cmd = [NVCC, *ARCH, *FLAGS, "-c", src, "-o", obj]
+    cmd = [NVCC, *ARCH, *FLAGS, *EXTRA, "-c", src, "-o", obj]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
     r = subprocess.run(cmd, capture_output=True, text=True)

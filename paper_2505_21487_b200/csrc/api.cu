@@ -90,16 +90,19 @@ int g_tile_override = 0;  // debug: force 64 / 96 / 128-token tiles (glad_debug_
 // 0.61 ms at T = 64 / 128).  The others stay available (and tested) through
 // glad_debug_set_tile.
 int tile_tokens(const glad::DecodeKey& k0) {
-  if (k0.nq == 128 && g_tile_override == 128) return 96;  // rows mode has no 128-token tiles
-  if (g_tile_override == 64 || g_tile_override == 96 || g_tile_override == 128) return g_tile_override;
   glad::DecodeKey k = k0;
-  if (k.nq == 128) {  // rows mode: the largest tile that leaves three KV stages next to the 128-row Q
+  if (k.nq == 128) {  // rows mode: no 128-token tiles; the largest tile with three KV stages
+    if (g_tile_override == 64 || g_tile_override == 96 || g_tile_override == 128) {
+      k.t = g_tile_override == 64 ? 64 : 96;
+      if (glad::decode_stages(k) >= 1) return k.t;
+    }
     for (int t : {96, 64}) {
       k.t = t;
       if (glad::decode_stages(k) >= 3) return t;
     }
     return 64;
   }
+  if (g_tile_override == 64 || g_tile_override == 96 || g_tile_override == 128) return g_tile_override;
   k.t = 128;
   if (glad::decode_stages(k) >= 2) return 128;
   return 64;  // MLA (144 KB tiles): one 128-token stage only; two 64-token stages measured 5 % faster

@@ -39,6 +39,8 @@
 #include <cuda.h>
 #include <cuda_bf16.h>
 
+#include <type_traits>
+
 #include "ptx.cuh"
 
 namespace glad {
@@ -80,11 +82,30 @@ struct DecodeParams {
 // [14+8i] P written by the second softmax warpgroup, [15+8i] epilogue done
 // (last tile of a segment only), [16+10i] QK issue returned, [17+10i] PV
 // issue returned (per-tile stride 10).
+#ifndef GLAD_ROWS_QK_CHUNK
+#define GLAD_ROWS_QK_CHUNK 32  // chunked QK issue (4) measured 1.3x slower (0.313 vs 0.236 ms, C3 q_len 2)
+#endif
+#ifndef GLAD_ROWS_QK_AHEAD
+#define GLAD_ROWS_QK_AHEAD 2
+#endif
+#ifndef GLAD_DBG_NO_TS
+#define GLAD_DBG_NO_TS 0
+#endif
+#ifndef GLAD_NS_CAP
+#define GLAD_NS_CAP 4
+#endif
 #ifndef GLAD_MMA_BACKOFF_NS
 #define GLAD_MMA_BACKOFF_NS 0
 #endif
 constexpr int kTraceTiles = 128;
 constexpr int kTraceStride = 8 + 12 * kTraceTiles;
+
+// Rows mode (NQ = 128) fits TMEM: two S buffers [128 x T] + O [128 x D_V] +
+// the query state part [128 x D_V / 2 columns].
+template <int D_V, int T>
+__host__ __device__ constexpr bool rows_fits() {
+  return T <= 96 && 2 * T + D_V + D_V / 2 <= 512;
+}
 
 template <int D_V_, int D_KN_, int D_R_, int NQ_, int T_ = 128>
 struct DecodeCfg {
@@ -119,7 +140,10 @@ struct DecodeCfg {
   static constexpr int LGRP = NCH_V * 1024;  // latent row-group stride
   static constexpr int OFF_R = NCH_V * CHUNK;
   static constexpr int QCHUNK = NQ * 128;
-  static constexpr int QBYTES = NQCH * QCHUNK;
+  // Rows mode keeps the query's state part (D_KN) in TMEM (A of a TS-mode
+  // QK, written by the softmax warps); only its RoPE chunk is staged in
+  // shared memory, which leaves room for four KV stages next to it.
+  static constexpr int QBYTES = ROWS ? QCHUNK : NQCH * QCHUNK;
   // P^T (bf16, [NQ/8][128 tok][8]) lives in the stage's RoPE chunk, which is
   // dead once QK of that tile has completed: P is thereby multi-buffered with
   // the KV stages at zero extra shared memory.
@@ -136,13 +160,19 @@ struct DecodeCfg {
   // bytes the M = 128 QK may read past the end of the last stage (rows >= T)
   static constexpr int OVER_RAW = ROWS ? 0 : (16 * LGRP > OFF_R + 16384 ? 16 * LGRP : OFF_R + 16384) - STAGE;
   static constexpr int XTRA = OVER_RAW - QBYTES - AUX > 0 ? OVER_RAW - QBYTES - AUX : 0;
-  static constexpr int NS_RAW = (AVAIL - QBYTES - XTRA) / STAGE;
-  static constexpr int NS = NS_RAW > 4 ? 4 : NS_RAW;
+  // Rows mode: P (bf16 [128 rows x T]) in two shared-memory buffers, K-major
+  // 128B-swizzled in 64-token chunks (A of an SS PV), so an S buffer is free
+  // as soon as the softmax has read it (QK(i+2) does not wait for PV(i)).
+  static constexpr int PCH = (T + 63) / 64;
+  static constexpr int PBUF = ROWS ? PCH * NQ * 128 : 0;  // one P buffer
+  static constexpr int NS_RAW = (AVAIL - QBYTES - 2 * PBUF - XTRA) / STAGE;
+  static constexpr int NS = NS_RAW > GLAD_NS_CAP ? GLAD_NS_CAP : NS_RAW;
   // a second Q buffer (next unit's Q prefetched while this one runs) when it
   // costs no KV stage
-  static constexpr int NQB = ((AVAIL - 2 * QBYTES - XTRA) / STAGE >= NS) ? 2 : 1;
+  static constexpr int NQB = ((AVAIL - 2 * QBYTES - 2 * PBUF - XTRA) / STAGE >= NS) ? 2 : 1;
   static constexpr int OFF_Q = NS * STAGE;
-  static constexpr int OFF_AUX = OFF_Q + NQB * QBYTES;
+  static constexpr int OFF_P = OFF_Q + NQB * QBYTES;
+  static constexpr int OFF_AUX = OFF_P + 2 * PBUF;
   static constexpr int SMEM_BYTES = 1024 + OFF_AUX + AUX + XTRA;
   // TMEM columns.  Swap-AB: two S^T buffers [128 tok x NQ], then O^T [128 d
   // lanes x NBLK_O*NQ].  Rows mode: two S buffers [128 rows x T] (a tile's
@@ -153,8 +183,10 @@ struct DecodeCfg {
   static constexpr int TMEM_O = 2 * SCOLS;                // after the two S buffers
   // two O buffers (the next unit's first PV overlaps this unit's epilogue)
   // when TMEM allows, else one (MLA d_c = 512 with 64 rows; rows mode d_c = 256)
-  static constexpr int NOB = (2 * SCOLS + 2 * OCOLS <= 512) ? 2 : 1;
-  static constexpr int TMEM_USED = 2 * SCOLS + NOB * OCOLS;
+  static constexpr int QNCOLS = ROWS ? D_KN / 2 : 0;  // rows mode: Q state part, 2 bf16 per column
+  static constexpr int NOB = (2 * SCOLS + 2 * OCOLS + QNCOLS <= 512) ? 2 : 1;
+  static constexpr int QN_COL = 2 * SCOLS + NOB * OCOLS;
+  static constexpr int TMEM_USED = QN_COL + QNCOLS;
   static constexpr int TMEM_COLS =
       TMEM_USED <= 32 ? 32 : TMEM_USED <= 64 ? 64 : TMEM_USED <= 128 ? 128 : TMEM_USED <= 256 ? 256 : 512;
   static constexpr int NTHREADS = 384;
@@ -346,6 +378,7 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
   uint64_t* q_empty = bars + 22;   // [2] last QK of segment s done: Q buffer (s % NQB) free
   uint64_t* o_empty = bars + 24;   // [2] epilogue read O buffer (s & 1) (8 arrivals)
   uint64_t* cl_empty = bars + 26;  // [4] cluster: stage free in all cl_n CTAs (leader's copy is used)
+  uint64_t* qn_full = bars + 30;   // [1] rows mode: Q state part of segment s written to TMEM (8 warps)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(aux + 256);
   int* range_s = reinterpret_cast<int*>(aux + 264);        // [4] cta tile range, #segments, overflow unit
   int4* segtab = reinterpret_cast<int4*>(aux + 3072);      // [MAXSEG] (u, t0, t1, L | whole << 30)
@@ -427,6 +460,7 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
     }
     for (int i = 0; i < 4; ++i) mbar_init(&pv_done[i], 1);
     for (int i = 0; i < 4; ++i) mbar_init(&cl_empty[i], p.cl_n);
+    mbar_init(qn_full, 8);
     for (int i = 0; i < 2; ++i) {
       mbar_init(&q_full[i], p.q_tma ? 1 : 64);
       mbar_init(&q_empty[i], 1);
@@ -684,58 +718,95 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
       auto probe = [&](uint64_t* bar, int parity) { return warp_uniform(mbar_test_wait(smem_u32(bar), parity)); };
       bool qk_left = advance(cq), pv_left = advance(cp);
       int next_qk = 0, next_pv = 0;
+      constexpr int NQK = C::NCH_QK * 4 + C::RK;  // MMAs of one QK
+      constexpr int QK_CHUNK = GLAD_ROWS_QK_CHUNK;
+      int qk_e = 0;                                // MMAs of QK(next_qk) issued so far
       long long t0 = clock64();
       while (pv_left) {
         bool did = false;
         if (next_pv < next_qk && probe(&p_full[next_pv & 1], (next_pv >> 1) & 1)) {
           const bool first = (cp.tl == cp.t0);
           if (!first || cp.seg < C::NOB || probe(&o_empty[cp.seg % C::NOB], ((cp.seg - C::NOB) / C::NOB) & 1)) {
+            if (trace && lane == 0 && next_pv < kTraceTiles) trace[12 + 12 * next_pv] = globaltimer();
             tc_fence_after();
             const int j = next_pv;
             const int stage = j % NS;
             const uint64_t bd = desc_mnmajor_sw128(sbase + stage * C::STAGE, 1024, C::LGRP);
             const uint32_t obuf = tm + C::TMEM_O + (cp.seg % C::NOB) * C::OCOLS;
-            const uint32_t pa = tm + (j & 1) * C::SCOLS + T / 2;
+            const uint64_t pd = desc_kmajor_sw128(sbase + C::OFF_P + (j & 1) * C::PBUF);
 #pragma unroll
             for (int k = 0; k < T / 16; ++k)
-              umma_f16_ts_warp(obuf, pa + k * 8, bd + static_cast<uint64_t>((k * 2 * C::LGRP) >> 4), idesc_pv,
-                               (!first || k > 0) ? 1u : 0u);
+              umma_f16_ss_warp(obuf, pd + static_cast<uint64_t>(((k >> 2) * NQ * 128 + (k & 3) * 32) >> 4),
+                               bd + static_cast<uint64_t>((k * 2 * C::LGRP) >> 4), idesc_pv, (!first || k > 0) ? 1u : 0u);
             umma_commit_warp(&kv_empty[stage]);
             umma_commit_warp(&pv_done[j & 3]);
+            if (trace && lane == 0 && next_pv < kTraceTiles) trace[17 + 12 * next_pv] = globaltimer();
             ++next_pv;
             pv_left = advance(cp);
             did = true;
           }
         }
-        if (qk_left && next_qk - next_pv <= 1 && probe(&kv_full[next_qk % NS], (next_qk / NS) & 1) &&
-            (next_qk < 2 || probe(&pv_done[(next_qk - 2) & 3], ((next_qk - 2) >> 2) & 1))) {
+        // QK is issued in chunks of GLAD_ROWS_QK_CHUNK MMAs, the PV check
+        // running between chunks: an MMA issue blocks until the tensor pipe
+        // takes it, so a whole 20-MMA QK(i+1) issued just before P(i) lands
+        // would hold PV(i) (and with it the stage refill chain) ~0.6 us back.
+        bool qk_go = qk_e > 0;
+        // QK runs up to two tiles ahead of PV: an S buffer is free once the
+        // softmax has read it, so S(i + 2) is ready before softmax(i + 1) ends
+        if (!qk_go && qk_left && next_qk - next_pv <= GLAD_ROWS_QK_AHEAD && probe(&kv_full[next_qk % NS], (next_qk / NS) & 1) &&
+            probe(&s_empty[next_qk & 1], ((next_qk >> 1) & 1) ^ 1)) {
           const bool first = (cq.tl == cq.t0);
-          if (!first || probe(&q_full[cq.seg % C::NQB], (cq.seg / C::NQB) & 1)) {
+          if (!first || (probe(&q_full[cq.seg % C::NQB], (cq.seg / C::NQB) & 1) && probe(qn_full, cq.seg & 1))) {
+            qk_go = true;
             if (trace && lane == 0 && next_qk == 0) trace[1] = globaltimer();
+            if (trace && lane == 0 && next_qk < kTraceTiles) trace[9 + 12 * next_qk] = globaltimer();
             tc_fence_after();
             if (p.cp_kv) fence_proxy_async_smem();
-            const int stage = next_qk % NS;
-            const uint32_t d = tm + (next_qk & 1) * C::SCOLS;
-            const uint64_t qd = desc_kmajor_sw128(sbase + C::OFF_Q + (cq.seg % C::NQB) * C::QBYTES);
-            const uint64_t kd = desc_kmajor_sw128(sbase + stage * C::STAGE, C::LGRP);
-            const uint64_t rd = desc_kmajor_sw128(sbase + stage * C::STAGE + C::OFF_R);
+          }
+        }
+        if (qk_go) {
+          const int stage = next_qk % NS;
+          const uint32_t d = tm + (next_qk & 1) * C::SCOLS;
+          const uint64_t qd = desc_kmajor_sw128(sbase + C::OFF_Q + (cq.seg % C::NQB) * C::QBYTES);
+          const uint64_t kd = desc_kmajor_sw128(sbase + stage * C::STAGE, C::LGRP);
+          const uint64_t rd = desc_kmajor_sw128(sbase + stage * C::STAGE + C::OFF_R);
+          // one chunk, fully unrolled per chunk index (a runtime MMA loop
+          // loses the uniform-register descriptors and issues 2x slower).
+          // State part: A = Q in TMEM (TS), RoPE part: A = Q's RoPE chunk in smem.
+          auto chunk = [&](auto ci) {
+            constexpr int e0 = decltype(ci)::value * QK_CHUNK;
 #pragma unroll
-            for (int c = 0; c < C::NCH_QK; ++c) {
-#pragma unroll
-              for (int k = 0; k < 4; ++k)
-                umma_f16_ss_warp(d, qd + static_cast<uint64_t>((c * C::QCHUNK + k * 32) >> 4),
-                                 kd + static_cast<uint64_t>((c * 1024 + k * 32) >> 4), idesc_qk, (c | k) != 0);
+            for (int e = e0; e < (e0 + QK_CHUNK < NQK ? e0 + QK_CHUNK : NQK); ++e) {
+              if (e < C::NCH_QK * 4) {
+                if (GLAD_DBG_NO_TS) continue;
+                umma_f16_ts_warp(d, tm + C::QN_COL + e * 8,
+                                 kd + static_cast<uint64_t>(((e >> 2) * 1024 + (e & 3) * 32) >> 4), idesc_qk, e != 0);
+              } else {
+                umma_f16_ss_warp(d, qd + static_cast<uint64_t>(((e - C::NCH_QK * 4) * 32) >> 4),
+                                 rd + static_cast<uint64_t>(((e - C::NCH_QK * 4) * 32) >> 4), idesc_qk,
+                                 (GLAD_DBG_NO_TS && e == C::NCH_QK * 4) ? 0u : 1u);
+              }
             }
-#pragma unroll
-            for (int k = 0; k < C::RK; ++k)
-              umma_f16_ss_warp(d, qd + static_cast<uint64_t>((C::NCH_QK * C::QCHUNK + k * 32) >> 4),
-                               rd + static_cast<uint64_t>((k * 32) >> 4), idesc_qk, 1u);
+          };
+          const int ci = qk_e / QK_CHUNK;
+          static_assert(NQK <= 6 * QK_CHUNK, "QK chunks");
+          if (ci == 0) chunk(std::integral_constant<int, 0>{});
+          else if (ci == 1) chunk(std::integral_constant<int, 1>{});
+          else if (ci == 2) chunk(std::integral_constant<int, 2>{});
+          else if (ci == 3) chunk(std::integral_constant<int, 3>{});
+          else if (ci == 4) chunk(std::integral_constant<int, 4>{});
+          else chunk(std::integral_constant<int, 5>{});
+          const int e1 = min(qk_e + QK_CHUNK, NQK);
+          qk_e = e1;
+          if (qk_e == NQK) {
             umma_commit_warp(&s_full[next_qk & 1]);
             if (cq.tl + 1 == cq.t1) umma_commit_warp(&q_empty[cq.seg % C::NQB]);
+            if (trace && lane == 0 && next_qk < kTraceTiles) trace[16 + 12 * next_qk] = globaltimer();
             ++next_qk;
             qk_left = advance(cq);
-            did = true;
+            qk_e = 0;
           }
+          did = true;
         }
         if (did) {
           t0 = clock64();
@@ -868,6 +939,7 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
   } else if (warp < 4 && !(warp == 3 && p.cp_kv && p.q_tma)) {
     // ========================= Q loader: TMA (one thread) or cp.async (64 threads) =========================
     const int tid = threadIdx.x - 64;
+    constexpr int QCH0 = C::ROWS ? C::NCH_QK : 0;  // first Q chunk staged in shared memory
     int k = 0, u = 0, seg = 0;
     Seg s;
     while (next_seg(k, u, s)) {
@@ -881,9 +953,9 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
           const int c1 = s.head * p.g_q + (p.q_box_t == 1 ? s.n0 % p.g_q : 0);
           const int c2 = s.b * p.Lq + s.n0 / p.g_q;
 #pragma unroll
-          for (int ch = 0; ch < C::NQCH; ++ch) {
+          for (int ch = QCH0; ch < C::NQCH; ++ch) {  // rows mode: the RoPE chunk only
             const int col = ch < C::NCH_QK ? ch * 64 : C::D_KN;
-            tma_load_3d(qdst + ch * C::QCHUNK, &qmap, &q_full[qbuf], col, c1, c2);
+            tma_load_3d(qdst + (ch - QCH0) * C::QCHUNK, &qmap, &q_full[qbuf], col, c1, c2);
           }
         }
         if (seg == 0) {
@@ -892,10 +964,11 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
           named_bar_arrive(3, 96);
         }
       } else {
-        for (int idx = tid; idx < NQ * C::NQCH * 8; idx += 64) {
-          const int n = idx / (C::NQCH * 8);
-          const int uu = idx - n * (C::NQCH * 8);
-          const int ch = uu >> 3, w = uu & 7;
+        constexpr int NCQ = C::NQCH - QCH0;  // chunks staged in shared memory
+        for (int idx = tid; idx < NQ * NCQ * 8; idx += 64) {
+          const int n = idx / (NCQ * 8);
+          const int uu = idx - n * (NCQ * 8);
+          const int ch = QCH0 + (uu >> 3), w = uu & 7;
           const void* src = p.q;
           uint32_t bytes = 0;
           if (n < s.nq) {
@@ -907,7 +980,7 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
               bytes = 16;
             }
           }
-          cp_async16(qdst + ch * C::QCHUNK + n * 128 + ((w ^ (n & 7)) << 4), src, bytes);
+          cp_async16(qdst + (ch - QCH0) * C::QCHUNK + n * 128 + ((w ^ (n & 7)) << 4), src, bytes);
         }
         if (seg == 0) named_bar_arrive(3, 96);
         cp_async_wait_all();
@@ -940,9 +1013,35 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
     float* mx_x = red;                                                   // [2 wg][128] partial row max
     float* l_x = reinterpret_cast<float*>(aux + 3072 + C::MAXSEG * 16 + T * 4);  // [2 wg][128] partial row sums
     const float sl2 = p.scale_log2;
+    // Q state part of segment sq's row n (this WG's half of D_KN) -> TMEM
+    // (A operand of the TS-mode QK: lane = row, 2 bf16 per column).  Called
+    // once the previous segment's last QK has completed (its S was read).
+    auto load_q = [&](const Seg& sq) {
+      constexpr int NV = C::D_KN / 16;  // 16-B vectors of this thread's half row
+      uint4 v[NV];
+      if (n < sq.nq) {
+        const int ng = sq.n0 + n, tq = ng / p.g_q, hq = sq.head * p.g_q + (ng - tq * p.g_q);
+        const uint4* src = reinterpret_cast<const uint4*>(
+            p.q + ((static_cast<size_t>(sq.b) * p.Lq + tq) * p.H + hq) * C::DQ + wg * (C::D_KN / 2));
+#pragma unroll
+        for (int i = 0; i < NV; ++i) v[i] = __ldg(src + i);
+      } else {
+#pragma unroll
+        for (int i = 0; i < NV; ++i) v[i] = make_uint4(0u, 0u, 0u, 0u);
+      }
+      const uint32_t qa = tmem + lane_addr + C::QN_COL + wg * (C::D_KN / 4);
+#pragma unroll
+      for (int i = 0; i < NV; i += 4) tmem_st16_u32(qa + i * 4, reinterpret_cast<const uint32_t*>(v + i));
+      tmem_st_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(qn_full);
+    };
     int k = 0, u = 0, seg = 0, it = 0;
     Seg s;
-    while (next_seg(k, u, s)) {
+    bool have = next_seg(k, u, s);
+    if (have) load_q(s);
+    while (have) {
       int vend = 0, t_row = 0, h_row = 0;
       if (n < s.nq) {
         const int ng = s.n0 + n;
@@ -958,11 +1057,15 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
         const uint32_t sbuf = tmem + lane_addr + sb * C::SCOLS;
         mbar_wait(&s_full[sb], (it >> 1) & 1);
         tc_fence_after();
+        if (trace && threadIdx.x == 128 && it < kTraceTiles) trace[10 + 12 * it] = globaltimer();
         const int c0 = tl * T + wg * TH;  // first token of this thread's columns
         float x[TH];
 #pragma unroll
         for (int c = 0; c < TH; c += 16) tmem_ld16(sbuf + wg * TH + c, x + c);
         tmem_ld_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&s_empty[sb]);  // S(sb) read: QK(it + 2) may overwrite it
         if (c0 + TH > vend) {
 #pragma unroll
           for (int j = 0; j < TH; ++j) x[j] = (c0 + j < vend) ? x[j] : -INFINITY;
@@ -1015,10 +1118,18 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
 #pragma unroll
         for (int j = 0; j < NP; ++j)
           l2 = fadd2(l2, make_float2(__uint_as_float(pk[j] << 16), __uint_as_float(pk[j] & 0xffff0000u)));
-        // bf16 P over the upper half of this tile's S buffer (A of the TS PV)
+        // bf16 P row piece into P buffer sb (K-major SW128, 64-token chunks);
+        // its previous contents (tile it - 2) must have been read by PV(it - 2)
+        if (it >= 2) mbar_wait(&pv_done[(it - 2) & 3], ((it - 2) >> 2) & 1);
+        {
+          const uint32_t pb = sbase + C::OFF_P + sb * C::PBUF + n * 128;
 #pragma unroll
-        for (int c = 0; c < NP; c += 8) tmem_st8(sbuf + T / 2 + wg * NP + c, reinterpret_cast<const float*>(pk + c));
-        tmem_st_wait();
+          for (int g = 0; g < NP / 4; ++g) {
+            const int tok = wg * TH + g * 8;  // first token of this 16-B piece
+            const uint32_t a = pb + (tok >> 6) * (NQ * 128) + ((((tok & 63) >> 3) ^ (n & 7)) << 4);
+            st_shared_v4(a, pk[4 * g], pk[4 * g + 1], pk[4 * g + 2], pk[4 * g + 3]);
+          }
+        }
         const int p0 = tl * T;
         if (p0 + T > s.kv_end) {  // never-loaded tile rows: zero V (0 * stale smem != NaN)
           const uint32_t stage_base = sbase + (it % NS) * C::STAGE;
@@ -1030,12 +1141,21 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
               for (int uu = 0; uu < 8; ++uu) st_shared_v4(a + uu * 16, 0u, 0u, 0u, 0u);
             }
           }
-          fence_proxy_async_smem();
         }
+        fence_proxy_async_smem();  // P (and zeroed V rows): generic-proxy writes -> UMMA reads
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&p_full[sb]);
+        if (trace && threadIdx.x == 128 && it < kTraceTiles) trace[11 + 12 * it] = globaltimer();
+        if (trace && threadIdx.x == 256 && it < kTraceTiles) trace[14 + 12 * it] = globaltimer();
+        if (trace && lane == 0 && it < kTraceTiles)  // debug: last softmax warp's P arrival
+          atomicMax(reinterpret_cast<unsigned long long*>(trace + 19 + 12 * it), globaltimer());
       }
+      // next segment's Q into TMEM now (this segment's last QK is done), so the
+      // load overlaps the epilogue below
+      Seg sn;
+      const bool have_n = next_seg(k, u, sn);
+      if (have_n) load_q(sn);
       // ---- segment epilogue: O / l, lse (natural log); each WG writes its O half
       l_x[wg * 128 + n] = l2.x + l2.y;
       named_bar_sync(pair_bar, 64);
@@ -1079,7 +1199,10 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
         }
       }
       named_bar_sync(pair_bar, 64);  // l_x read by both WGs before the next segment rewrites it
+      if (trace && threadIdx.x == 128 && it - 1 < kTraceTiles) trace[15 + 12 * (it - 1)] = globaltimer();
       ++seg;
+      s = sn;
+      have = have_n;
     }
   } else {
     // ========================= softmax / correction / epilogue =========================

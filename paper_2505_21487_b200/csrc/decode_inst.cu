@@ -12,9 +12,10 @@ bool decode_rows_supported(const DecodeKey& k) {
 
 bool decode_supported(const DecodeKey& k) {
   if (k.t != 64 && k.t != 96 && k.t != 128) return false;
-  // rows mode: 64- and 96-token tiles (128: S + P + O fill all of TMEM and
-  // the 128-column S row of a thread spills; it faulted on the second tile)
-  if (k.nq == 128) return k.t <= 96 && decode_rows_supported(k);
+  // rows mode: 64- and 96-token tiles whose S buffers, O and the query
+  // state part fit TMEM (rows_fits; 128-token tiles faulted on the second
+  // tile when they still fitted, before Q moved to TMEM)
+  if (k.nq == 128) return decode_rows_supported(k) && (k.t == 64 || k.t == 96) && 2 * k.t + k.d_v + k.d_v / 2 <= 512;
   if (k.nq != 16 && k.nq != 32 && k.nq != 64) return false;
   if (k.nq > decode_max_nq(k.d_v)) return false;
   if (k.d_kn == k.d_v) {  // GLA / MLA: key state == value state

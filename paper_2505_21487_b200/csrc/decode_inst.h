@@ -60,7 +60,7 @@ cudaError_t with_cfg(const DecodeKey& k, F&& f) {
     case 32: return f.template run<DecodeCfg<DV, DV, DR, 32, T>>();           \
     case 64: return f.template run<DecodeCfg<DV, DV, DR, 64, T>>();           \
     case 128:                                                                 \
-      if constexpr (T <= 96) return f.template run<DecodeCfg<DV, DV, DR, 128, T>>(); \
+      if constexpr (rows_fits<DV, T>()) return f.template run<DecodeCfg<DV, DV, DR, 128, T>>(); \
       else return cudaErrorInvalidValue;                                      \
     default: return cudaErrorInvalidValue;                                    \
   }

@@ -71,6 +71,7 @@ print(f"  S->P      {med(tile[:, :, 3] - tile[:, :, 2], m):8.0f}")
 print(f"  P->PV     {med(tile[:, :, 4] - tile[:, :, 3], m):8.0f}")
 print(f"  P(WG1)-P(WG0) {med(tile[:, :, 6] - tile[:, :, 3], m):8.0f}")
 print(f"  P(WG1)->PV {med(tile[:, :, 4] - tile[:, :, 6], m):8.0f}")
+print(f"  P(last warp)-P(WG0) {med(tile[:, :, 11] - tile[:, :, 3], m & (tile[:, :, 11] > 0)):8.0f}  P(last warp)->PV {med(tile[:, :, 4] - tile[:, :, 11], m & (tile[:, :, 11] > 0)):8.0f}")
 ns = a.ns
 pv_to_free = tile[:, ns:, 5] - tile[:, :-ns, 4]
 print(f"  free(i+{ns})-PV(i) {med(pv_to_free, valid[:, ns:] & valid[:, :-ns]):8.0f}")
@@ -104,9 +105,9 @@ print(f"  epilogue: S(last)->epi done {np.nanmedian(np.where(epi > 0, epi - tile
 if os.environ.get("TRACE_RAW"):
     c = int(os.environ.get("TRACE_CTA", "5"))
     base = tr[c, 0]
-    print(f"raw timeline of CTA {c} (us from CTA start): free, load, landed, QK, QKret, S, P0, P1, PV, PVret, epi")
+    print(f"raw timeline of CTA {c} (us from CTA start): free, load, landed, QK, QKret, S, P0, P1, Plast, PV, PVret, epi")
     for i in range(int(os.environ.get("TRACE_FROM", "0")), int(os.environ.get("TRACE_TO", "128"))):
         if tile[c, i, 1] == 0:
             break
         print(f"  tile {i:2d}: " + "  ".join(f"{(tile[c, i, j] - base) / 1e3:8.2f}" if tile[c, i, j] else "       -"
-                                          for j in (5, 0, 10, 1, 8, 2, 3, 6, 4, 9, 7)))
+                                          for j in (5, 0, 10, 1, 8, 2, 3, 6, 11, 4, 9, 7)))
