@@ -88,6 +88,15 @@ struct DecodeParams {
 #ifndef GLAD_ROWS_QK_AHEAD
 #define GLAD_ROWS_QK_AHEAD 2
 #endif
+#ifndef GLAD_SOFTMAX_PHASES
+#define GLAD_SOFTMAX_PHASES 0
+#endif
+#ifndef GLAD_PF_MAX_NS
+#define GLAD_PF_MAX_NS 2
+#endif
+#ifndef GLAD_ROWS_NS_CAP
+#define GLAD_ROWS_NS_CAP 4
+#endif
 #ifndef GLAD_DBG_NO_TS
 #define GLAD_DBG_NO_TS 0
 #endif
@@ -166,7 +175,13 @@ struct DecodeCfg {
   static constexpr int PCH = (T + 63) / 64;
   static constexpr int PBUF = ROWS ? PCH * NQ * 128 : 0;  // one P buffer
   static constexpr int NS_RAW = (AVAIL - QBYTES - 2 * PBUF - XTRA) / STAGE;
-  static constexpr int NS = NS_RAW > GLAD_NS_CAP ? GLAD_NS_CAP : NS_RAW;
+  static constexpr int NS_CAP = ROWS ? GLAD_ROWS_NS_CAP : GLAD_NS_CAP;
+  static constexpr int NS = NS_RAW > NS_CAP ? NS_CAP : NS_RAW;
+  // L2 prefetch of the tile NS ahead by the producer: it shortens the stage
+  // refill chain when there are only two stages (C2 GLA-2: 0.277 -> 0.270
+  // ms); with three or more the extra TMA issues cost more than they save
+  // (C4 GTA 0.573 -> 0.432 ms, C3 rows 0.223 -> 0.213 ms without it).
+  static constexpr bool L2PF = NS <= GLAD_PF_MAX_NS;
   // a second Q buffer (next unit's Q prefetched while this one runs) when it
   // costs no KV stage
   static constexpr int NQB = ((AVAIL - 2 * QBYTES - 2 * PBUF - XTRA) / STAGE >= NS) ? 2 : 1;
@@ -678,7 +693,7 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
             issue_item(s, item_row(bt_row, p0, bx >> 1), bx >> 1, bx & 1, stage_addr, &kv_full[stage]);
         }
         if (trace && lane == 0 && it < kTraceTiles) trace[8 + 12 * it] = globaltimer();
-        if (pvalid && loader) {  // L2 prefetch of tile it + NS, after the stage load so it never delays it
+        if (C::L2PF && pvalid && loader) {  // L2 prefetch of tile it + NS, after the stage load so it never delays it
           issue_tile(ps, ptl, 0, true, -1);
           pf_advance();
         }
@@ -1037,6 +1052,12 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(qn_full);
     };
+    // debug phase timer (warp 4 of a traced launch): cycles spent between
+    // softmax checkpoints, summed over tiles, written at the end
+    long long ph_t = clock64(), ph_acc[6] = {0, 0, 0, 0, 0, 0};
+    auto PH = [&](int i) {
+      if (GLAD_SOFTMAX_PHASES && trace) { const long long t = clock64(); ph_acc[i] += t - ph_t; ph_t = t; }
+    };
     int k = 0, u = 0, seg = 0, it = 0;
     Seg s;
     bool have = next_seg(k, u, s);
@@ -1056,6 +1077,7 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
         const int sb = it & 1;
         const uint32_t sbuf = tmem + lane_addr + sb * C::SCOLS;
         mbar_wait(&s_full[sb], (it >> 1) & 1);
+        PH(0);
         tc_fence_after();
         if (trace && threadIdx.x == 128 && it < kTraceTiles) trace[10 + 12 * it] = globaltimer();
         const int c0 = tl * T + wg * TH;  // first token of this thread's columns
@@ -1066,6 +1088,7 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&s_empty[sb]);  // S(sb) read: QK(it + 2) may overwrite it
+        PH(1);
         if (c0 + TH > vend) {
 #pragma unroll
           for (int j = 0; j < TH; ++j) x[j] = (c0 + j < vend) ? x[j] : -INFINITY;
@@ -1083,6 +1106,7 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
 #pragma unroll
         for (int j = 1; j < NP; ++j) pmax = max_u16x2(pmax, pk[j]);
         const bool need = (tl == s.t0) || ((pmax & 0xffffu) > kTrig) || ((pmax >> 16) > kTrig);
+        PH(2);
         if (named_bar_red_or(pair_bar, 64, need)) {
           float mt = x[0];
 #pragma unroll
@@ -1114,6 +1138,7 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
           }
           exp_pack();
         }
+        PH(3);
         // row sum of the bf16-rounded p the PV multiplies
 #pragma unroll
         for (int j = 0; j < NP; ++j)
@@ -1143,9 +1168,11 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
           }
         }
         fence_proxy_async_smem();  // P (and zeroed V rows): generic-proxy writes -> UMMA reads
+        PH(4);
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&p_full[sb]);
+        PH(5);
         if (trace && threadIdx.x == 128 && it < kTraceTiles) trace[11 + 12 * it] = globaltimer();
         if (trace && threadIdx.x == 256 && it < kTraceTiles) trace[14 + 12 * it] = globaltimer();
         if (trace && lane == 0 && it < kTraceTiles)  // debug: last softmax warp's P arrival
@@ -1203,7 +1230,10 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
       ++seg;
       s = sn;
       have = have_n;
+      PH(5);
     }
+    if (GLAD_SOFTMAX_PHASES && trace && threadIdx.x == 128)
+      for (int i = 0; i < 6; ++i) trace[kTraceStride - 14 + i] = static_cast<uint64_t>(ph_acc[i]);
   } else {
     // ========================= softmax / correction / epilogue =========================
     // Thread -> data: token row tr = 32*wq + lane of S^T (rows >= T carry no
