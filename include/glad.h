@@ -205,6 +205,37 @@ GLAD_API int32_t glad_tp_duplication(int32_t N, int32_t g_q, int32_t h_q);
 GLAD_API glad_status glad_tp_shard(int32_t h_q, int32_t n_kv_heads, int32_t N, int32_t rank, int32_t* kv_begin,
                           int32_t* kv_end, int32_t* q_begin, int32_t* q_end);
 
+/* ---- sequence split (context-parallel decode, BASELINE
+ * north_star "optional sequence-split for long context merged with an LSE
+ * all-gather"; the paper itself splits heads only) ---- */
+
+/*
+ * Token range [*begin, *end) of a sequence of L keys owned by rank `rank` of
+ * the P ranks that hold the same latent / KV heads (host-only, pure).  Ranges
+ * are contiguous, page-aligned (except the final end = L), disjoint, ordered
+ * by rank and cover [0, L); pages are split as evenly as possible with later
+ * ranks taking the extra ones.  Rank P-1 always holds the last
+ * min(L, Lq - 1) keys, so it alone decodes with causal = 1 (bottom-right
+ * aligned on its local length, R2) and every other rank with causal = 0.
+ * An empty range is begin == end.  Output pointers are HOST.
+ */
+GLAD_API glad_status glad_seq_split_range(int32_t L, int32_t page_size, int32_t Lq, int32_t P, int32_t rank,
+                                          int32_t* begin, int32_t* end);
+
+/*
+ * LSE all-gather merge step of the sequence split (device).  lse_all
+ * [P, rows] fp32: every rank's lse of the same rows (gathered by the caller,
+ * e.g. NCCL all-gather; -inf for an empty range).  o [rows, d_v] bf16: this
+ * rank's normalised partial output.  Writes o_out [rows, d_v] fp32 (a
+ * separate buffer; fp32 so the split adds no rounding of its own) =
+ * o * exp(lse_all[rank] - lse) with lse = ln sum_p exp(lse_all[p]), and
+ * lse_out [rows] (may be NULL).  Summing o_out over the P ranks (e.g. inside
+ * the o_proj all-reduce, which is linear) gives the attention output over the
+ * whole sequence.  d_v % 8 == 0; o, o_out 16-byte aligned.
+ */
+GLAD_API glad_status glad_seq_split_rescale(const float* lse_all, int32_t P, int32_t rank, const void* o,
+                                            int64_t rows, int32_t d_v, void* o_out, float* lse_out, void* stream);
+
 /* Variants for glad_kv_bytes_per_token_per_device. */
 enum { GLAD_MHA = 0, GLAD_MQA = 1, GLAD_GQA = 2, GLAD_GTA = 3, GLAD_GLA = 4, GLAD_MLA = 5 };
 

@@ -88,3 +88,40 @@ def tp_oproj_allreduce(o_lat, W_vo, N, n_kv_heads):
         part = o_lat[:, q0:q1, :].reshape(T, -1) @ W_vo[q0:q1].reshape(-1, W_vo.shape[2])
         total += part
     return total
+
+
+def seq_split_ranges(L, page_size, Lq, P):
+    """Sequence split of one head group (reading R17 in
+    DESIGN.md): the P ranks own contiguous page-aligned token ranges,
+    later ranks first in line for the extra pages, and the last rank holds
+    the last min(L, Lq - 1) keys so that it alone needs the causal mask.
+
+    Written page by page: pages are dealt out in rank order with counts
+    floor(n/P) (+1 for the last n mod P ranks); then whole pages move from
+    the earlier ranks to the last one until it holds every key index
+    >= L - (Lq - 1).  Returns [(begin, end)] per rank.
+    """
+    n = -(-L // page_size)
+    counts = [n // P + (1 if r >= P - n % P else 0) for r in range(P)]
+    owner = []
+    for r in range(P):
+        owner += [r] * counts[r]
+    must = max(0, L - (Lq - 1))          # keys with index >= must belong to the last rank
+    for pg in range(n):
+        if (pg + 1) * page_size > must:  # page holds a key >= must
+            owner[pg] = P - 1
+    ranges = []
+    for r in range(P):
+        toks = [j for j in range(L) if owner[j // page_size] == r]
+        ranges.append((toks[0], toks[-1] + 1) if toks else None)
+    # empty ranges sit where the rank's pages would have started
+    out = []
+    for r in range(P):
+        if ranges[r] is not None:
+            out.append(ranges[r])
+        else:
+            nxt = [ranges[q][0] for q in range(r + 1, P) if ranges[q] is not None]
+            prv = [ranges[q][1] for q in range(r) if ranges[q] is not None]
+            pos = prv[-1] if prv else (nxt[0] if nxt else 0)
+            out.append((pos, pos))
+    return out

@@ -434,6 +434,47 @@ glad_status glad_splitkv_combine(const float* o_part, const float* lse_part, int
   return GLAD_OK;
 }
 
+glad_status glad_seq_split_rescale(const float* lse_all, int32_t P, int32_t rank, const void* o, int64_t rows,
+                                   int32_t d_v, void* o_out, float* lse_out, void* stream) {
+  if (P < 1 || rank < 0 || rank >= P || rows < 0 || d_v < 8 || d_v % 8)
+    return fail(GLAD_ERR_INVALID_ARG, "seq split rescale P=%d rank=%d rows=%lld d_v=%d invalid", P, rank,
+                static_cast<long long>(rows), d_v);
+  if (rows == 0) return GLAD_OK;
+  if (!lse_all || !o || !o_out) return fail(GLAD_ERR_INVALID_ARG, "NULL pointer");
+  if (!aligned16(o) || !aligned16(o_out)) return fail(GLAD_ERR_INVALID_ARG, "o/o_out must be 16-byte aligned");
+  cudaError_t e = glad::launch_lse_rescale(lse_all, P, rank, o, rows, d_v, o_out, lse_out,
+                                           static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return fail(GLAD_ERR_CUDA, "seq split rescale launch failed: %s", cudaGetErrorString(e));
+  return GLAD_OK;
+}
+
+glad_status glad_seq_split_range(int32_t L, int32_t page_size, int32_t Lq, int32_t P, int32_t rank, int32_t* begin,
+                                 int32_t* end) {
+  if (!begin || !end) return fail(GLAD_ERR_INVALID_ARG, "NULL output pointer");
+  if (L < 0 || page_size < 1 || Lq < 1 || P < 1 || rank < 0 || rank >= P)
+    return fail(GLAD_ERR_INVALID_ARG, "seq split L=%d page=%d Lq=%d P=%d rank=%d invalid", L, page_size, Lq, P, rank);
+  // pages split as evenly as possible, the later ranks taking the extra ones
+  const int64_t n = (static_cast<int64_t>(L) + page_size - 1) / page_size;
+  const int64_t base = n / P, rem = n % P;
+  auto first_page = [&](int64_t r) { return r * base + std::max<int64_t>(0, r - (P - rem)); };
+  // the last rank holds (at least) the last Lq - 1 keys, so it alone needs the
+  // causal mask: every key of an earlier rank is visible to every query
+  int64_t last = first_page(P - 1) * page_size;
+  const int64_t must = std::max<int64_t>(0, static_cast<int64_t>(L) - (Lq - 1));
+  if (last > must) last = (must / page_size) * page_size;
+  int64_t b, e;
+  if (rank == P - 1) {
+    b = last;
+    e = L;
+  } else {
+    b = std::min<int64_t>(first_page(rank) * page_size, last);
+    e = std::min<int64_t>(std::min<int64_t>(first_page(rank + 1) * page_size, last), L);
+  }
+  *begin = static_cast<int32_t>(b);
+  *end = static_cast<int32_t>(std::max(b, e));
+  return GLAD_OK;
+}
+
 int32_t glad_tp_duplication(int32_t N, int32_t g_q, int32_t h_q) {
   if (N < 1 || g_q < 1 || h_q < 1 || g_q > h_q) return -1;
   return static_cast<int32_t>((static_cast<int64_t>(N) * g_q + h_q - 1) / h_q);

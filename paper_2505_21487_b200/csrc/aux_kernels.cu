@@ -311,6 +311,54 @@ cudaError_t launch_gather(const void* pool, int64_t row_stride, int page_size, c
   return cudaGetLastError();
 }
 
+// Sequence split across the P ranks of a head group: one
+// warp per row; the row's global lse = ln sum_p exp(lse_all[p][row]) and the
+// rank's normalised partial output is scaled by exp(lse_rank - lse), so the
+// group sum of the scaled rows (folded into the o_proj all-reduce) is the
+// attention output over the whole sequence.
+__global__ void lse_rescale_kernel(const float* __restrict__ lse_all, int32_t P, int32_t rank,
+                                   const __nv_bfloat16* __restrict__ o, int64_t rows, int32_t d_v,
+                                   float* __restrict__ o_out, float* __restrict__ lse_out) {
+  const int64_t row = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (row >= rows) return;
+  float mx = -INFINITY;
+  for (int p = lane; p < P; p += 32) mx = fmaxf(mx, lse_all[p * rows + row]);
+#pragma unroll
+  for (int s = 16; s >= 1; s >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, s));
+  float z = 0.f;
+  for (int p = lane; p < P; p += 32) {
+    const float ls = lse_all[p * rows + row];
+    if (ls != -INFINITY) z += __expf(ls - mx);
+  }
+#pragma unroll
+  for (int s = 16; s >= 1; s >>= 1) z += __shfl_xor_sync(0xffffffffu, z, s);
+  const float lse = (z > 0.f) ? mx + __logf(z) : -INFINITY;
+  if (lane == 0 && lse_out) lse_out[row] = lse;
+  const float own = lse_all[static_cast<int64_t>(rank) * rows + row];
+  const float w = (own == -INFINITY || lse == -INFINITY) ? 0.f : __expf(own - lse);
+  for (int d0 = lane * 8; d0 < d_v; d0 += 256) {
+    const uint4 v = __ldg(reinterpret_cast<const uint4*>(o + row * d_v + d0));
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v);
+    const float2 f0 = __bfloat1622float2(h[0]), f1 = __bfloat1622float2(h[1]);
+    const float2 f2 = __bfloat1622float2(h[2]), f3 = __bfloat1622float2(h[3]);
+    float4* dst = reinterpret_cast<float4*>(o_out + row * d_v + d0);
+    dst[0] = make_float4(f0.x * w, f0.y * w, f1.x * w, f1.y * w);
+    dst[1] = make_float4(f2.x * w, f2.y * w, f3.x * w, f3.y * w);
+  }
+}
+
+cudaError_t launch_lse_rescale(const float* lse_all, int32_t P, int32_t rank, const void* o, int64_t rows,
+                               int32_t d_v, void* o_out, float* lse_out, cudaStream_t stream) {
+  if (rows == 0) return cudaSuccess;
+  const int threads = 128;
+  const int64_t blocks = (rows * 32 + threads - 1) / threads;
+  lse_rescale_kernel<<<static_cast<unsigned>(blocks), threads, 0, stream>>>(
+      lse_all, P, rank, static_cast<const __nv_bfloat16*>(o), rows, d_v, static_cast<float*>(o_out),
+      lse_out);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_combine(const float* o_part, const float* lse_part, int32_t S, int64_t rows, int32_t d_v,
                            void* out, float* lse, cudaStream_t stream) {
   if (rows == 0) return cudaSuccess;

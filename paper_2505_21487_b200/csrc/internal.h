@@ -37,6 +37,8 @@ cudaError_t launch_append(void* pool, int64_t row_stride, int page_size, const i
 cudaError_t launch_gather(const void* pool, int64_t row_stride, int page_size, const int32_t* block_table,
                           int32_t bt_stride, const int32_t* seqlens, int32_t B, int32_t max_len, int32_t width,
                           void* dense_out, cudaStream_t stream);
+cudaError_t launch_lse_rescale(const float* lse_all, int32_t P, int32_t rank, const void* o, int64_t rows,
+                               int32_t d_v, void* o_out, float* lse_out, cudaStream_t stream);
 cudaError_t launch_combine(const float* o_part, const float* lse_part, int32_t S, int64_t rows, int32_t d_v,
                            void* out, float* lse, cudaStream_t stream);
 

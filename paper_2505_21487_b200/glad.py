@@ -72,6 +72,9 @@ def _sig(lib):
         "glad_splitkv_combine": ([_VP, _VP] + [ctypes.c_int32] * 5 + [_VP, _VP, _VP], S),
         "glad_tp_duplication": ([ctypes.c_int32] * 3, ctypes.c_int32),
         "glad_tp_shard": ([ctypes.c_int32] * 4 + [_I32P] * 4, S),
+        "glad_seq_split_range": ([ctypes.c_int32] * 5 + [_I32P] * 2, S),
+        "glad_seq_split_rescale": ([_VP, ctypes.c_int32, ctypes.c_int32, _VP, ctypes.c_int64, ctypes.c_int32, _VP, _VP,
+                                    _VP], S),
         "glad_kv_bytes_per_token_per_device": ([ctypes.c_int32] * 6, ctypes.c_int64),
     }
     for name, (args, res) in table.items():
@@ -96,6 +99,7 @@ def exported_symbols():
     return ["glad_last_error", "glad_version", "glad_debug_set_trace", "glad_debug_set_phase_mask", "glad_debug_set_tile", "glad_pool_bytes", "glad_cache_append", "glad_paged_gather",
             "glad_decode_workspace_bytes", "glad_gla_decode", "glad_mla_decode",
             "glad_gta_decode", "glad_splitkv_combine", "glad_tp_duplication", "glad_tp_shard",
+            "glad_seq_split_range", "glad_seq_split_rescale",
             "glad_kv_bytes_per_token_per_device"]
 
 
@@ -226,6 +230,29 @@ def tp_shard(h_q, n_kv_heads, N, rank):
     vals = [ctypes.c_int32() for _ in range(4)]
     _check(lib().glad_tp_shard(h_q, n_kv_heads, N, rank, *[ctypes.byref(v) for v in vals]))
     return tuple(v.value for v in vals)
+
+
+def seq_split_range(L, page_size, Lq, P, rank):
+    """Token range [begin, end) of rank `rank` of a sequence-split group (glad_seq_split_range)."""
+    b, e = ctypes.c_int32(), ctypes.c_int32()
+    _check(lib().glad_seq_split_range(int(L), int(page_size), int(Lq), int(P), int(rank), ctypes.byref(b),
+                                      ctypes.byref(e)))
+    return b.value, e.value
+
+
+def seq_split_rescale(lse_all, rank, o, out=None, lse_out=None, stream=None):
+    """lse_all [P, ...rows] fp32 (device), o [...rows, d_v] bf16 -> o * exp(lse_rank - lse) (fp32) and the
+    merged lse (glad_seq_split_rescale)."""
+    P = lse_all.shape[0]
+    d_v = o.shape[-1]
+    rows = o.numel() // d_v
+    assert lse_all.dtype == torch.float32 and lse_all.is_contiguous() and lse_all[0].numel() == rows
+    assert o.dtype == torch.bfloat16 and o.is_contiguous()
+    out = torch.empty(o.shape, dtype=torch.float32, device=o.device) if out is None else out
+    lse_out = torch.empty(lse_all.shape[1:], dtype=torch.float32, device=o.device) if lse_out is None else lse_out
+    _check(lib().glad_seq_split_rescale(lse_all.data_ptr(), P, int(rank), o.data_ptr(), rows, d_v, out.data_ptr(),
+                                        lse_out.data_ptr(), _stream(stream)))
+    return out, lse_out
 
 
 def kv_bytes_per_token_per_device(variant, n_kv_heads, d_head, d_rope, N, dtype_bytes=2):

@@ -39,3 +39,43 @@ def oproj_allreduce(o_local, w_vo_local, out=None, group=None):
     if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
         dist.all_reduce(y, group=group)
     return y
+
+
+# ------------------------------------------------------------ sequence split
+# SURVEY §8(f)-1 (north_star: "optional sequence-split for long context
+# merged with an LSE all-gather"): the P ranks of a head group each hold a
+# contiguous page-aligned token range of every sequence (glad_seq_split_range)
+# in their own pool, decode it (rank P-1 causal, the others not: it holds the
+# last Lq - 1 keys), all-gather only the LSE [B, Lq, H_loc] fp32, rescale their
+# partial output by exp(lse_r - lse) (glad_seq_split_rescale) and let the
+# o_proj all-reduce (linear) do the sum.
+
+
+def seq_split_ranges(seqlens, page_size, Lq, P, rank):
+    """Per-sequence (begin, end) token ranges of `rank` -> int32 arrays, and
+    the causal flag its decode call uses."""
+    import numpy as np
+    rng = [glad.seq_split_range(int(L), page_size, Lq, P, rank) for L in seqlens]
+    begin = np.array([b for b, _ in rng], dtype=np.int32)
+    end = np.array([e for _, e in rng], dtype=np.int32)
+    return begin, end, rank == P - 1
+
+
+def gather_lse(lse_local, group=None):
+    """[P, *lse.shape]: every rank's lse of the same rows (all-gather over the
+    sequence-split group; NCCL on GPUs, gloo in the CPU tests)."""
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size(group) == 1:
+        return lse_local.unsqueeze(0).contiguous()
+    parts = [torch.empty_like(lse_local) for _ in range(dist.get_world_size(group))]
+    dist.all_gather(parts, lse_local.contiguous(), group=group)
+    return torch.stack(parts).contiguous()
+
+
+def seq_split_oproj_allreduce(o_local, lse_local, w_vo_local, split_group=None, group=None, out=None):
+    """o_local [T, H_loc, d_c] bf16 (this rank's normalised output over its
+    token range), lse_local [T, H_loc] fp32 -> all-reduced [T, d_model]:
+    sum over ranks of (o_r exp(lse_r - lse)) W_r^vo."""
+    lse_all = gather_lse(lse_local, split_group)
+    rank = dist.get_rank(split_group) if (dist.is_available() and dist.is_initialized()) else 0
+    o_scaled, _ = glad.seq_split_rescale(lse_all, rank, o_local.contiguous())
+    return oproj_allreduce(o_scaled.to(w_vo_local.dtype), w_vo_local, out=out, group=group)

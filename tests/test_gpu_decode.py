@@ -372,3 +372,41 @@ def test_c3_full_size_sampled(name):
     out, lse = workloads.run(wl, st)
     torch.cuda.synchronize()
     _sampled_latent_check(wl, st, out, lse, samples=[(0, 0), (21, 1), (63, 0), (63, 1)])
+
+
+# ------------------------------------------- sequence split
+@pytest.mark.parametrize("P,Lq,page", [(2, 1, 64), (4, 2, 16), (3, 4, 64), (8, 2, 1)])
+def test_seq_split_emulated(P, Lq, page):
+    """Single-GPU emulation of the sequence split: each of the P ranks of a
+    head group decodes its token range (glad_seq_split_range) from its own
+    pool (rank P-1 causal, others not), glad_seq_split_rescale scales its
+    output by exp(lse_r - lse) from the gathered LSE, and the sum over ranks
+    (what the o_proj all-reduce adds) equals the oracle over the whole
+    sequence."""
+    from paper_2505_21487_b200 import tp
+    B, H, h_c, d_c, d_R = 3, 64, 2, 256, 64
+    sl = np.array([1500, 333, 70])
+    q, c, kr = synth.latent_kernel_inputs(B, Lq, H, h_c, d_c, d_R, int(sl.max()), seed=70 + P)
+    rows = latent_rows(c, kr)
+    scale = 1.0 / math.sqrt(192)
+    outs, lses = [], []
+    for r in range(P):
+        begin, end, causal = tp.seq_split_ranges(sl, page, Lq, P, r)
+        n = end - begin
+        Lm = max(int(n.max()), 1)
+        loc = torch.zeros(B, Lm, rows.shape[-1], dtype=rows.dtype)
+        for b in range(B):
+            loc[b, :n[b]] = rows[b, begin[b]:end[b]]
+        layout, pool, bt = build_paged(loc, n, page, h_c, d_c, d_R, seed=r)
+        o_r, lse_r = glad.gla_decode(q.to(DEV), pool, layout, bt, torch.from_numpy(n.astype(np.int32)).to(DEV),
+                                     scale, causal=causal)
+        outs.append(o_r)
+        lses.append(lse_r)
+    lse_all = torch.stack(lses).contiguous()
+    acc = torch.zeros(outs[0].shape, dtype=torch.float32, device=DEV)
+    for r in range(P):
+        o_s, lse_m = glad.seq_split_rescale(lse_all, r, outs[r])
+        acc += o_s.float()
+    torch.cuda.synchronize()
+    o_ref, lse_ref = OA.latent_decode(f64(q), f64(c), f64(kr), sl, scale, causal=True)
+    check(acc, lse_m, o_ref, lse_ref, what=f"seq split P={P} Lq={Lq}")

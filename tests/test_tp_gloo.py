@@ -52,3 +52,32 @@ def test_tp2_oproj_allreduce_matches_unsharded(tmp_path, h_c):
     w_vo = torch.randn(16 * 8, 12, generator=g, dtype=torch.float64)
     ref = SH.tp_oproj_allreduce(o_lat.numpy(), w_vo.numpy().reshape(16, 8, 12), world, h_c)
     np.testing.assert_allclose(np.load(out), ref, atol=1e-10)
+
+
+def _worker_lse(rank, world, port, out_path):
+    import sys
+    sys.path.insert(0, ROOT)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2505_21487_b200 import tp
+    g = torch.Generator().manual_seed(7)
+    lse = torch.randn(world, 3, 2, 5, generator=g)
+    lse[0, 1, 1, 2] = -float("inf")  # an empty range on rank 0
+    gathered = tp.gather_lse(lse[rank].clone())
+    if rank == 0:
+        np.save(out_path, gathered.numpy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_seq_split_lse_allgather(tmp_path):
+    """Sequence split host plumbing over gloo, world size 2:
+    the LSE all-gather returns every rank's lse in rank order (the input of
+    glad_seq_split_rescale)."""
+    world = 2
+    out = str(tmp_path / "g.npy")
+    mp.start_processes(_worker_lse, args=(world, _free_port(), out), nprocs=world, join=True, start_method="spawn")
+    g = torch.Generator().manual_seed(7)
+    lse = torch.randn(world, 3, 2, 5, generator=g)
+    lse[0, 1, 1, 2] = -float("inf")
+    np.testing.assert_array_equal(np.load(out), lse.numpy())
