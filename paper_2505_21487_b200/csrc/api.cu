@@ -244,7 +244,21 @@ glad_status decode_common(Variant v, const void* q, const void* pool, const glad
   // K-major atom layout the kernel's descriptors expect.
   CUtensorMap lmap;
   std::memset(&lmap, 0, sizeof(lmap));
-  if (L->page_size >= 16) {
+  // pages shorter than 16 tokens: TMA gather4 (4 token rows per instruction)
+  // unless glad_debug_set_phase_mask bit 32 selects the cooperative cp.async
+  // producer; lmap is then the row map (box 64 cols x 1 row, 128B swizzle)
+  const bool g4 = L->page_size < 16 && !(g_phase_mask & 32);
+  if (g4) {
+    cuuint64_t gd[2] = {static_cast<cuuint64_t>(row_width(L)),
+                        static_cast<cuuint64_t>(L->num_pages) * static_cast<cuuint64_t>(L->page_size)};
+    cuuint64_t gs[1] = {static_cast<cuuint64_t>(L->row_stride) * 2};
+    cuuint32_t gb[2] = {64u, 1u};
+    cuuint32_t ge[2] = {1u, 1u};
+    cr = enc(&lmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(pool), gd, gs, gb, ge,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, pr, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (cr != CUDA_SUCCESS)
+      return fail(GLAD_ERR_CUDA, "cuTensorMapEncodeTiled (gather4 rows) failed (%d)", static_cast<int>(cr));
+  } else if (L->page_size >= 16) {
     const cuuint64_t rs = static_cast<cuuint64_t>(L->row_stride) * 2;
     cuuint64_t ld[4] = {64u, 8u, static_cast<cuuint64_t>(L->n_heads_kv) * L->d_head / 64,
                         static_cast<cuuint64_t>(L->num_pages) * static_cast<cuuint64_t>(L->page_size) / 8};
@@ -284,7 +298,8 @@ glad_status decode_common(Variant v, const void* q, const void* pool, const glad
   p.row_stride = L->row_stride;
   // pages shorter than 16 tokens: one TMA per page run per chunk costs ~100
   // cycles of issue each; the cooperative cp.async producer wins (measured)
-  p.cp_kv = L->page_size < 16 ? 1 : 0;
+  p.cp_kv = (L->page_size < 16 && !g4) ? 1 : 0;
+  p.g4 = g4 ? 1 : 0;
   p.head_groups = head_groups;
   p.q_box_h = q_box_h;
   p.q_box_t = q_box_t;
@@ -344,7 +359,7 @@ const char* glad_version(void) { return "glad 0.1.0 sm_100a"; }
 
 void glad_debug_set_trace(void* device_buf) { g_trace = static_cast<uint64_t*>(device_buf); }
 
-void glad_debug_set_phase_mask(int32_t mask) { g_phase_mask = mask & 31; }
+void glad_debug_set_phase_mask(int32_t mask) { g_phase_mask = mask & 63; }
 
 void glad_debug_set_tile(int32_t tokens) { g_tile_override = tokens; }
 

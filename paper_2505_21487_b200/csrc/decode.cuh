@@ -66,6 +66,7 @@ struct DecodeParams {
   const __nv_bfloat16* pool;  // paged cache (cp.async producer path)
   int64_t row_stride;       // elements
   int32_t cp_kv;            // 1: small pages -> cooperative cp.async producer instead of TMA
+  int32_t g4;               // 1: small pages -> TMA gather4 of 4 token rows per instruction (lmap = row map, box (64, 1))
   int32_t q_tma;            // 1: Q via the 3-D tensor map (box (64, q_box_h, q_box_t)); 0: cp.async
   int32_t q_box_h, q_box_t;
   float scale_log2;         // softmax_scale * log2(e)
@@ -482,7 +483,7 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
     }
     fence_barrier_init();
     tma_prefetch_desc(&tmap);
-    if (!p.cp_kv) tma_prefetch_desc(&lmap);
+    if (!p.cp_kv) tma_prefetch_desc(&lmap);  // latent boxes, or the gather4 row map
     if (p.q_tma) tma_prefetch_desc(&qmap);
   }
   if (warp == 2) { tmem_alloc(tmem_slot, C::TMEM_COLS); tmem_relinquish(); }
@@ -605,10 +606,12 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
         }
       }
     }
-  } else if (warp == 0) {
+  } else if (warp == 0 || (warp == 3 && p.g4 && p.q_tma)) {
     // ========================= TMA producer (all 32 lanes issue) =========================
+    // (gather4 mode with TMA-loaded Q: warp 3 is a second producer warp that
+    // issues half of every tile's row groups)
     named_bar_sync(3, 96);  // the first Q load is issued first: QK needs Q, not a second tile
-    if (trace && lane == 0) trace[4] = globaltimer();
+    if (trace && lane == 0 && warp == 0) trace[4] = globaltimer();
     const int box_rows = p.box_rows;
     // Two boxes per page run of a tile: item 2*box = the latent slice (4-D
     // map, all NCH_V chunks in one box), item 2*box + 1 = the RoPE chunk
@@ -660,7 +663,7 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
     };
     pf_advance();
     for (int i = 0; i < NS && pvalid; ++i) pf_advance();
-    if (trace && lane == 0) trace[kTraceStride - 6] = globaltimer();  // debug: prefetch cursor ready
+    if (trace && lane == 0 && warp == 0) trace[kTraceStride - 6] = globaltimer();  // debug: prefetch cursor ready
     int k = 0, u = 0, it = 0;
     Seg s;
     while (next_seg(k, u, s)) {
@@ -673,27 +676,55 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
         const int nitem = nbox * 2;
         // the page lookup of this lane's first item is done before the stage
         // wait: after the release only the TMA issue remains on the critical path
-        const int row0 = (loader && lane < nitem) ? item_row(bt_row, p0, lane >> 1) : 0;
-        if (trace && lane == 0 && it == 0) {
+        const int row0 = (loader && !p.g4 && lane < nitem) ? item_row(bt_row, p0, lane >> 1) : 0;
+        if (trace && lane == 0 && warp == 0 && it == 0) {
           if (row0 == 0x7fffffff) __nanosleep(1);  // debug: wait for the lookup itself
           trace[6] = globaltimer();
         }
         mbar_wait(&kv_empty[stage], ((it / NS) & 1) ^ 1);
-        if (trace && lane == 0 && it < kTraceTiles) trace[13 + 12 * it] = globaltimer();
-        if (lane == 0) mbar_arrive_expect_tx(&kv_full[stage], static_cast<uint32_t>(nbox * box_rows * C::NCH * 128));
+        if (trace && lane == 0 && warp == 0 && it < kTraceTiles) trace[13 + 12 * it] = globaltimer();
+        if (lane == 0 && !p.g4)
+          mbar_arrive_expect_tx(&kv_full[stage], static_cast<uint32_t>(nbox * box_rows * C::NCH * 128));
         if (p.cl_n > 1) {  // stage free here -> tell the loader; the loader waits for every CTA
           if (lane == 0) mbar_arrive_cluster(&cl_empty[stage], 0);
           if (loader) mbar_wait(&cl_empty[stage], (it / NS) & 1);
         }
         __syncwarp();
         const uint32_t stage_addr = sbase + stage * C::STAGE;
-        if (loader) {
+        if (p.g4) {
+          // small pages: one gather4 per (4 token rows, 64-column chunk) —
+          // the TMA unit does the per-row address generation of P:308-314;
+          // each lane resolves the block-table entries of its row groups
+          // (rows past the visible end repeat the last visible row: they
+          // are zeroed / masked by the softmax like any unloaded row)
+          const int ngrp = (ntok + 3) >> 2;
+          if (lane == 0 && warp == 0)
+            mbar_arrive_expect_tx(&kv_full[stage], static_cast<uint32_t>(ngrp * C::NCH * 512));
+          __syncwarp();
+          const int npw = (p.q_tma ? 2 : 1), pw = warp == 0 ? 0 : 1;
+          for (int g = lane + 32 * pw; g < ngrp; g += 32 * npw) {
+            int rr[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const int pos = p0 + min(4 * g + j, ntok - 1);
+              rr[j] = __ldg(bt_row + (pos >> p.log2_page)) * p.page_size + (pos & (p.page_size - 1));
+            }
+            const int r = 4 * g;
+            const uint32_t ldst = stage_addr + (r >> 3) * C::LGRP + (r & 7) * 128;
+            const int c_head = s.head * p.d_head;
+#pragma unroll
+            for (int ch = 0; ch < C::NCH_V; ++ch)
+              tma_gather4(ldst + ch * 1024, &lmap, &kv_full[stage], c_head + ch * 64, rr[0], rr[1], rr[2], rr[3]);
+            tma_gather4(stage_addr + C::OFF_R + r * 128, &lmap, &kv_full[stage], p.rope_col, rr[0], rr[1], rr[2],
+                        rr[3]);
+          }
+        } else if (loader) {
           if (lane < nitem) issue_item(s, row0, lane >> 1, lane & 1, stage_addr, &kv_full[stage]);
           for (int bx = lane + 32; bx < nitem; bx += 32)  // small pages: more boxes than lanes
             issue_item(s, item_row(bt_row, p0, bx >> 1), bx >> 1, bx & 1, stage_addr, &kv_full[stage]);
         }
-        if (trace && lane == 0 && it < kTraceTiles) trace[8 + 12 * it] = globaltimer();
-        if (C::L2PF && pvalid && loader) {  // L2 prefetch of tile it + NS, after the stage load so it never delays it
+        if (trace && lane == 0 && warp == 0 && it < kTraceTiles) trace[8 + 12 * it] = globaltimer();
+        if (C::L2PF && !p.g4 && pvalid && loader) {  // L2 prefetch of tile it + NS, after the stage load so it never delays it
           issue_tile(ps, ptl, 0, true, -1);
           pf_advance();
         }
@@ -951,7 +982,7 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
       }
       if (trace && lane == 0) trace[3] = cp.seg + 1;
     }
-  } else if (warp < 4 && !(warp == 3 && p.cp_kv && p.q_tma)) {
+  } else if (warp < 4 && !(warp == 3 && (p.cp_kv || p.g4) && p.q_tma)) {
     // ========================= Q loader: TMA (one thread) or cp.async (64 threads) =========================
     const int tid = threadIdx.x - 64;
     constexpr int QCH0 = C::ROWS ? C::NCH_QK : 0;  // first Q chunk staged in shared memory
