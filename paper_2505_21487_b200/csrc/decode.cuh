@@ -661,9 +661,9 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
       pvalid = next_seg(pk, pu, ps);
       if (pvalid) { ptl = ps.t0; pt1 = ps.t1; }
     };
-    pf_advance();
-    for (int i = 0; i < NS && pvalid; ++i) pf_advance();
-    if (trace && lane == 0 && warp == 0) trace[kTraceStride - 6] = globaltimer();  // debug: prefetch cursor ready
+    // the prefetch cursor is positioned after the first stage load is out
+    // (kernel start is latency-bound: the first load must not wait for it)
+    bool pf_ready = false;
     int k = 0, u = 0, it = 0;
     Seg s;
     while (next_seg(k, u, s)) {
@@ -724,6 +724,12 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
             issue_item(s, item_row(bt_row, p0, bx >> 1), bx >> 1, bx & 1, stage_addr, &kv_full[stage]);
         }
         if (trace && lane == 0 && warp == 0 && it < kTraceTiles) trace[8 + 12 * it] = globaltimer();
+        if (C::L2PF && !p.g4 && loader && !pf_ready) {
+          pf_advance();
+          for (int i = 0; i < NS + it && pvalid; ++i) pf_advance();
+          pf_ready = true;
+          if (trace && lane == 0 && warp == 0) trace[kTraceStride - 6] = globaltimer();  // debug: prefetch cursor ready
+        }
         if (C::L2PF && !p.g4 && pvalid && loader) {  // L2 prefetch of tile it + NS, after the stage load so it never delays it
           issue_tile(ps, ptl, 0, true, -1);
           pf_advance();
