@@ -205,6 +205,36 @@ GLAD_API int32_t glad_tp_duplication(int32_t N, int32_t g_q, int32_t h_q);
 GLAD_API glad_status glad_tp_shard(int32_t h_q, int32_t n_kv_heads, int32_t N, int32_t rank, int32_t* kv_begin,
                           int32_t* kv_end, int32_t* q_begin, int32_t* q_end);
 
+/* ---- the upstream step: kernel inputs from raw tensors ---- */
+
+/*
+ * Absorbed query formation (P:48 weight absorption; R2 positions, R5 RoPE):
+ *   q_out[b,t,h] = [ W_UK[h] q_nope[b,t,h]  ||  RoPE(q_pe[b,t,h], p) ],
+ *   p = seqlens[b] - Lq + t  (seqlens include the Lq new tokens, R2).
+ * q_nope [B, Lq, H, d_h] bf16, q_pe [B, Lq, H, d_rope] bf16 (unrotated),
+ * w_uk [H, d_c, d_h] bf16 (head h's latent -> key up-projection, so the
+ * absorbed query is W_UK[h] q_nope), seqlens [B] int32 (device).  q_out
+ * [B, Lq, H, d_c + d_rope] bf16 = the q of glad_gla_decode / glad_mla_decode.
+ * RoPE: interleaved pairs, theta_i = rope_base^(-2i/d_rope), angle in fp64.
+ * fp32 accumulation, bf16 result.  Supported: d_h in {64, 128}, d_c in
+ * {128, 256, 512}; q_nope / w_uk 16-byte aligned.
+ */
+GLAD_API glad_status glad_gla_absorb_query(const void* q_nope, const void* q_pe, const void* w_uk,
+                                           const int32_t* seqlens, int32_t B, int32_t Lq, int32_t H, int32_t d_h,
+                                           int32_t d_c, int32_t d_rope, float rope_base, void* q_out, void* stream);
+
+/*
+ * Cache append with the RoPE key rotated in the same pass (R5): token
+ * p = seqlens_before[b] + i gets the row [ latent[b,i] || RoPE(k_pe[b,i], p) ]
+ * (paging as glad_cache_append).  latent [B, n_new, n_heads_kv*d_head] bf16,
+ * k_pe [B, n_new, d_rope] bf16 unrotated.  The latent part is a bit-exact
+ * copy; the RoPE part is rotated in fp64 and rounded to bf16.
+ */
+GLAD_API glad_status glad_cache_append_rope(const glad_cache_layout* layout, void* pool, const int32_t* block_table,
+                                            int32_t bt_stride, const int32_t* seqlens_before, const void* latent,
+                                            const void* k_pe, int32_t B, int32_t n_new, float rope_base,
+                                            void* stream);
+
 /* ---- sequence split (context-parallel decode, BASELINE
  * north_star "optional sequence-split for long context merged with an LSE
  * all-gather"; the paper itself splits heads only) ---- */

@@ -260,6 +260,29 @@ def gqa_decode(q, k, v, seqlens, scale, causal=True):
 #   lse = ln sum_s exp(lse_s),  O = sum_s exp(lse_s - lse) O_s
 # where O_s is the *normalised* partial output over split s.
 # --------------------------------------------------------------------------
+def absorb_query(q_nope, q_pe, W_UK, seqlens, Lq, rope_base=10000.0):
+    """Kernel query from raw tensors (P:48 weight absorption, R2 positions,
+    R5 RoPE): q[b,t,h] = [ W_UK[h] q_nope[b,t,h] || RoPE(q_pe[b,t,h], L_b - Lq + t) ].
+
+    q_nope [B,Lq,H,d_h], q_pe [B,Lq,H,d_R], W_UK [H,d_c,d_h] -> [B,Lq,H,d_c+d_R] fp64.
+    """
+    q_nope, q_pe, W_UK = _f64(q_nope), _f64(q_pe), _f64(W_UK)
+    B, _, H, _ = q_nope.shape
+    q_abs = np.einsum("hcd,bthd->bthc", W_UK, q_nope)
+    pos = np.array([[int(seqlens[b]) - Lq + t for t in range(Lq)] for b in range(B)], dtype=np.float64)
+    q_r = rope_rotate(q_pe, pos[:, :, None], rope_base)
+    return np.concatenate([q_abs, q_r], axis=-1)
+
+
+def rope_cache_rows(c, k_pe, start, rope_base=10000.0):
+    """Cache rows [c || RoPE(k_pe, start_b + i)] (P:304 append with the RoPE
+    key rotated at its position).  c [B,n,h_c,d_c], k_pe [B,n,d_R] -> [B,n,W]."""
+    c, k_pe = _f64(c), _f64(k_pe)
+    B, n = c.shape[:2]
+    pos = np.asarray(start, dtype=np.float64)[:, None] + np.arange(n)[None, :]
+    return np.concatenate([c.reshape(B, n, -1), rope_rotate(k_pe, pos, rope_base)], axis=-1)
+
+
 def merge_partials(o_parts, lse_parts):
     """o_parts [S, ..., d], lse_parts [S, ...] -> (o [..., d], lse [...])."""
     o_parts, lse_parts = _f64(o_parts), _f64(lse_parts)

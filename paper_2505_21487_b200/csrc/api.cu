@@ -449,6 +449,44 @@ glad_status glad_splitkv_combine(const float* o_part, const float* lse_part, int
   return GLAD_OK;
 }
 
+glad_status glad_gla_absorb_query(const void* q_nope, const void* q_pe, const void* w_uk, const int32_t* seqlens,
+                                  int32_t B, int32_t Lq, int32_t H, int32_t d_h, int32_t d_c, int32_t d_rope,
+                                  float rope_base, void* q_out, void* stream) {
+  if (B < 0 || Lq < 1 || H < 1 || d_rope < 2 || d_rope % 2 || !(rope_base > 1.f))
+    return fail(GLAD_ERR_INVALID_ARG, "absorb B=%d Lq=%d H=%d d_rope=%d base=%g invalid", B, Lq, H, d_rope, rope_base);
+  if (!glad::absorb_supported(d_h, d_c))
+    return fail(GLAD_ERR_UNSUPPORTED, "absorb: no kernel for d_h=%d d_c=%d", d_h, d_c);
+  if (B == 0) return GLAD_OK;
+  if (!q_nope || !q_pe || !w_uk || !seqlens || !q_out) return fail(GLAD_ERR_INVALID_ARG, "NULL pointer");
+  if (!aligned16(q_nope) || !aligned16(w_uk) || (reinterpret_cast<uintptr_t>(q_out) & 3u) ||
+      (reinterpret_cast<uintptr_t>(q_pe) & 3u))
+    return fail(GLAD_ERR_INVALID_ARG, "q_nope / w_uk must be 16-byte aligned, q_pe / q_out 4-byte aligned");
+  cudaError_t e = glad::launch_absorb_query(q_nope, q_pe, w_uk, seqlens, B, Lq, H, d_h, d_c, d_rope, rope_base, q_out,
+                                            static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return fail(GLAD_ERR_CUDA, "absorb launch failed: %s", cudaGetErrorString(e));
+  return GLAD_OK;
+}
+
+glad_status glad_cache_append_rope(const glad_cache_layout* layout, void* pool, const int32_t* block_table,
+                                   int32_t bt_stride, const int32_t* seqlens_before, const void* latent,
+                                   const void* k_pe, int32_t B, int32_t n_new, float rope_base, void* stream) {
+  glad_status st = check_layout(layout);
+  if (st != GLAD_OK) return st;
+  if (B < 0 || n_new < 0 || bt_stride < 1 || !(rope_base > 1.f))
+    return fail(GLAD_ERR_INVALID_ARG, "append_rope B=%d n_new=%d bt_stride=%d invalid", B, n_new, bt_stride);
+  if (layout->d_rope % 2) return fail(GLAD_ERR_INVALID_ARG, "d_rope=%d must be even", layout->d_rope);
+  if (B == 0 || n_new == 0) return GLAD_OK;
+  if (!pool || !block_table || !seqlens_before || !latent || !k_pe) return fail(GLAD_ERR_INVALID_ARG, "NULL pointer");
+  const int w_lat = layout->n_heads_kv * layout->d_head;
+  if (w_lat % 8 || !aligned16(pool) || !aligned16(latent) || (reinterpret_cast<uintptr_t>(k_pe) & 3u))
+    return fail(GLAD_ERR_INVALID_ARG, "latent width %% 8, pool / latent 16-byte and k_pe 4-byte alignment required");
+  cudaError_t e = glad::launch_append_rope(pool, layout->row_stride, layout->page_size, block_table, bt_stride,
+                                           seqlens_before, latent, k_pe, B, n_new, w_lat, layout->d_rope, rope_base,
+                                           static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return fail(GLAD_ERR_CUDA, "append_rope launch failed: %s", cudaGetErrorString(e));
+  return GLAD_OK;
+}
+
 glad_status glad_seq_split_rescale(const float* lse_all, int32_t P, int32_t rank, const void* o, int64_t rows,
                                    int32_t d_v, void* o_out, float* lse_out, void* stream) {
   if (P < 1 || rank < 0 || rank >= P || rows < 0 || d_v < 8 || d_v % 8)

@@ -37,6 +37,14 @@ cudaError_t launch_append(void* pool, int64_t row_stride, int page_size, const i
 cudaError_t launch_gather(const void* pool, int64_t row_stride, int page_size, const int32_t* block_table,
                           int32_t bt_stride, const int32_t* seqlens, int32_t B, int32_t max_len, int32_t width,
                           void* dense_out, cudaStream_t stream);
+bool absorb_supported(int d_h, int d_c);
+cudaError_t launch_absorb_query(const void* q_nope, const void* q_pe, const void* w_uk, const int32_t* seqlens,
+                                int32_t B, int32_t Lq, int32_t H, int32_t d_h, int32_t d_c, int32_t d_R,
+                                float rope_base, void* q_out, cudaStream_t stream);
+cudaError_t launch_append_rope(void* pool, int64_t row_stride, int page_size, const int32_t* block_table,
+                               int32_t bt_stride, const int32_t* seqlens_before, const void* latent,
+                               const void* k_pe, int32_t B, int32_t n_new, int32_t w_lat, int32_t d_R,
+                               float rope_base, cudaStream_t stream);
 cudaError_t launch_lse_rescale(const float* lse_all, int32_t P, int32_t rank, const void* o, int64_t rows,
                                int32_t d_v, void* o_out, float* lse_out, cudaStream_t stream);
 cudaError_t launch_combine(const float* o_part, const float* lse_part, int32_t S, int64_t rows, int32_t d_v,

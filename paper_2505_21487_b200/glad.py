@@ -73,6 +73,9 @@ def _sig(lib):
         "glad_tp_duplication": ([ctypes.c_int32] * 3, ctypes.c_int32),
         "glad_tp_shard": ([ctypes.c_int32] * 4 + [_I32P] * 4, S),
         "glad_seq_split_range": ([ctypes.c_int32] * 5 + [_I32P] * 2, S),
+        "glad_gla_absorb_query": ([_VP, _VP, _VP, _VP] + [ctypes.c_int32] * 6 + [ctypes.c_float, _VP, _VP], S),
+        "glad_cache_append_rope": ([L, _VP, _VP, ctypes.c_int32, _VP, _VP, _VP, ctypes.c_int32, ctypes.c_int32,
+                                    ctypes.c_float, _VP], S),
         "glad_seq_split_rescale": ([_VP, ctypes.c_int32, ctypes.c_int32, _VP, ctypes.c_int64, ctypes.c_int32, _VP, _VP,
                                     _VP], S),
         "glad_kv_bytes_per_token_per_device": ([ctypes.c_int32] * 6, ctypes.c_int64),
@@ -99,7 +102,7 @@ def exported_symbols():
     return ["glad_last_error", "glad_version", "glad_debug_set_trace", "glad_debug_set_phase_mask", "glad_debug_set_tile", "glad_pool_bytes", "glad_cache_append", "glad_paged_gather",
             "glad_decode_workspace_bytes", "glad_gla_decode", "glad_mla_decode",
             "glad_gta_decode", "glad_splitkv_combine", "glad_tp_duplication", "glad_tp_shard",
-            "glad_seq_split_range", "glad_seq_split_rescale",
+            "glad_seq_split_range", "glad_seq_split_rescale", "glad_gla_absorb_query", "glad_cache_append_rope",
             "glad_kv_bytes_per_token_per_device"]
 
 
@@ -230,6 +233,29 @@ def tp_shard(h_q, n_kv_heads, N, rank):
     vals = [ctypes.c_int32() for _ in range(4)]
     _check(lib().glad_tp_shard(h_q, n_kv_heads, N, rank, *[ctypes.byref(v) for v in vals]))
     return tuple(v.value for v in vals)
+
+
+def gla_absorb_query(q_nope, q_pe, w_uk, seqlens, rope_base=10000.0, out=None, stream=None):
+    """q_nope [B,Lq,H,d_h], q_pe [B,Lq,H,d_R], w_uk [H,d_c,d_h] (bf16, device), seqlens [B] int32 ->
+    q [B,Lq,H,d_c+d_R] bf16 for gla_decode / mla_decode (glad_gla_absorb_query)."""
+    B, Lq, H, d_h = q_nope.shape
+    d_R = q_pe.shape[-1]
+    d_c = w_uk.shape[1]
+    for t in (q_nope, q_pe, w_uk):
+        assert t.dtype == torch.bfloat16 and t.is_contiguous()
+    out = torch.empty((B, Lq, H, d_c + d_R), dtype=torch.bfloat16, device=q_nope.device) if out is None else out
+    _check(lib().glad_gla_absorb_query(q_nope.data_ptr(), q_pe.data_ptr(), w_uk.data_ptr(), seqlens.data_ptr(), B, Lq,
+                                       H, d_h, d_c, d_R, float(rope_base), out.data_ptr(), _stream(stream)))
+    return out
+
+
+def cache_append_rope(layout, pool, block_table, seqlens_before, latent, k_pe, rope_base=10000.0, stream=None):
+    """Append [latent || RoPE(k_pe, p)] rows (glad_cache_append_rope); latent [B,n,h*d], k_pe [B,n,d_R] bf16."""
+    B, n = latent.shape[:2]
+    assert latent.dtype == torch.bfloat16 and latent.is_contiguous() and k_pe.is_contiguous()
+    _check(lib().glad_cache_append_rope(ctypes.byref(layout), pool.data_ptr(), block_table.data_ptr(),
+                                        block_table.shape[-1], seqlens_before.data_ptr(), latent.data_ptr(),
+                                        k_pe.data_ptr(), B, n, float(rope_base), _stream(stream)))
 
 
 def seq_split_range(L, page_size, Lq, P, rank):

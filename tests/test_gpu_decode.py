@@ -410,3 +410,83 @@ def test_seq_split_emulated(P, Lq, page):
     torch.cuda.synchronize()
     o_ref, lse_ref = OA.latent_decode(f64(q), f64(c), f64(kr), sl, scale, causal=True)
     check(acc, lse_m, o_ref, lse_ref, what=f"seq split P={P} Lq={Lq}")
+
+
+# ------------------------------------------------ upstream step (§8(f)-3)
+@pytest.mark.parametrize("B,Lq,H,h_c,d_c,d_R,d_h", [(3, 2, 32, 2, 256, 64, 128), (2, 1, 16, 1, 512, 64, 128),
+                                                  (5, 4, 128, 2, 256, 64, 128), (2, 3, 8, 2, 128, 32, 64)])
+def test_absorb_query_vs_oracle(B, Lq, H, h_c, d_c, d_R, d_h):
+    """glad_gla_absorb_query (W_UK absorption with mma.sync + RoPE of q_pe at
+    p = L - Lq + t) vs the fp64 oracle: bf16 output, fp32 accumulation."""
+    sl = np.array([900 + 37 * b for b in range(B)])
+    x = synth.gla_method_inputs(B, Lq, H, h_c, d_c, d_R, d_h, 8, seed=B + Lq)
+    w = x["W_UK"]  # [H, d_c, d_h]
+    q = glad.gla_absorb_query(x["q_nope"].to(DEV), x["q_pe"].to(DEV), w.contiguous().to(DEV),
+                              torch.from_numpy(sl.astype(np.int32)).to(DEV))
+    torch.cuda.synchronize()
+    ref = OA.absorb_query(f64(x["q_nope"]), f64(x["q_pe"]), f64(w), sl, Lq)
+    got = q.double().cpu().numpy()
+    rel = np.linalg.norm(got - ref) / np.linalg.norm(ref)
+    assert rel <= 5e-3, rel
+    # absorbed part: one bf16 rounding (half ulp, 2^-8 relative) of the fp32
+    # dot product (fp32 accumulation error << 1e-4 at d_h <= 128)
+    a = ref[..., :d_c]
+    assert np.all(np.abs(got[..., :d_c] - a) <= np.abs(a) * 2.0 ** -8 + 1e-4)
+    # RoPE part: within one bf16 rounding of the fp64 value
+    r = ref[..., d_c:]
+    assert np.all(np.abs(got[..., d_c:] - r) <= np.abs(r) * 2.0 ** -8 + 1e-30)
+
+
+@pytest.mark.parametrize("page", [1, 16, 64])
+def test_append_rope_vs_oracle(page):
+    """glad_cache_append_rope: latent part bit-exact, RoPE key within one bf16
+    rounding of the fp64 rotation at position seqlens_before + i."""
+    B, n, h_c, d_c, d_R = 3, 5, 2, 256, 64
+    before = np.array([0, 63, 700], dtype=np.int32)
+    after = before + n
+    x = synth.gla_method_inputs(B, 1, 8, h_c, d_c, d_R, 64, n, seed=page)
+    bt, num_pages = synth.block_table(after, page, seed=page)
+    layout = glad.make_layout(num_pages, page, h_c, d_c, d_R)
+    pool = torch.full((num_pages, page, layout.row_stride), float("nan"), dtype=torch.bfloat16, device=DEV)
+    bt_d = torch.from_numpy(bt).to(DEV)
+    glad.cache_append_rope(layout, pool, bt_d, torch.from_numpy(before).to(DEV),
+                           x["c"].reshape(B, n, -1).contiguous().to(DEV), x["k_pe"].contiguous().to(DEV))
+    torch.cuda.synchronize()
+    ref = OA.rope_cache_rows(f64(x["c"]), f64(x["k_pe"]), before)
+    flat = pool.reshape(-1, layout.row_stride).cpu()
+    for b in range(B):
+        for i in range(n):
+            p = int(before[b]) + i
+            row = flat[int(bt[b, p // page]) * page + p % page]
+            assert torch.equal(row[:h_c * d_c], x["c"][b, i].reshape(-1)), (b, i)
+            g = row[h_c * d_c:h_c * d_c + d_R].double().numpy()
+            r = ref[b, i, h_c * d_c:]
+            assert np.all(np.abs(g - r) <= np.abs(r) * 2.0 ** -8 + 1e-30), (b, i)
+
+
+@pytest.mark.parametrize("Lq,page", [(1, 64), (2, 16), (4, 1)])
+def test_fused_upstream_end_to_end_unabsorbed(Lq, page):
+    """Raw model tensors -> glad_cache_append_rope + glad_gla_absorb_query ->
+    glad_gla_decode, against the UNabsorbed fp64 definition (per-head K/V
+    up-projection, RoPE, softmax; P:48, P:231)."""
+    B, H, h_c, d_c, d_R, d_h = 2, 128, 2, 256, 64, 128
+    sl = np.array([777, 300])
+    x = synth.gla_method_inputs(B, Lq, H, h_c, d_c, d_R, d_h, int(sl.max()), seed=30 + Lq)
+    bt, num_pages = synth.block_table(sl, page, seed=3)
+    layout = glad.make_layout(num_pages, page, h_c, d_c, d_R)
+    pool = torch.full((num_pages, page, layout.row_stride), float("nan"), dtype=torch.bfloat16, device=DEV)
+    bt_d = torch.from_numpy(bt).to(DEV)
+    zero = torch.zeros(1, dtype=torch.int32, device=DEV)
+    for b in range(B):
+        L = int(sl[b])
+        glad.cache_append_rope(layout, pool, bt_d[b:b + 1].contiguous(), zero,
+                               x["c"][b:b + 1, :L].reshape(1, L, -1).contiguous().to(DEV),
+                               x["k_pe"][b:b + 1, :L].contiguous().to(DEV))
+    sl_d = torch.from_numpy(sl.astype(np.int32)).to(DEV)
+    q = glad.gla_absorb_query(x["q_nope"].to(DEV), x["q_pe"].to(DEV), x["W_UK"].contiguous().to(DEV), sl_d)
+    scale = 1.0 / math.sqrt(d_h + d_R)
+    out, lse = glad.gla_decode(q, pool, layout, bt_d, sl_d, scale)
+    torch.cuda.synchronize()
+    _, o_lat, lse_u = OA.gla_unabsorbed(f64(x["q_nope"]), f64(x["q_pe"]), f64(x["c"]), f64(x["k_pe"]),
+                                        f64(x["W_UK"]), f64(x["W_UV"]), sl, scale)
+    check(out, lse, o_lat, lse_u, what=f"fused upstream Lq={Lq} page={page}")

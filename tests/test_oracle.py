@@ -413,3 +413,23 @@ def test_shard_sum_equals_unsharded(h_c, N):
         k0, k1, q0, q1 = SH.tp_shard(H, h_c, N, r)
         g_q = H // h_c
         assert q0 // g_q >= k0 and (q1 - 1) // g_q < k1
+
+
+def test_absorb_query_identity_with_unabsorbed_definition():
+    """Pin of oracle.attention.absorb_query / rope_cache_rows (the upstream
+    step): decoding the absorbed query against the rotated
+    cache rows equals the unabsorbed definition (per-head K/V up-projection,
+    RoPE, softmax; P:48, P:231) in fp64."""
+    import synth
+    from oracle import attention as OA
+    B, Lq, H, h_c, d_c, d_R, d_h = 2, 3, 8, 2, 32, 16, 24
+    sl = np.array([40, 17])
+    x = synth.gla_method_inputs(B, Lq, H, h_c, d_c, d_R, d_h, 40, seed=5)
+    q = OA.absorb_query(x["q_nope"], x["q_pe"], x["W_UK"], sl, Lq)
+    rows = OA.rope_cache_rows(x["c"], x["k_pe"], np.zeros(B))
+    c = rows[..., :h_c * d_c].reshape(B, 40, h_c, d_c)
+    kr = rows[..., h_c * d_c:]
+    o, lse = OA.latent_decode(q, c, kr, sl, 0.3)
+    _, o_lat, lse_u = OA.gla_unabsorbed(x["q_nope"], x["q_pe"], x["c"], x["k_pe"], x["W_UK"], x["W_UV"], sl, 0.3)
+    np.testing.assert_allclose(o, o_lat, atol=1e-12)
+    np.testing.assert_allclose(lse, lse_u, atol=1e-12)
