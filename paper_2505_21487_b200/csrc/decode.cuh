@@ -98,6 +98,9 @@ struct DecodeParams {
 #ifndef GLAD_ROWS_NS_CAP
 #define GLAD_ROWS_NS_CAP 4
 #endif
+#ifndef GLAD_POLY_EVERY
+#define GLAD_POLY_EVERY 0  // every k-th pair of exponentials via exp2_poly2 (0: all on MUFU)
+#endif
 #ifndef GLAD_DBG_NO_TS
 #define GLAD_DBG_NO_TS 0
 #endif
@@ -1135,7 +1138,12 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
 #pragma unroll
           for (int j = 0; j < TH; j += 2) {
             const float2 e = ffma2(make_float2(x[j], x[j + 1]), make_float2(sl2, sl2), make_float2(nm, nm));
-            pk[j / 2] = pack_bf16x2(ex2(e.x), ex2(e.y));
+            if (GLAD_POLY_EVERY && ((j / 2) % GLAD_POLY_EVERY) == GLAD_POLY_EVERY - 1) {
+              const float2 y = exp2_poly2(e);  // part of the exponentials on the FMA pipe
+              pk[j / 2] = pack_bf16x2(y.x, y.y);
+            } else {
+              pk[j / 2] = pack_bf16x2(ex2(e.x), ex2(e.y));
+            }
           }
         };
         exp_pack();
@@ -1353,7 +1361,13 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
             const float2 e1 =
                 ffma2(make_float2(x[n + 2], x[n + 3]), make_float2(sl2, sl2), make_float2(m4.z, m4.w));
             const __nv_bfloat162 v0 = __floats2bfloat162_rn(ex2(e0.x), ex2(e0.y));
-            const __nv_bfloat162 v1 = __floats2bfloat162_rn(ex2(e1.x), ex2(e1.y));
+            __nv_bfloat162 v1;
+            if (GLAD_POLY_EVERY && ((n / 4) % GLAD_POLY_EVERY) == GLAD_POLY_EVERY - 1) {
+              const float2 y = exp2_poly2(e1);  // part of the exponentials on the FMA pipe
+              v1 = __floats2bfloat162_rn(y.x, y.y);
+            } else {
+              v1 = __floats2bfloat162_rn(ex2(e1.x), ex2(e1.y));
+            }
             pk[n / 2] = *reinterpret_cast<const uint32_t*>(&v0);
             pk[n / 2 + 1] = *reinterpret_cast<const uint32_t*>(&v1);
           }

@@ -452,6 +452,28 @@ __device__ __forceinline__ uint64_t globaltimer() {
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t) : : "memory");  // not hoisted across barriers
   return t;
 }
+// 2^x for a pair on the FMA pipe (offloads MUFU.EX2, FA4-style): round to
+// the nearest integer with the 1.5*2^23 magic add, degree-3 fit of 2^f on
+// [-0.5, 0.5] (max relative error 2.8e-4, below bf16's 2^-9 rounding of P),
+// integer part added to the exponent bits.  x < -126 (masked keys, -inf)
+// gives exactly 0.
+__device__ __forceinline__ float2 exp2_poly2(float2 x) {
+  const float2 xc = make_float2(fmaxf(x.x, -127.f), fmaxf(x.y, -127.f));
+  float2 t, r, f, p;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(*reinterpret_cast<unsigned long long*>(&t))
+      : "l"(*reinterpret_cast<const unsigned long long*>(&xc)), "l"(0x4B4000004B400000ull));
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(*reinterpret_cast<unsigned long long*>(&r))
+      : "l"(*reinterpret_cast<const unsigned long long*>(&t)), "l"(0x4B4000004B400000ull));
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(*reinterpret_cast<unsigned long long*>(&f))
+      : "l"(*reinterpret_cast<const unsigned long long*>(&xc)), "l"(*reinterpret_cast<const unsigned long long*>(&r)));
+  p = ffma2(f, make_float2(0.055827971f, 0.055827971f), make_float2(0.241802884f, 0.241802884f));
+  p = ffma2(p, f, make_float2(0.693075671f, 0.693075671f));
+  p = ffma2(p, f, make_float2(0.999971936f, 0.999971936f));
+  float2 y;
+  y.x = x.x < -126.f ? 0.f : __int_as_float(__float_as_int(p.x) + (__float_as_int(t.x) << 23));
+  y.y = x.y < -126.f ? 0.f : __int_as_float(__float_as_int(p.y) + (__float_as_int(t.y) << 23));
+  return y;
+}
 __device__ __forceinline__ float ex2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
