@@ -171,6 +171,9 @@ cudaError_t launch_plan(const int32_t* seqlens, int32_t* plan, int U, int cl_n, 
 // partials of unit entry * cl_n + r (workspace slots (c + entry) * cl_n + r,
 // c = first..last range of the entry) into out / lse.  All other blocks
 // exit at once.
+#ifndef GLAD_MERGE_SPLIT
+#define GLAD_MERGE_SPLIT 2  // blocks per merged unit
+#endif
 constexpr int kMergeThreads = 256;
 constexpr int kMergeMaxParts = 8;  // weights staged per pass
 __global__ void __launch_bounds__(kMergeThreads) merge_split_kernel(
@@ -223,7 +226,7 @@ __global__ void __launch_bounds__(kMergeThreads) merge_split_kernel(
     if (mx != -INFINITY)
       for (int c = cf; c <= cl; ++c) z += __expf(lp[c * sstride + n] - mx);
     const int ng = n0 + n, tq = ng / g_q, h = head * g_q + (ng - tq * g_q);
-    lse[(static_cast<int64_t>(b) * Lq + tq) * H + h] = z > 0.f ? mx + __logf(z) : -INFINITY;
+    if (blockIdx.y == 0) lse[(static_cast<int64_t>(b) * Lq + tq) * H + h] = z > 0.f ? mx + __logf(z) : -INFINITY;
     mx_s[n] = mx;
     iz_s[n] = z > 0.f ? 1.f / z : 0.f;
   }
@@ -232,7 +235,8 @@ __global__ void __launch_bounds__(kMergeThreads) merge_split_kernel(
   const int d4n = d_v / 4;
   const int items = nq * d4n;
   constexpr int kPer = 8;  // items per thread per sweep (loads in flight)
-  for (int base = 0; base < items; base += kMergeThreads * kPer) {
+  // the unit's items are interleaved over gridDim.y blocks (more loads in flight per unit)
+  for (int base = blockIdx.y * kMergeThreads * kPer; base < items; base += gridDim.y * kMergeThreads * kPer) {
     float4 acc[kPer];
 #pragma unroll
     for (int i = 0; i < kPer; ++i) acc[i] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -279,7 +283,7 @@ cudaError_t launch_merge_split(const int32_t* plan, const float* o_part, const f
                                int U, int nq_blk, int n_qblk, int B, int n_heads, int head_groups, int g_q, int Lq,
                                int H, int d_v, void* out, float* lse, cudaStream_t stream) {
   if (G / cl_n < 2) return cudaSuccess;
-  merge_split_kernel<<<(G / cl_n - 1) * cl_n, kMergeThreads, 0, stream>>>(
+  merge_split_kernel<<<dim3((G / cl_n - 1) * cl_n, GLAD_MERGE_SPLIT), kMergeThreads, 0, stream>>>(
       plan, o_part, lse_part, G, cl_n, U, nq_blk, n_qblk, B, n_heads, head_groups, g_q, Lq, H, d_v,
       static_cast<__nv_bfloat16*>(out), lse);
   return cudaGetLastError();
