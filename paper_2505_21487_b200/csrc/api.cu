@@ -158,8 +158,8 @@ glad_status decode_geom(Variant v, const glad_cache_layout* L, int32_t Lq, int32
   return GLAD_OK;
 }
 
-// Workspace of one decode call: [plan (U+1) int32][lse_part (G+U)*NQ f32]
-// [o_part (G+U)*NQ*D_V f32], each 256-byte aligned.
+// Workspace of one decode call: [plan (U+1) int32][lse_part 2G*NQ f32]
+// [o_part 2G*NQ*D_V f32] (two partial slots per CTA range), each 256-byte aligned.
 struct WsLayout {
   size_t plan, lse, opart, total;
 };
@@ -168,8 +168,8 @@ WsLayout ws_layout(int64_t U, int64_t G, int nq, int d_v) {
   WsLayout w;
   w.plan = 0;
   w.lse = al(static_cast<size_t>(U + 1) * 4);
-  w.opart = w.lse + al(static_cast<size_t>(G + U) * nq * 4);
-  w.total = w.opart + al(static_cast<size_t>(G + U) * nq * d_v * 4);
+  w.opart = w.lse + al(static_cast<size_t>(2 * G) * nq * 4);
+  w.total = w.opart + al(static_cast<size_t>(2 * G) * nq * d_v * 4);
   return w;
 }
 

@@ -216,15 +216,17 @@ __global__ void __launch_bounds__(kMergeThreads) merge_split_kernel(
   const int n0 = qb * nq_blk;
   const int nq = min(nq_blk, Lq * g_q - n0);
   if (nq <= 0) return;
-  // slot of range c: (c + pe) * cl_n + rank
-  const float* lp = lse_part + (static_cast<int64_t>(pe) * cl_n + rank) * nq_blk;  // + c * cl_n * nq_blk
-  const int64_t sstride = static_cast<int64_t>(cl_n) * nq_blk;
+  // partial slot of range c (decode epilogue): 2c if the entry is c's first
+  // segment, 2c + 1 if it is its last one (only range cf can have earlier
+  // segments, when its range starts before the entry)
+  const int cf_last = cta_range(cf, GR, total, n_heads, head_groups).t0 < pu0 ? 1 : 0;
+  auto slot_of = [&](int c) -> int64_t { return static_cast<int64_t>(2 * c + (c == cf ? cf_last : 0)) * cl_n + rank; };
   for (int n = threadIdx.x; n < nq; n += kMergeThreads) {
     float mx = -INFINITY;
-    for (int c = cf; c <= cl; ++c) mx = fmaxf(mx, lp[c * sstride + n]);
+    for (int c = cf; c <= cl; ++c) mx = fmaxf(mx, lse_part[slot_of(c) * nq_blk + n]);
     float z = 0.f;
     if (mx != -INFINITY)
-      for (int c = cf; c <= cl; ++c) z += __expf(lp[c * sstride + n] - mx);
+      for (int c = cf; c <= cl; ++c) z += __expf(lse_part[slot_of(c) * nq_blk + n] - mx);
     const int ng = n0 + n, tq = ng / g_q, h = head * g_q + (ng - tq * g_q);
     if (blockIdx.y == 0) lse[(static_cast<int64_t>(b) * Lq + tq) * H + h] = z > 0.f ? mx + __logf(z) : -INFINITY;
     mx_s[n] = mx;
@@ -246,12 +248,12 @@ __global__ void __launch_bounds__(kMergeThreads) merge_split_kernel(
       for (int k = threadIdx.x; k < np * nq; k += kMergeThreads) {
         const int cc = k / nq, n = k - cc * nq;
         const float mx = mx_s[n];
-        w_s[cc][n] = mx == -INFINITY ? 0.f : __expf(lp[(c0 + cc) * sstride + n] - mx) * iz_s[n];
+        w_s[cc][n] = mx == -INFINITY ? 0.f : __expf(lse_part[slot_of(c0 + cc) * nq_blk + n] - mx) * iz_s[n];
       }
       __syncthreads();
       for (int cc = 0; cc < np; ++cc) {
         const float4* src = reinterpret_cast<const float4*>(
-            o_part + ((static_cast<int64_t>(c0 + cc) + pe) * cl_n + rank) * nq_blk * d_v);
+            o_part + slot_of(c0 + cc) * nq_blk * d_v);
         float4 v[kPer];
 #pragma unroll
         for (int i = 0; i < kPer; ++i) {

@@ -26,7 +26,7 @@
 //    seqlens into per-unit tile prefix sums; CTA c walks the flattened tile
 //    range [c*per, (c+1)*per) across units (unit = (b, head, query block)).
 //    A unit finished inside one CTA is written directly; a unit cut by a
-//    range boundary leaves partials (o/l, lse) in workspace slot c + u and
+//    range boundary leaves partials (o/l, lse) in workspace slot 2c or 2c+1 and
 //    the combine kernel merges them (split-KV LSE merge).
 //  * Warp roles (384 threads): w0 TMA producer, w1 UMMA issuer (warp-uniform
 //    scheduler, one elected lane issues), w2-3 Q loader (+ TMEM alloc), w4-7 / w8-11 two
@@ -52,8 +52,8 @@ struct DecodeParams {
   const int32_t* plan;      // [U + 1] exclusive prefix sum of tiles per unit (plan_kernel)
   __nv_bfloat16* out;       // [B, Lq, H, D_V]
   float* lse;               // [B, Lq, H]
-  float* o_part;            // [G + U][NQ][D_V] partials of split units
-  float* lse_part;          // [G + U][NQ]
+  float* o_part;            // [2G][NQ][D_V] partials of split units (first / last segment of a range)
+  float* lse_part;          // [2G][NQ]
   int32_t bt_stride;
   int32_t B, Lq, H, g_q;
   int32_t n_heads_kv;       // heads (latent / tied) in the cache
@@ -1236,7 +1236,9 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
       const int j = it - 1;
       mbar_wait(&pv_done[j & 3], (j >> 2) & 1);
       tc_fence_after();
-      const int slot = (cta / p.cl_n + s.pi) * p.cl_n + cta % p.cl_n;
+      // partial slot: 2 per range — the range's first segment (2c) or its
+      // last one (2c + 1); only those two can be cut by a range boundary
+      const int slot = (2 * (cta / p.cl_n) + (seg == 0 ? 0 : 1)) * p.cl_n + cta % p.cl_n;
       const bool valid = n < s.nq;
       if (valid && wg == 0) {
         const float lse = ls > 0.f ? (m + __log2f(ls)) * 0.69314718055994531f : -INFINITY;
@@ -1501,9 +1503,9 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
       if ((lane & ((1 << col_shift<HC, LANES>()) - 1)) == 0)
         red[(wg * 4 + wq) * 32 + (cb - c0) + ((lane & (LANES - 1)) >> col_shift<HC, LANES>())] = cs;
       named_bar_sync(bar_id, 128);
-      // partial slot of a split unit: (range + plan entry) * cl_n + rank is
-      // unique (both increase together along the tile order)
-      const int slot = (cta / p.cl_n + s.pi) * p.cl_n + cta % p.cl_n;
+      // partial slot: 2 per range — the range's first segment (2c) or its
+      // last one (2c + 1); only those two can be cut by a range boundary
+      const int slot = (2 * (cta / p.cl_n) + (seg == 0 ? 0 : 1)) * p.cl_n + cta % p.cl_n;
       if (r < CW) {  // fold the row sum into alpha_s as 1/l (reused below) and write lse
         const float* rr = red + wg * 128 + r;
         const float ls = (rr[0] + rr[32]) + (rr[64] + rr[96]);

@@ -80,6 +80,9 @@ WORKLOADS = {w.name: w for w in [
     Workload("c4_gta", "gta", 256, 1, 64, 8, 128, 64, 4096, page=64, scale=1 / math.sqrt(128), seed=4,
              description="GTA Llama-style: h_q=64, 8 tied KV heads, d_h=128 half-RoPE, B=256, ctx 4K"),
     _c5(1), _c5(2), _c5(4), _c5(8), _c5(8, "skew"),
+    # prefill in the absorbed form: every prompt token is a query (Lq = L)
+    Workload("c6_prefill_gla2", "gla", 2, 4096, 128, 2, 256, 64, 4096, page=64, scale=1 / math.sqrt(192), seed=6,
+             description="GLA-2 prefill as a full-length causal query: B=2, L=Lq=4096, h_q=128, 2x256 + 64"),
     # page-size ablation (page 1 vs 64 for GLA 2x256+64)
     Workload("c2_gla2_p1", "gla", 128, 1, 128, 2, 256, 64, 8192, page=1, scale=1 / math.sqrt(192), seed=1,
              description="C2 GLA-2 with page size 1 (prefix caching, P:316)"),

@@ -490,3 +490,15 @@ def test_fused_upstream_end_to_end_unabsorbed(Lq, page):
     _, o_lat, lse_u = OA.gla_unabsorbed(f64(x["q_nope"]), f64(x["q_pe"]), f64(x["c"]), f64(x["k_pe"]),
                                         f64(x["W_UK"]), f64(x["W_UV"]), sl, scale)
     check(out, lse, o_lat, lse_u, what=f"fused upstream Lq={Lq} page={page}")
+
+
+# ------------------------------------------- prefill through the same path
+@pytest.mark.parametrize("L,H,h_c,d_c,d_R,page", [(400, 32, 2, 256, 64, 64), (300, 16, 2, 128, 32, 16),
+                                                 (257, 64, 2, 256, 64, 1)])
+def test_prefill_as_full_length_query(L, H, h_c, d_c, d_R, page):
+    """Prefill in the absorbed form: every prompt token is a
+    query (Lq = L, bottom-right causal = plain causal), served by the same
+    decode kernels (rows mode, 128 query rows per CTA).  Against the oracle."""
+    sl = np.array([L, L])
+    out, lse, o_ref, lse_ref = run_latent(2, L, H, h_c, d_c, d_R, sl, page, seed=L)
+    check(out, lse, o_ref, lse_ref, what=f"prefill L={L} H={H}")
