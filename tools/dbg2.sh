@@ -1,3 +1,6 @@
-python -m pytest tests -m gpu -x -q 2>&1 | tail -2
-tools/sweep.sh c2_gla2:0:7 c3_gla2_q2:0:7 c6_prefill_gla2:0:7
-timeout 300 python bench.py --workload c6_prefill_gla2 --steps 5 --warmup 3 --no-cpu-baseline 2>&1 | tail -1 | python -c "import json,sys;d=json.loads(sys.stdin.read());r=d['roofline'];print('prefill', d['ms_per_step'], d['tflops'], r['tensor_frac'])"
+med() { python -c "import sys,statistics;v=[float(x) for x in sys.stdin.read().split(':')[1].split()];print(round(statistics.median(v[3:]),4))"; }
+python -m pytest tests/test_gpu_decode.py -x -q -k "rows or prefill or peaked or c3_full or seq_split or fused" 2>&1 | tail -2
+for w in c3_gla2_q2 c3_gla2_q4 c6_prefill_gla2; do for r in 1 2; do
+ echo -n "new $w "; python tools/abtime.py --workload $w --n 20 | tail -1 | med
+ echo -n "old $w "; GLAD_LIB=$PWD/abtest/libglad_old.so python tools/abtime.py --workload $w --n 20 | tail -1 | med
+done; done
