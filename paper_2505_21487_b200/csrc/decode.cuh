@@ -101,6 +101,9 @@ struct DecodeParams {
 #ifndef GLAD_POLY_EVERY
 #define GLAD_POLY_EVERY 0  // every k-th pair of exponentials via exp2_poly2 (0: all on MUFU)
 #endif
+#ifndef GLAD_ROWS_WG
+#define GLAD_ROWS_WG 2  // rows mode: softmax warpgroups splitting each tile's columns (2: C3 q_len 2 0.203 ms vs 0.213 with 1)
+#endif
 #ifndef GLAD_DBG_NO_TS
 #define GLAD_DBG_NO_TS 0
 #endif
@@ -470,16 +473,16 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
     for (int i = 0; i < NS; ++i) {
       mbar_init(&kv_full[i], p.cp_kv ? (p.q_tma ? 64 : 32) : 1);
       mbar_init(&kv_empty[i], 1);
-      mbar_init(&p_full[i], 8);  // softmax warps
+      mbar_init(&p_full[i], C::ROWS ? 4 * GLAD_ROWS_WG : 8);  // softmax warps
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&s_full[i], 1);
-      mbar_init(&s_empty[i], 8);
-      mbar_init(&o_empty[i], 8);
+      mbar_init(&s_empty[i], C::ROWS ? 4 * GLAD_ROWS_WG : 8);
+      mbar_init(&o_empty[i], C::ROWS ? 4 * GLAD_ROWS_WG : 8);
     }
     for (int i = 0; i < 4; ++i) mbar_init(&pv_done[i], 1);
     for (int i = 0; i < 4; ++i) mbar_init(&cl_empty[i], p.cl_n);
-    mbar_init(qn_full, 8);
+    mbar_init(qn_full, 4 * GLAD_ROWS_WG);
     for (int i = 0; i < 2; ++i) {
       mbar_init(&q_full[i], p.q_tma ? 1 : 64);
       mbar_init(&q_empty[i], 1);
@@ -1054,9 +1057,11 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
     // from the same exchanged values), vote the lazy rescale together
     // (bar.red.or over the pair, barrier 4 + wq) and each keeps a partial
     // row sum, combined in the epilogue.
-    constexpr int TH = T / 2;            // S columns per thread
+    if (warp < 4 + 4 * GLAD_ROWS_WG) {  // softmax warpgroups (the rest idle)
+    constexpr int NWGR = GLAD_ROWS_WG;   // softmax warpgroups (column split)
+    constexpr int TH = T / NWGR;         // S columns per thread
     constexpr int NP = TH / 2;           // bf16 pairs of them (TMEM columns of P)
-    constexpr int DH = C::D_V / 2;       // O columns per thread
+    constexpr int DH = C::D_V / NWGR;    // O columns per thread
     constexpr uint32_t kTrig = 0x4380u;  // bf16 bits of 2^TAU = 256
     static_assert(TAU == 8.f, "kTrig encodes 2^TAU");
     static_assert(TH % 16 == 0 && NP % 8 == 0 && DH % 32 == 0, "rows mode tile split");
@@ -1072,19 +1077,19 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
     // (A operand of the TS-mode QK: lane = row, 2 bf16 per column).  Called
     // once the previous segment's last QK has completed (its S was read).
     auto load_q = [&](const Seg& sq) {
-      constexpr int NV = C::D_KN / 16;  // 16-B vectors of this thread's half row
+      constexpr int NV = C::D_KN / (8 * NWGR);  // 16-B vectors of this thread's part of the row
       uint4 v[NV];
       if (n < sq.nq) {
         const int ng = sq.n0 + n, tq = ng / p.g_q, hq = sq.head * p.g_q + (ng - tq * p.g_q);
         const uint4* src = reinterpret_cast<const uint4*>(
-            p.q + ((static_cast<size_t>(sq.b) * p.Lq + tq) * p.H + hq) * C::DQ + wg * (C::D_KN / 2));
+            p.q + ((static_cast<size_t>(sq.b) * p.Lq + tq) * p.H + hq) * C::DQ + wg * (C::D_KN / NWGR));
 #pragma unroll
         for (int i = 0; i < NV; ++i) v[i] = __ldg(src + i);
       } else {
 #pragma unroll
         for (int i = 0; i < NV; ++i) v[i] = make_uint4(0u, 0u, 0u, 0u);
       }
-      const uint32_t qa = tmem + lane_addr + C::QN_COL + wg * (C::D_KN / 4);
+      const uint32_t qa = tmem + lane_addr + C::QN_COL + wg * (C::D_KN / (2 * NWGR));
 #pragma unroll
       for (int i = 0; i < NV; i += 4) tmem_st16_u32(qa + i * 4, reinterpret_cast<const uint32_t*>(v + i));
       tmem_st_wait();
@@ -1152,13 +1157,16 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
         for (int j = 1; j < NP; ++j) pmax = max_u16x2(pmax, pk[j]);
         const bool need = (tl == s.t0) || ((pmax & 0xffffu) > kTrig) || ((pmax >> 16) > kTrig);
         PH(2);
-        if (named_bar_red_or(pair_bar, 64, need)) {
+        const bool vote = NWGR == 2 ? named_bar_red_or(pair_bar, 64, need) : __any_sync(0xffffffffu, need);
+        if (vote) {
           float mt = x[0];
 #pragma unroll
           for (int j = 1; j < TH; ++j) mt = fmaxf(mt, x[j]);
-          mx_x[wg * 128 + n] = mt;
-          named_bar_sync(pair_bar, 64);
-          mt = fmaxf(mt, mx_x[(wg ^ 1) * 128 + n]);
+          if constexpr (NWGR == 2) {
+            mx_x[wg * 128 + n] = mt;
+            named_bar_sync(pair_bar, 64);
+            mt = fmaxf(mt, mx_x[(wg ^ 1) * 128 + n]);
+          }
           const float mn = fmaxf(m, mt * sl2);
           const float alpha = (mn == -INFINITY) ? 1.f : ex2(m - mn);
           m = mn;
@@ -1203,7 +1211,7 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
         const int p0 = tl * T;
         if (p0 + T > s.kv_end) {  // never-loaded tile rows: zero V (0 * stale smem != NaN)
           const uint32_t stage_base = sbase + (it % NS) * C::STAGE;
-          for (int idx = wg * 128 + n; idx < T * C::NCH_V; idx += 256) {
+          for (int idx = wg * 128 + n; idx < T * C::NCH_V; idx += 128 * NWGR) {
             const int tr = idx / C::NCH_V, ch = idx - tr * C::NCH_V;
             if (p0 + tr >= s.kv_end) {
               const uint32_t a = stage_base + (tr >> 3) * C::LGRP + ch * 1024 + (tr & 7) * 128;
@@ -1229,9 +1237,12 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
       const bool have_n = next_seg(k, u, sn);
       if (have_n) load_q(sn);
       // ---- segment epilogue: O / l, lse (natural log); each WG writes its O half
-      l_x[wg * 128 + n] = l2.x + l2.y;
-      named_bar_sync(pair_bar, 64);
-      const float ls = l_x[n] + l_x[128 + n];  // same order in both WGs
+      float ls = l2.x + l2.y;
+      if constexpr (NWGR == 2) {
+        l_x[wg * 128 + n] = ls;
+        named_bar_sync(pair_bar, 64);
+        ls = l_x[n] + l_x[128 + n];  // same order in both WGs
+      }
       const float inv_l = ls > 0.f ? 1.f / ls : 0.f;
       const int j = it - 1;
       mbar_wait(&pv_done[j & 3], (j >> 2) & 1);
@@ -1272,7 +1283,7 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
           }
         }
       }
-      named_bar_sync(pair_bar, 64);  // l_x read by both WGs before the next segment rewrites it
+      if constexpr (NWGR == 2) named_bar_sync(pair_bar, 64);  // l_x read by both WGs before the next segment rewrites it
       if (trace && threadIdx.x == 128 && it - 1 < kTraceTiles) trace[15 + 12 * (it - 1)] = globaltimer();
       ++seg;
       s = sn;
@@ -1281,6 +1292,7 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
     }
     if (GLAD_SOFTMAX_PHASES && trace && threadIdx.x == 128)
       for (int i = 0; i < 6; ++i) trace[kTraceStride - 14 + i] = static_cast<uint64_t>(ph_acc[i]);
+    }
   } else {
     // ========================= softmax / correction / epilogue =========================
     // Thread -> data: token row tr = 32*wq + lane of S^T (rows >= T carry no
