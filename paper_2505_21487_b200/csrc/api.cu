@@ -202,7 +202,7 @@ glad_status decode_common(Variant v, const void* q, const void* pool, const glad
   // per-tile QK/softmax/PV chain, not by HBM, and the cluster-wide stage
   // handshake lengthens that chain.  Off by default.
   int cl_n = 1;
-  if (g.n_qblk >= 2 && g.n_qblk <= 8 && L->page_size >= 16 && (g_phase_mask & 8) &&
+  if (g.n_qblk >= 2 && g.n_qblk <= 8 && L->page_size >= 16 && (g_phase_mask & 8) && g.key.nq != 128 &&
       (num_ctas == 0 || num_ctas % g.n_qblk == 0)) {
     cl_n = g.n_qblk;
     if (max_clusters(g.key, cl_n) < 1) cl_n = 1;
