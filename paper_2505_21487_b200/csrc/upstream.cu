@@ -25,8 +25,12 @@ namespace {
 __device__ __forceinline__ void rope_pair(float x0, float x1, int pos, int i, int d, double log_base, float& y0,
                                           float& y1) {
   const double theta = exp(-2.0 * i / d * log_base);
+  // reduce mod 2 pi in fp64 first (|angle| <= pi keeps sincos on its fast
+  // path; the large-argument reduction used local memory and dominated)
+  double a = static_cast<double>(pos) * theta;
+  a -= rint(a * 0.15915494309189535) * 6.283185307179586;
   double s, c;
-  sincos(static_cast<double>(pos) * theta, &s, &c);
+  sincos(a, &s, &c);
   y0 = static_cast<float>(x0 * c - x1 * s);
   y1 = static_cast<float>(x0 * s + x1 * c);
 }
@@ -66,6 +70,9 @@ __global__ void __launch_bounds__(kAbsorbThreads) absorb_query_kernel(
   const int DQ = DC + d_R;
   // stage q_nope rows and W_UK[h] (16-B vectors)
   constexpr int VR = DH / 8;
+  // (fully unrolled: all of a thread's 16-B loads are in flight at once —
+  // a rolled load -> st.shared loop paid one memory latency per iteration)
+#pragma unroll
   for (int idx = tid; idx < kRowsPerCta * VR; idx += kAbsorbThreads) {
     const int r = idx / VR, v = idx - r * VR;
     uint4 x = make_uint4(0u, 0u, 0u, 0u);
@@ -73,6 +80,7 @@ __global__ void __launch_bounds__(kAbsorbThreads) absorb_query_kernel(
     *reinterpret_cast<uint4*>(sq + r * LD + v * 8) = x;
   }
   const __nv_bfloat16* wh = w_uk + static_cast<int64_t>(h) * DC * DH;
+#pragma unroll
   for (int idx = tid; idx < DC * VR; idx += kAbsorbThreads) {
     const int c = idx / VR, v = idx - c * VR;
     *reinterpret_cast<uint4*>(sw + c * LD + v * 8) = __ldg(reinterpret_cast<const uint4*>(wh + c * DH) + v);
