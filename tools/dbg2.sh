@@ -1,6 +1,4 @@
-med() { python -c "import sys,statistics;v=[float(x) for x in sys.stdin.read().split(':')[1].split()];print(round(statistics.median(v[3:]),4))"; }
-python -m pytest tests -m gpu -q 2>&1 | tail -2
-for w in c3_gla2_q2 c3_gla2_q4 c6_prefill_gla2; do for r in 1 2; do
- echo -n "wg1 $w "; python tools/abtime.py --workload $w --n 20 | tail -1 | med
- echo -n "wg2 $w "; GLAD_LIB=$PWD/abtest/libglad_wg2.so python tools/abtime.py --workload $w --n 20 | tail -1 | med
-done; done
+for r in 1 2 3; do
+  echo -n "base "; python bench.py --steps 50 --warmup 5 --no-cpu-baseline 2>/dev/null | tail -1 | python -c "import json,sys;d=json.loads(sys.stdin.read());print(round(d['ms_per_step'],4), d['clocks']['sm_mhz'])"
+  echo -n "backoff "; GLAD_LIB=$PWD/abtest/libglad_bo.so python bench.py --steps 50 --warmup 5 --no-cpu-baseline 2>/dev/null | tail -1 | python -c "import json,sys;d=json.loads(sys.stdin.read());print(round(d['ms_per_step'],4), d['clocks']['sm_mhz'])"
+done
