@@ -1,27 +1,37 @@
 """Benchmark: decode attention (GLA-2 / MLA / GTA / GLA-8 TP) on B200.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c2_gla2] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload NAME]
+                    [--shard-of N] [--impl ours|reference]
 
-One "step" = one pass of the whole hot path (split planning is on the host;
-decode kernel + split-KV combine on the device) over one batch of synthetic
-input with the BASELINE.json shape.  Default workload is configs[1] (C2,
-GLA-2 DeepSeek-V3 shape, B=128, ctx 8K, page 64).
+One "step" = one pass of the whole hot path over one batch of synthetic
+input with the BASELINE.json shape: split planning (plan kernel), the decode
+kernel, the split-KV merge kernel (and, for the tensor-parallel workloads,
+the rank's row-parallel o_proj slice + ONE NCCL all-reduce).
 
-N > 1 (torchrun, one process per GPU, NCCL):
-  * c1..c4 workloads: independent decode batches per rank (weak scaling, no
-    data-path collective: the problems are independent).
-  * c5 workloads: GLA-8 latent heads sharded TP=N: rank r runs
-    decode on its h_c/N latent heads and h_q/N query heads, the row-parallel
-    o_proj slice (cuBLAS GEMM via torch) and ONE NCCL all-reduce.
-Timing: W warm-up steps, then K steps bracketed by barrier + synchronize,
-CUDA events on the launching stream, max over ranks.  Rank 0 prints one JSON
-line.
+Default workload: N = 1 -> c2_gla2 (BASELINE configs[1], GLA-2 DeepSeek-V3
+shape, B=128, ctx 8K, page 64).  N > 1 (torchrun, one process per GPU,
+NCCL) -> c5_gla8 latent-head tensor parallelism TP=N (BASELINE configs[4]):
+rank r decodes its h_c/N latent heads and h_q/N query heads from its own pool
+(no cache replication), applies its W^vo slice and joins one all-reduce of
+[B, d_model] bf16; the TP1 problem of the same batch is timed on rank 0 and
+reported as "tp1_base" (the scaling reference).  --workload c5_gla8_tpN at
+N = 1 (or --shard-of N) times one rank's TP-N shard alone (decode + o_proj
+slice, no all-reduce).  The other workloads at N > 1 run as independent
+replicas (weak scaling, no data-path collective).
+
+Timing (task contract): W >= 3 warm-up steps, then exactly K steps, each a
+CUDA-graph replay, bracketed by barrier + synchronize, CUDA events on the
+launching stream, max over ranks.  Per-step events give median/min/max.
+The decode kernel alone is timed the same way from a graph holding only the
+decode launch (phase mask 2, after one plan launch), so roofline.achieved is
+the algorithmic bytes per decode launch / that launch's time.
 """
 
 import argparse
 import json
 import math
 import os
+import platform
 import statistics
 import subprocess
 import sys
@@ -34,6 +44,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "decode attention TB/s & TFLOP/s (% B200 roofline); tokens/s at 1/2/4/8 GPUs"
+D_MODEL = 5120  # C5 o_proj output width (R15)
 
 
 def _peaks():
@@ -41,72 +52,186 @@ def _peaks():
     if os.path.exists(p):
         d = json.load(open(p))
         return dict(hbm=d["hbm_gbs"], bf16=d["bf16_tflops"], bf16_sus=d.get("bf16_tflops_sustained"),
-                    src="measured")
-    return dict(hbm=6650.0, bf16=1590.0, bf16_sus=1400.0, src="fallback")
+                    src="measured (MEASURED_PEAKS.json)")
+    # /opt/skills/guides/B200_PROFILING.md fallback figures
+    return dict(hbm=6650.0, bf16=1590.0, bf16_sus=1400.0, src="fallback (B200_PROFILING.md)")
+
+
+def _cpu_info():
+    model = platform.processor() or ""
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    blas = None
+    try:
+        import threadpoolctl
+        info = threadpoolctl.threadpool_info()
+        blas = {i.get("internal_api", "?"): i.get("num_threads") for i in info}
+    except Exception:
+        pass
+    return {"cpu_count": os.cpu_count(), "cpu_model": model, "blas_threads": blas}
 
 
 # ------------------------------------------------------------- oracle leg
-def oracle_sample(wl, n_seq=1, seed=0, max_seconds=20.0):
-    """Time the fp64 oracle (as it stands) on a bounded sample of `wl`:
-    n_seq whole sequences (all heads, all Lq queries) at the workload's
-    longest length.  Returns (seconds, tokens, description, threads)."""
+def _d_head(wl):
+    """Per-head width of the unabsorbed GLA/MLA problem (q_nope, K, V): 128
+    for the DeepSeek-V3-shaped configs, 64 for C1 (BASELINE.json)."""
+    return 64 if wl.d_c == 128 else 128
+
+
+def oracle_units(wl, sl, n_units, seed):
+    """Sampled (b, kv head) units: the longest sequence first (both ends of
+    the head range), then seeded random ones."""
+    rng = np.random.default_rng(seed)
+    b_long = int(np.argmax(sl))
+    units = [(b_long, 0), (b_long, wl.h_c - 1)]
+    while len(units) < n_units:
+        units.append((int(rng.integers(0, wl.B)), int(rng.integers(0, wl.h_c))))
+    return list(dict.fromkeys(units))[:max(n_units, 1)]
+
+
+def time_oracle_units(wl, sl, units, seed=0, max_seconds=30.0):
+    """Time the UNabsorbed fp64 oracle (oracle.attention.gla_unabsorbed /
+    gta_decode, as it stands) on whole (b, kv head) units of the workload's
+    shape: per-head K/V up-projection of the latent, RoPE, softmax attention
+    for the g_q query heads x Lq queries of the unit.  Returns
+    (seconds, sum of the units' L, units done, raw inputs per unit)."""
+    import synth
+    from oracle import attention as OA
+
+    g_q = wl.H // wl.h_c
+    t0 = time.perf_counter()
+    done, l_sum, raws = 0, 0, []
+    for k, (b, i) in enumerate(units):
+        L = int(sl[b])
+        if wl.variant == "gta":
+            q, kv, kr = synth.gta_kernel_inputs(1, wl.Lq, g_q, 1, wl.d_c, L, seed=seed + k)
+            OA.gta_decode(q, kv, kr, [L], wl.scale, causal=wl.causal)
+            raws.append(None)
+        else:
+            x = synth.gla_method_inputs(1, wl.Lq, g_q, 1, wl.d_c, wl.d_R, _d_head(wl), L, seed=seed + k)
+            OA.gla_unabsorbed(x["q_nope"], x["q_pe"], x["c"], x["k_pe"], x["W_UK"], x["W_UV"], [L], wl.scale,
+                              causal=wl.causal)
+            raws.append(x)
+        done += 1
+        l_sum += L
+        if time.perf_counter() - t0 > max_seconds and done >= 1:
+            break
+    return time.perf_counter() - t0, l_sum, done, raws
+
+
+def parity_units(wl, st, units, seed=0):
+    """Parity of sampled units of the GPU path against the UNabsorbed oracle:
+    raw GLA tensors (q_nope, q_pe, W_UK, W_UV) are drawn for the unit's query
+    heads; the GPU absorbs them (glad_gla_absorb_query) into the bench's query
+    tensor and decodes against the bench's pool; the oracle up-projects the
+    unit's latent rows read back from that pool (with its RoPE key
+    un-rotated by the oracle, which re-rotates it) and runs plain softmax
+    attention.  GTA: the oracle's gta_decode on the same rows (the query's
+    RoPE half and K_RoPE un-rotated by the oracle).  Returns the worst
+    (max_abs, rel_l2, lse_max_abs) over the units."""
     import torch
 
     import synth
     from oracle import attention as OA
+    from oracle import rope as OR
+    from paper_2505_21487_b200 import glad, workloads
 
-    L = wl.L
-    tokens = 0
-    t0 = time.perf_counter()
-    done = 0
-    for s in range(n_seq):
+    dev = st["q"].device
+    g_q = wl.H // wl.h_c
+    layout, pool, bt = st["layout"], st["pool"], st["block_table"]
+    q_mod = st["q"].clone()
+    raws = {}
+    for k, (b, i) in enumerate(units):
+        L = int(st["seqlens_host"][b])
+        if wl.variant != "gta":
+            x = synth.gla_method_inputs(1, wl.Lq, g_q, 1, wl.d_c, wl.d_R, _d_head(wl), 1, seed=seed + 100 + k)
+            qa = glad.gla_absorb_query(x["q_nope"].to(dev), x["q_pe"].to(dev), x["W_UK"].contiguous().to(dev),
+                                       torch.tensor([L], dtype=torch.int32, device=dev))
+            q_mod[b, :, i * g_q:(i + 1) * g_q] = qa[0]
+            raws[(b, i)] = x
+    out = torch.empty_like(st["out"])
+    lse = torch.empty_like(st["lse"])
+    fn = {"gla": glad.gla_decode, "mla": glad.mla_decode, "gta": glad.gta_decode}[wl.variant]
+    fn(q_mod, pool, layout, bt, st["seqlens"], wl.scale, causal=wl.causal, out=out, lse=lse,
+       num_ctas=st["num_ctas"], workspace=st["workspace"])
+    torch.cuda.synchronize(dev)
+    worst = [0.0, 0.0, 0.0]
+    for b, i in units:
+        L = int(st["seqlens_host"][b])
+        pos = torch.arange(L, device=dev)
+        prow = bt[b, pos // layout.page_size].long() * layout.page_size + pos % layout.page_size
+        rows = pool.reshape(-1, layout.row_stride)[prow].double().cpu().numpy()
+        kr_rot = rows[:, wl.h_c * wl.d_c: wl.h_c * wl.d_c + wl.d_R]
+        k_pe = OR.rope_unrotate(kr_rot, np.arange(L))
         if wl.variant == "gta":
-            q, kv, kr = synth.gta_kernel_inputs(1, wl.Lq, wl.H, wl.h_c, wl.d_c, L, seed=seed + s)
-            OA.tied_decode(q, kv, kr, [L], wl.scale, causal=wl.causal)
+            kv = rows[:, i * wl.d_c:(i + 1) * wl.d_c][None, :, None, :]
+            qg = q_mod[b:b + 1, :, i * g_q:(i + 1) * g_q].double().cpu().numpy()
+            half = wl.d_c // 2
+            pos_q = np.array([L - wl.Lq + t for t in range(wl.Lq)], dtype=np.float64)
+            qg[..., half:] = OR.rope_unrotate(qg[..., half:], pos_q[None, :, None])
+            o_ref, lse_ref = OA.gta_decode(qg, kv, k_pe[None], [L], wl.scale, causal=wl.causal)
         else:
-            q, c, kr = synth.latent_kernel_inputs(1, wl.Lq, wl.H, wl.h_c, wl.d_c, wl.d_R, L, seed=seed + s)
-            OA.latent_decode(q, c, kr, [L], wl.scale, causal=wl.causal)
-        tokens += wl.Lq
-        done += 1
-        if time.perf_counter() - t0 > max_seconds:
-            break
-    dt = time.perf_counter() - t0
-    threads = torch.get_num_threads()
-    try:
-        import threadpoolctl
-        info = threadpoolctl.threadpool_info()
-        threads = max([i.get("num_threads", 1) for i in info] + [1])
-    except Exception:
-        pass
-    desc = (f"{done} sequence(s) of ctx {L} x {wl.H} heads x q_len {wl.Lq} ({wl.name} shape), "
-            f"fp64 numpy oracle, tokens/s extrapolates linearly in sum(L)*heads")
-    return dt, tokens, desc, threads
+            x = raws[(b, i)]
+            c = rows[:, i * wl.d_c:(i + 1) * wl.d_c][None, :, None, :]
+            _, o_ref, lse_ref = OA.gla_unabsorbed(x["q_nope"], x["q_pe"], c, k_pe[None], x["W_UK"], x["W_UV"], [L],
+                                                  wl.scale, causal=wl.causal)
+        o_g = out[b:b + 1, :, i * g_q:(i + 1) * g_q].double().cpu().numpy()
+        l_g = lse[b:b + 1, :, i * g_q:(i + 1) * g_q].double().cpu().numpy()
+        fin = np.isfinite(lse_ref)
+        worst[0] = max(worst[0], float(np.abs(o_g - o_ref).max()))
+        worst[1] = max(worst[1], float(np.linalg.norm(o_g - o_ref) / max(np.linalg.norm(o_ref), 1e-300)))
+        if fin.any():
+            worst[2] = max(worst[2], float(np.abs(l_g[fin] - lse_ref[fin]).max()))
+    return worst
+
+
+def cpu_baseline(wl, sl, n_units=4, seed=0, max_seconds=20.0):
+    """The oracle on the host cores, extrapolated to the whole step: work is
+    linear in sum(L_b) x kv heads, so seconds per step = (time / sum of the
+    sampled units' L) x sum_b L_b x h_c."""
+    units = oracle_units(wl, sl, n_units, seed)
+    dt, l_sum, done, _ = time_oracle_units(wl, sl, units, seed=seed, max_seconds=max_seconds)
+    step_s = dt / l_sum * float(np.sum(sl, dtype=np.int64)) * wl.h_c
+    value = wl.B * wl.Lq / step_s
+    info = _cpu_info()
+    threads = info["blas_threads"]
+    cores = max(threads.values()) if threads else (os.cpu_count() or 1)
+    desc = (f"UNabsorbed fp64 numpy oracle (gla_unabsorbed / gta_decode) on {done} sampled (sequence, kv head) "
+            f"units of {wl.name} incl. the longest sequence (sum L = {l_sum}, {dt:.1f} s), extrapolated "
+            f"linearly in sum(L) x heads to the whole step ({step_s:.1f} s)")
+    return {"value": value, "unit": "tokens/s", "cores": cores, "kind": "oracle", "sample": desc,
+            "extrapolated": True, "units": units[:done], "seconds": dt, "step_seconds": step_s, **info}
 
 
 def run_reference(args, rank):
-    """--impl reference: the oracle on the host cores, same metric/unit."""
+    """--impl reference: the oracle on the host cores (rank 0 only), on the
+    same workload, metric and unit as our arm; each step is a bounded sample
+    of the workload (sampled units, extrapolated to the whole step)."""
     from paper_2505_21487_b200 import workloads
 
     if rank != 0:
         return
-    wl = workloads.get(args.workload)
-    for _ in range(args.warmup):
-        oracle_sample(wl, 1, seed=99, max_seconds=5.0)
-    t_total, tok_total = 0.0, 0
-    desc, threads = "", 1
+    wl = workloads.get(_workload_name(args, 1))
+    sl = wl.seqlens()
+    for k in range(args.warmup):
+        time_oracle_units(wl, sl, oracle_units(wl, sl, 1, 99 + k), seed=99, max_seconds=3.0)
+    vals, secs = [], []
+    last = None
     for k in range(args.steps):
-        dt, tok, desc, threads = oracle_sample(wl, 1, seed=k, max_seconds=30.0)
-        t_total += dt
-        tok_total += tok
-    # a sampled sequence is at the max length; scale to the workload's mean length
-    mean_L = float(np.mean(wl.seqlens()))
-    value = tok_total / t_total * (wl.L / mean_L)
+        last = cpu_baseline(wl, sl, n_units=2, seed=k, max_seconds=8.0)
+        vals.append(last["value"])
+        secs.append(last["step_seconds"])
+    value = float(statistics.median(vals))
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t_total / args.steps,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * float(statistics.median(secs)),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": {"workload": wl.name, "B": wl.B, "q_len": wl.Lq, "H": wl.H},
-            "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": threads, "kind": "oracle",
-                             "sample": desc},
+            "cpu_baseline": {k: v for k, v in last.items() if k != "units"} | {"value": value},
             "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -133,7 +258,7 @@ class ClockSampler:
                     self.samples.append([x.strip() for x in out.split(",")])
             except Exception:
                 pass
-            self._stop.wait(0.1)
+            self._stop.wait(0.05)
 
     def __enter__(self):
         self._t.start()
@@ -157,11 +282,75 @@ class ClockSampler:
 
 # ------------------------------------------------------------- our arm
 def _traffic(workload):
+    """ncu dram__bytes_read.sum + dram__bytes_write.sum of one decode launch,
+    from the committed `ncu --set full` capture (not measured in this run)."""
     p = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(p):
         d = json.load(open(p))
-        return d.get(workload)
-    return None
+        v = d.get(workload)
+        if isinstance(v, dict):
+            return v.get("bytes"), v.get("source")
+        if v is not None:
+            return v, "profiles/traffic.json"
+    return None, None
+
+
+def _workload_name(args, world):
+    name = args.workload or ("c5_gla8" if world > 1 else "c2_gla2")
+    if name.startswith("c5_gla8"):
+        skew = name.endswith("_skew")
+        tp_n = world
+        if world == 1:
+            tp_n = args.shard_of or 1
+            for n in (1, 2, 4, 8):
+                if f"_tp{n}" in name:
+                    tp_n = args.shard_of or n
+        elif args.shard_of and args.shard_of != world:
+            raise SystemExit(f"--shard-of {args.shard_of} != world size {world}")
+        name = f"c5_gla8_tp{tp_n}" + ("_skew" if skew else "")
+    return name
+
+
+def _events_time(stream, fn, K, world, dev):
+    """K calls of fn bracketed by barrier + synchronize; per-call events.
+    Returns (ms per step over the whole region (max over ranks), per-step ms list)."""
+    import torch
+    import torch.distributed as dist
+
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(K + 1)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    ev[0].record(stream)
+    for k in range(K):
+        fn()
+        ev[k + 1].record(stream)
+    torch.cuda.synchronize(dev)
+    per = [ev[k].elapsed_time(ev[k + 1]) for k in range(K)]
+    ms = ev[0].elapsed_time(ev[K]) / K
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    return ms, per
+
+
+def _capture(dev, stream, fn):
+    import torch
+
+    g = torch.cuda.CUDAGraph()
+    s2 = torch.cuda.Stream(dev)
+    s2.wait_stream(stream)
+    with torch.cuda.stream(s2):
+        with torch.cuda.graph(g, stream=s2):
+            fn(s2)
+    stream.wait_stream(s2)
+    return g
+
+
+def _stats(per):
+    return {"median": float(statistics.median(per)), "min": float(min(per)), "max": float(max(per)),
+            "n": len(per)}
 
 
 def run_ours(args, rank, world, local_rank):
@@ -172,11 +361,9 @@ def run_ours(args, rank, world, local_rank):
 
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
-    name = args.workload
+    name = _workload_name(args, world)
     is_tp = name.startswith("c5")
-    if is_tp:
-        base = name.replace("_tp1", "").replace("_tp2", "").replace("_tp4", "").replace("_tp8", "")
-        name = base.replace("c5_gla8", f"c5_gla8_tp{world}")
+    allreduce = is_tp and world > 1
     wl = workloads.get(name)
     if args.tile:
         glad.debug_set_tile(args.tile)
@@ -186,79 +373,54 @@ def run_ours(args, rank, world, local_rank):
 
     o_proj = None
     if is_tp:  # row-parallel o_proj slice W_r^vo [H_loc*d_c, d_model], d_model 5120 (R15)
-        d_model = 5120
         g = torch.Generator(device=dev).manual_seed(1234 + rank)
-        w_vo = (torch.randn(wl.H * wl.d_c, d_model, generator=g, device=dev) / math.sqrt(wl.H * wl.d_c)).to(
+        w_vo = (torch.randn(wl.H * wl.d_c, D_MODEL, generator=g, device=dev) / math.sqrt(wl.H * wl.d_c)).to(
             torch.bfloat16)
-        y = torch.empty(wl.B * wl.Lq, d_model, dtype=torch.bfloat16, device=dev)
+        y = torch.empty(wl.B * wl.Lq, D_MODEL, dtype=torch.bfloat16, device=dev)
         o_proj = (w_vo, y)
 
-    def step():
-        out, _ = workloads.run(wl, st, stream=stream)
+    def step(s=None):
+        out, _ = workloads.run(wl, st, stream=s)
         if o_proj is not None:  # row-parallel W^vo slice + one all-reduce
             w_vo, y = o_proj
             tp.oproj_allreduce(out.view(wl.B * wl.Lq, wl.H, wl.d_v), w_vo, out=y)
         return out
 
     for _ in range(max(3, args.warmup)):
-        step()
+        step(stream)
     torch.cuda.synchronize(dev)
 
     # CUDA graph of one step (host argument marshalling and TMA descriptor
-    # encoding happen once at capture; replay is launch-overhead free).
-    graph = None
-    if not is_tp:
-        try:
-            g = torch.cuda.CUDAGraph()
-            s2 = torch.cuda.Stream(dev)
-            s2.wait_stream(stream)
-            with torch.cuda.stream(s2):
-                with torch.cuda.graph(g, stream=s2):
-                    workloads.run(wl, st, stream=s2)
-            stream.wait_stream(s2)
-            graph = g
-            for _ in range(3):
-                graph.replay()
-            torch.cuda.synchronize(dev)
-        except Exception as e:  # eager launches still time the same kernels
-            print(f"[bench] graph capture failed ({e}); timing eager launches", file=sys.stderr)
-            graph = None
+    # encoding happen once at capture; replay is launch-overhead free).  The
+    # NCCL all-reduce of the TP step is captured with it.
+    graph = _capture(dev, stream, step)
+    for _ in range(3):
+        graph.replay()
+    torch.cuda.synchronize(dev)
 
-    def timed(fn, K):
-        if world > 1:
-            dist.barrier()
-        torch.cuda.synchronize(dev)
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        for _ in range(K):
-            fn()
-        e1.record(stream)
-        torch.cuda.synchronize(dev)
-        ms = e0.elapsed_time(e1) / K
-        if world > 1:
-            t = torch.tensor([ms], device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ms = float(t.item())
-        return ms
-
-    run_step = graph.replay if graph is not None else step
     with ClockSampler(local_rank) as clk:
         t_end = time.perf_counter() + 1.0
         while time.perf_counter() < t_end:  # soak: clocks settle under load
             for _ in range(20):
-                run_step()
+                graph.replay()
             torch.cuda.synchronize(dev)
-        ms = timed(run_step, args.steps)
+        ms, per_step = _events_time(stream, graph.replay, args.steps, world, dev)
     clocks = clk.summary()
 
-    # plan + merge kernels alone (same plan/partials) -> decode kernel share of the step
-    glad.debug_set_phase_mask(1 | 4)
-    aux_step = lambda: workloads.run(wl, st, stream=stream)
-    aux_step()
-    aux_ms = timed(aux_step, args.steps)
-    glad.debug_set_phase_mask(7)
-    decode_ms = max(ms - aux_ms, 1e-9)
+    # ---- the decode kernel alone: a graph holding only the decode launch
+    # (phase mask 2) over the plan written by one plan launch; >= 50 replays
+    glad.debug_set_phase_mask(1)
+    workloads.run(wl, st, stream=stream)
+    glad.debug_set_phase_mask(2)
+    try:
+        dgraph = _capture(dev, stream, lambda s: workloads.run(wl, st, stream=s))
+    finally:
+        glad.debug_set_phase_mask(7)
+    for _ in range(3):
+        dgraph.replay()
+    n_dec = max(50, args.steps)
+    decode_ms, per_dec = _events_time(stream, dgraph.replay, n_dec, world, dev)
+    decode_med = float(statistics.median(per_dec))
 
     # ---- end to end through the public API with host buffers ----
     pinned_q = st["q"].cpu().pin_memory()
@@ -266,6 +428,7 @@ def run_ours(args, rank, world, local_rank):
         torch.bfloat16).pin_memory()
     out_h = torch.empty(wl.B, wl.Lq, wl.H, wl.d_v, dtype=torch.bfloat16).pin_memory()
     lse_h = torch.empty(wl.B, wl.Lq, wl.H, dtype=torch.float32).pin_memory()
+    y_h = torch.empty(wl.B * wl.Lq, D_MODEL, dtype=torch.bfloat16).pin_memory() if o_proj else None
     q_d = torch.empty_like(st["q"])
     rows_d = torch.empty(wl.B, wl.Lq, wl.width, dtype=torch.bfloat16, device=dev)
     before = (st["seqlens"] - wl.Lq).clamp_min(0).to(torch.int32)
@@ -278,61 +441,120 @@ def run_ours(args, rank, world, local_rank):
         if o_proj is not None:
             w_vo, y = o_proj
             tp.oproj_allreduce(out.view(wl.B * wl.Lq, wl.H, wl.d_v), w_vo, out=y)
+            y_h.copy_(y, non_blocking=True)
         out_h.copy_(out, non_blocking=True)
         lse_h.copy_(lse, non_blocking=True)
 
     for _ in range(3):
         e2e_step()
-    e2e_ms = timed(e2e_step, args.steps)
+    e2e_ms, per_e2e = _events_time(stream, e2e_step, args.steps, world, dev)
     h2d = pinned_q.numel() * 2 + new_rows.numel() * 2
-    d2h = out_h.numel() * 2 + lse_h.numel() * 4
+    d2h = out_h.numel() * 2 + lse_h.numel() * 4 + (y_h.numel() * 2 if y_h is not None else 0)
 
     tokens_per_rank = wl.B * wl.Lq
-    total_tokens = tokens_per_rank if is_tp else tokens_per_rank * world
+    total_tokens = tokens_per_rank if allreduce else tokens_per_rank * world
     value = total_tokens / (ms * 1e-3)
     abytes = workloads.algorithmic_bytes(wl, sl)
     aflops = workloads.algorithmic_flops(wl, sl)
     pk = _peaks()
-    gbs = abytes / (decode_ms * 1e-3) / 1e9
-    tfs = aflops / (decode_ms * 1e-3) / 1e12
+    gbs = abytes / (decode_med * 1e-3) / 1e9
+    tfs = aflops / (decode_med * 1e-3) / 1e12
     hbm_frac = gbs / pk["hbm"]
     ten_frac = tfs / pk["bf16"]
     bound = "hbm" if aflops / abytes < pk["bf16"] * 1e12 / (pk["hbm"] * 1e9) else "tensor"
+    traffic, traffic_src = _traffic(wl.name)
     roof = {"bound": bound, "achieved": gbs if bound == "hbm" else tfs,
             "peak": pk["hbm"] if bound == "hbm" else pk["bf16"], "unit": "GB/s" if bound == "hbm" else "TFLOP/s",
-            "frac": hbm_frac if bound == "hbm" else ten_frac, "traffic": _traffic(wl.name),
-            "peak_source": pk["src"] + " (MEASURED_PEAKS.json)",
-            "kernel": "glad::decode_kernel", "kernel_ms": decode_ms, "plan_merge_ms": aux_ms,
+            "frac": hbm_frac if bound == "hbm" else ten_frac, "traffic": traffic,
+            "traffic_source": (f"static: ncu --set full capture ({traffic_src}), not measured in this run"
+                               if traffic is not None else None),
+            "peak_source": pk["src"], "kernel": "glad::decode_kernel",
+            "kernel_ms": {**_stats(per_dec), "mean": decode_ms,
+                          "how": "CUDA graph holding only the decode launch (phase mask 2), events per replay"},
             "algorithmic_bytes": abytes, "algorithmic_flops": aflops,
-            "hbm_frac": hbm_frac, "tensor_frac": ten_frac}
-    launches_per_step = 3  # plan, decode, merge
+            "hbm_frac": hbm_frac, "tensor_frac": ten_frac,
+            "step_hbm_frac": abytes / (ms * 1e-3) / 1e9 / pk["hbm"]}
+    launches_per_step = 3  # plan, decode, merge (o_proj = cuBLAS, all-reduce = NCCL)
+
+    base = None
+    if allreduce:  # TP1 of the same batch on one GPU (rank 0): the scaling reference
+        del st, graph, dgraph
+        torch.cuda.empty_cache()
+        if rank == 0:
+            base = _tp1_base(name.replace(f"_tp{world}", "_tp1"), dev, stream, args.steps)
+        dist.barrier()
 
     if rank == 0:
         cpu = None
+        parity = None
         if world == 1 and not args.no_cpu_baseline:
-            dt, tok, desc, threads = oracle_sample(wl, 1, seed=0, max_seconds=20.0)
-            mean_L = float(np.mean(sl))
-            cpu_val = tok / dt * (wl.L / mean_L)
-            cpu = {"value": cpu_val, "unit": "tokens/s", "cores": threads, "kind": "oracle", "sample": desc}
+            units = oracle_units(wl, sl, 4, seed=0)
+            parity = parity_units(wl, st, units, seed=0)
+            cpu = cpu_baseline(wl, sl, n_units=4, seed=0, max_seconds=20.0)
+            cpu["parity_vs_gpu"] = {"units": [list(u) for u in units], "max_abs": parity[0], "rel_l2": parity[1],
+                                    "lse_max_abs": parity[2],
+                                    "pass": parity[0] <= 1e-2 and parity[1] <= 5e-3 and parity[2] <= 1e-2}
+            cpu.pop("units", None)
         line = {
             "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-            "scaling": "strong" if is_tp else "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "warmup": args.warmup, "ms_per_step": ms, "step_ms": _stats(per_step), "higher_is_better": True,
+            "scaling": "strong" if allreduce else "weak", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (seeded N(0,1) bf16 cache and queries, random page permutation)",
             "config": {"workload": wl.name, "desc": wl.description, "B": wl.B, "q_len": wl.Lq, "H": wl.H,
                        "n_kv_heads": wl.h_c, "d_head": wl.d_c, "d_rope": wl.d_R, "ctx_max": wl.L,
-                       "ctx_mean": float(np.mean(sl)), "page": wl.page, "num_ctas": st["num_ctas"] or "num_SMs",
-                       "parallelism": (f"tp{world}" if is_tp else f"dp{world} (independent batches)"),
+                       "ctx_mean": float(np.mean(sl)), "page": wl.page, "num_ctas": st_ctas(args),
+                       "parallelism": (f"tp{world} (latent heads, NCCL all-reduce after o_proj)" if allreduce else
+                                       f"tp shard of {name.split('_tp')[1]}" if is_tp else
+                                       f"dp{world} (independent batches)"),
                        "l2": f"inputs larger than L2 ({abytes / 1e9:.2f} GB algorithmic per step > 126 MB); "
-                             "no flush", "cuda_graph": graph is not None},
+                             "no flush", "cuda_graph": True},
             "tbps": gbs / 1e3, "tflops": tfs,
             "roofline": roof, "cpu_baseline": cpu,
             "e2e": {"value": total_tokens / (e2e_ms * 1e-3), "unit": "tokens/s", "ms_per_step": e2e_ms,
-                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                    "includes": "H2D q + new KV rows (pinned), cache append, plan+decode+merge, D2H out + lse"},
+                    "step_ms": _stats(per_e2e), "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                    "includes": "H2D q + new KV rows (pinned), cache append, plan+decode+merge"
+                                + (", o_proj + all-reduce, D2H y" if o_proj else "") + ", D2H out + lse"},
             "gpu_launches": launches_per_step * args.steps,
             "clocks": clocks,
         }
+        if base is not None:
+            line["tp1_base"] = base
         print(json.dumps(line), flush=True)
+
+
+def st_ctas(args):
+    return args.ctas or "num_SMs"
+
+
+def _tp1_base(name, dev, stream, steps):
+    """Step time of the TP1 problem (all latent heads, whole batch, one GPU:
+    decode + o_proj, no all-reduce), CUDA graph, on this rank's GPU."""
+    import torch
+
+    from paper_2505_21487_b200 import tp, workloads
+
+    wl = workloads.get(name)
+    st = workloads.build_device_state(wl, device=dev)
+    g = torch.Generator(device=dev).manual_seed(1234)
+    w_vo = (torch.randn(wl.H * wl.d_c, D_MODEL, generator=g, device=dev) / math.sqrt(wl.H * wl.d_c)).to(
+        torch.bfloat16)
+    y = torch.empty(wl.B * wl.Lq, D_MODEL, dtype=torch.bfloat16, device=dev)
+
+    def step(s):
+        out, _ = workloads.run(wl, st, stream=s)
+        tp.oproj_allreduce(out.view(wl.B * wl.Lq, wl.H, wl.d_v), w_vo, out=y)
+
+    for _ in range(3):
+        step(stream)
+    graph = _capture(dev, stream, step)
+    for _ in range(3):
+        graph.replay()
+    ms, per = _events_time(stream, graph.replay, max(10, steps), 1, dev)
+    value = wl.B * wl.Lq / (ms * 1e-3)
+    out = {"workload": wl.name, "value": value, "unit": "tokens/s", "ms_per_step": ms, "step_ms": _stats(per)}
+    del st, graph
+    torch.cuda.empty_cache()
+    return out
 
 
 def main():
@@ -340,12 +562,16 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--workload", default="c2_gla2")
+    ap.add_argument("--workload", default=None,
+                    help="default: c2_gla2 at N=1, c5_gla8 (TP=N) at N>1; see paper_2505_21487_b200/workloads.py")
+    ap.add_argument("--shard-of", type=int, default=0,
+                    help="c5 workloads at N=1: time one rank's shard of a TP-N job (decode + o_proj slice)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ctas", type=int, default=0, help="persistent CTA count (0 = one per SM)")
     ap.add_argument("--tile", type=int, default=0, help="debug: force the KV tile height (0 = library choice)")
     args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))

@@ -258,8 +258,10 @@ GLAD_API glad_status glad_seq_split_range(int32_t L, int32_t page_size, int32_t 
  * LSE all-gather merge step of the sequence split (device).  lse_all
  * [P, rows] fp32: every rank's lse of the same rows (gathered by the caller,
  * e.g. NCCL all-gather; -inf for an empty range).  o [rows, d_v] bf16: this
- * rank's normalised partial output.  Writes o_out [rows, d_v] fp32 (a
- * separate buffer; fp32 so the split adds no rounding of its own) =
+ * rank's normalised partial output (the decode's bf16 output: one rounding,
+ * as in the unsplit path).  Writes o_out [rows, d_v] fp32 (a separate
+ * buffer; kept fp32 so the rescale adds no second bf16 rounding: the caller
+ * feeds it to the fp32 o_proj GEMM, see tp.seq_split_oproj_allreduce) =
  * o * exp(lse_all[rank] - lse) with lse = ln sum_p exp(lse_all[p]), and
  * lse_out [rows] (may be NULL).  Summing o_out over the P ranks (e.g. inside
  * the o_proj all-reduce, which is linear) gives the attention output over the

@@ -5,16 +5,11 @@
 
 namespace glad {
 
+// The > 48 KB dynamic shared memory opt-in is a per-device (per-context)
+// function attribute: cached per device ordinal, set on first use on each.
 template <class C>
 cudaError_t set_smem_attr() {
-  static bool attr_set = false;  // benign race: idempotent attribute set
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(decode_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         C::SMEM_BYTES);
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
-  return cudaSuccess;
+  return set_func_smem_once(reinterpret_cast<const void*>(decode_kernel<C>), C::SMEM_BYTES);
 }
 
 template <int DV, int DKN, int DR, int NQ, int T>

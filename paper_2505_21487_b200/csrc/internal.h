@@ -4,10 +4,34 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <map>
+#include <mutex>
 
 #include "decode.cuh"
 
 namespace glad {
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device
+// ordinal): the opt-in is a per-context attribute, so a process that drives
+// several GPUs sets it on each (benign race: the set is idempotent).
+inline cudaError_t set_func_smem_once(const void* func, int bytes) {
+  constexpr int kMaxDev = 64;
+  struct Flags { bool done[kMaxDev] = {}; };
+  static std::mutex mu;
+  static std::map<const void*, Flags> seen;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev < 0 || dev >= kMaxDev) return cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  std::lock_guard<std::mutex> lk(mu);
+  bool& done = seen[func].done[dev];
+  if (!done) {
+    e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (e != cudaSuccess) return e;
+    done = true;
+  }
+  return cudaSuccess;
+}
 
 // Kernel family key: value width, key-from-state width, rope width, query
 // rows per CTA.

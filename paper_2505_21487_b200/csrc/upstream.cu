@@ -160,12 +160,8 @@ cudaError_t launch_absorb_t(const void* q_nope, const void* q_pe, const void* w_
                             int32_t B, int32_t Lq, int32_t H, int32_t d_R, float rope_base, void* q_out,
                             cudaStream_t stream) {
   constexpr int smem = (kRowsPerCta + DC) * (DH + 8) * 2;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(absorb_query_kernel<DH, DC>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  cudaError_t e = set_func_smem_once(reinterpret_cast<const void*>(absorb_query_kernel<DH, DC>), smem);
+  if (e != cudaSuccess) return e;
   const dim3 grid((B * Lq + kRowsPerCta - 1) / kRowsPerCta, H);
   absorb_query_kernel<DH, DC><<<grid, kAbsorbThreads, smem, stream>>>(
       static_cast<const __nv_bfloat16*>(q_nope), static_cast<const __nv_bfloat16*>(q_pe),

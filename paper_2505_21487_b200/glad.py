@@ -192,7 +192,11 @@ def _decode(fn, variant, q, pool, layout, block_table, seqlens, softmax_scale, c
         lse = torch.empty(B, Lq, H, dtype=torch.float32, device=q.device)
     nbytes = workspace_bytes(layout, B, Lq, H, variant, num_ctas)
     if workspace is None:
-        workspace = _default_ws.setdefault(q.device, Workspace(q.device))
+        # one default workspace per (device, stream): decodes in flight on
+        # different streams never share plan / partial slots (concurrent
+        # streams may also pass their own Workspace)
+        key = (q.device, (stream or torch.cuda.current_stream(q.device)).cuda_stream)
+        workspace = _default_ws.setdefault(key, Workspace(q.device))
     ws = workspace.get(nbytes)
     _check(fn(_ptr(q), _ptr(pool), ctypes.byref(layout), _ptr(block_table), block_table.shape[1], _ptr(seqlens),
               B, Lq, H, float(softmax_scale), 1 if causal else 0, _ptr(out), _ptr(lse), _ptr(ws), nbytes,
@@ -238,24 +242,46 @@ def tp_shard(h_q, n_kv_heads, N, rank):
 def gla_absorb_query(q_nope, q_pe, w_uk, seqlens, rope_base=10000.0, out=None, stream=None):
     """q_nope [B,Lq,H,d_h], q_pe [B,Lq,H,d_R], w_uk [H,d_c,d_h] (bf16, device), seqlens [B] int32 ->
     q [B,Lq,H,d_c+d_R] bf16 for gla_decode / mla_decode (glad_gla_absorb_query)."""
+    _need(q_nope, torch.bfloat16, "q_nope"); _need(q_pe, torch.bfloat16, "q_pe")
+    _need(w_uk, torch.bfloat16, "w_uk"); _need(seqlens, torch.int32, "seqlens")
+    if q_nope.dim() != 4 or q_pe.dim() != 4 or w_uk.dim() != 3:
+        raise ValueError("q_nope / q_pe must be [B, Lq, H, d], w_uk [H, d_c, d_h]")
     B, Lq, H, d_h = q_nope.shape
     d_R = q_pe.shape[-1]
     d_c = w_uk.shape[1]
-    for t in (q_nope, q_pe, w_uk):
-        assert t.dtype == torch.bfloat16 and t.is_contiguous()
-    out = torch.empty((B, Lq, H, d_c + d_R), dtype=torch.bfloat16, device=q_nope.device) if out is None else out
-    _check(lib().glad_gla_absorb_query(q_nope.data_ptr(), q_pe.data_ptr(), w_uk.data_ptr(), seqlens.data_ptr(), B, Lq,
-                                       H, d_h, d_c, d_R, float(rope_base), out.data_ptr(), _stream(stream)))
+    if tuple(q_pe.shape[:3]) != (B, Lq, H):
+        raise ValueError(f"q_pe shape {tuple(q_pe.shape)} does not match q_nope {tuple(q_nope.shape)}")
+    if tuple(w_uk.shape) != (H, d_c, d_h):
+        raise ValueError(f"w_uk shape {tuple(w_uk.shape)} != (H, d_c, d_h) = ({H}, {d_c}, {d_h})")
+    if tuple(seqlens.shape) != (B,):
+        raise ValueError(f"seqlens shape {tuple(seqlens.shape)} != ({B},)")
+    if out is None:
+        out = torch.empty((B, Lq, H, d_c + d_R), dtype=torch.bfloat16, device=q_nope.device)
+    _need(out, torch.bfloat16, "out")
+    if tuple(out.shape) != (B, Lq, H, d_c + d_R):
+        raise ValueError(f"out shape {tuple(out.shape)} != {(B, Lq, H, d_c + d_R)}")
+    _check(lib().glad_gla_absorb_query(_ptr(q_nope), _ptr(q_pe), _ptr(w_uk), _ptr(seqlens), B, Lq, H, d_h, d_c,
+                                       d_R, float(rope_base), _ptr(out), _stream(stream)))
     return out
 
 
 def cache_append_rope(layout, pool, block_table, seqlens_before, latent, k_pe, rope_base=10000.0, stream=None):
     """Append [latent || RoPE(k_pe, p)] rows (glad_cache_append_rope); latent [B,n,h*d], k_pe [B,n,d_R] bf16."""
+    _need(pool, torch.bfloat16, "pool"); _need(block_table, torch.int32, "block_table")
+    _need(seqlens_before, torch.int32, "seqlens_before")
+    _need(latent, torch.bfloat16, "latent"); _need(k_pe, torch.bfloat16, "k_pe")
+    if latent.dim() != 3 or k_pe.dim() != 3:
+        raise ValueError("latent must be [B, n, n_heads_kv*d_head], k_pe [B, n, d_rope]")
     B, n = latent.shape[:2]
-    assert latent.dtype == torch.bfloat16 and latent.is_contiguous() and k_pe.is_contiguous()
-    _check(lib().glad_cache_append_rope(ctypes.byref(layout), pool.data_ptr(), block_table.data_ptr(),
-                                        block_table.shape[-1], seqlens_before.data_ptr(), latent.data_ptr(),
-                                        k_pe.data_ptr(), B, n, float(rope_base), _stream(stream)))
+    if latent.shape[-1] != layout.n_heads_kv * layout.d_head:
+        raise ValueError(f"latent width {latent.shape[-1]} != n_heads_kv*d_head = {layout.n_heads_kv * layout.d_head}")
+    if tuple(k_pe.shape) != (B, n, layout.d_rope):
+        raise ValueError(f"k_pe shape {tuple(k_pe.shape)} != {(B, n, layout.d_rope)}")
+    if seqlens_before.numel() != B or block_table.dim() != 2 or block_table.shape[0] < B:
+        raise ValueError("seqlens_before must be [B] and block_table [>= B, max_pages]")
+    _check(lib().glad_cache_append_rope(ctypes.byref(layout), _ptr(pool), _ptr(block_table),
+                                        block_table.shape[-1], _ptr(seqlens_before), _ptr(latent),
+                                        _ptr(k_pe), B, n, float(rope_base), _stream(stream)))
 
 
 def seq_split_range(L, page_size, Lq, P, rank):
@@ -272,8 +298,9 @@ def seq_split_rescale(lse_all, rank, o, out=None, lse_out=None, stream=None):
     P = lse_all.shape[0]
     d_v = o.shape[-1]
     rows = o.numel() // d_v
-    assert lse_all.dtype == torch.float32 and lse_all.is_contiguous() and lse_all[0].numel() == rows
-    assert o.dtype == torch.bfloat16 and o.is_contiguous()
+    _need(lse_all, torch.float32, "lse_all"); _need(o, torch.bfloat16, "o")
+    if lse_all[0].numel() != rows:
+        raise ValueError(f"lse_all rows {lse_all[0].numel()} != o rows {rows}")
     out = torch.empty(o.shape, dtype=torch.float32, device=o.device) if out is None else out
     lse_out = torch.empty(lse_all.shape[1:], dtype=torch.float32, device=o.device) if lse_out is None else lse_out
     _check(lib().glad_seq_split_rescale(lse_all.data_ptr(), P, int(rank), o.data_ptr(), rows, d_v, out.data_ptr(),

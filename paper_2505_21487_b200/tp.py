@@ -66,9 +66,12 @@ def gather_lse(lse_local, group=None):
     sequence-split group; NCCL on GPUs, gloo in the CPU tests)."""
     if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size(group) == 1:
         return lse_local.unsqueeze(0).contiguous()
-    parts = [torch.empty_like(lse_local) for _ in range(dist.get_world_size(group))]
-    dist.all_gather(parts, lse_local.contiguous(), group=group)
-    return torch.stack(parts).contiguous()
+    src = lse_local.contiguous()
+    if src.is_cuda and dist.get_backend(group) == "gloo":  # gloo all-gathers host tensors only
+        src = src.cpu()
+    parts = [torch.empty_like(src) for _ in range(dist.get_world_size(group))]
+    dist.all_gather(parts, src, group=group)
+    return torch.stack(parts).to(lse_local.device).contiguous()
 
 
 def seq_split_oproj_allreduce(o_local, lse_local, w_vo_local, split_group=None, group=None, out=None):
@@ -78,4 +81,10 @@ def seq_split_oproj_allreduce(o_local, lse_local, w_vo_local, split_group=None, 
     lse_all = gather_lse(lse_local, split_group)
     rank = dist.get_rank(split_group) if (dist.is_available() and dist.is_initialized()) else 0
     o_scaled, _ = glad.seq_split_rescale(lse_all, rank, o_local.contiguous())
-    return oproj_allreduce(o_scaled.to(w_vo_local.dtype), w_vo_local, out=out, group=group)
+    # the rescaled partial stays fp32 through the GEMM and the all-reduce:
+    # o is rounded to bf16 once (by the decode), as in the unsplit path
+    y = oproj_allreduce(o_scaled, w_vo_local.to(torch.float32), group=group)
+    if out is not None:
+        out.copy_(y)
+        return out
+    return y

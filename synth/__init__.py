@@ -111,10 +111,19 @@ def gta_kernel_inputs(B, Lq, H, h_kv, d_h, Lmax, seed, q_scale=1.0):
     return q, kv, kr
 
 
-def device_pool(num_pages, page_size, row_stride, seed, device):
+def device_pool(num_pages, page_size, row_stride, seed, device, chunk_bytes=1 << 30):
     """A whole pool of N(0,1) bf16 rows drawn directly on ``device`` (bench
-    sizes; the oracle reads sampled rows back through the block table)."""
-    return normal_bf16((num_pages, page_size, row_stride), seed, device=device)
+    sizes; the oracle reads sampled rows back through the block table).
+    Drawn in ~1 GB fp32 chunks from one seeded generator, so the peak memory
+    is the bf16 pool plus one chunk (the C5 TP1 pool is 53 GB)."""
+    pool = torch.empty((num_pages, page_size, row_stride), dtype=torch.bfloat16, device=device)
+    flat = pool.view(num_pages, -1)
+    per = max(1, chunk_bytes // max(1, 4 * flat.shape[1]))
+    g = _gen(seed, device)
+    for p0 in range(0, num_pages, per):
+        p1 = min(num_pages, p0 + per)
+        flat[p0:p1] = torch.randn(p1 - p0, flat.shape[1], generator=g, device=device, dtype=torch.float32)
+    return pool
 
 
 def device_queries(B, Lq, H, d_qk, seed, device, q_scale=1.0):

@@ -271,16 +271,29 @@ def test_absorbed_equals_unabsorbed(h_c, d_h, Lq):
     np.testing.assert_allclose(up, o_head, atol=1e-12)
 
 
-def test_gla_one_group_is_mla():
-    """GLA(h_c=1, d_c=4 d_h) == MLA: the grouping degenerates — every
-    head maps to latent 0, identical to a per-head loop over one latent."""
-    B, Lq, H, d_c, d_R, L = 1, 2, 4, 16, 4, 7
+@pytest.mark.parametrize("Lq,causal", [(1, True), (2, True), (3, False)])
+def test_mla_is_one_group_vs_sdpa(Lq, causal):
+    """MLA = GLA with one latent head (h_c = 1, d_c = 4 d_h): every
+    query head attends to the same latent + shared RoPE key.  Pinned against
+    torch SDPA (fp64, a library routine) per head, so a wrong head-to-group
+    map at h_c = 1 (e.g. h // g_q off by one) fails here."""
+    B, H, d_h, d_R, L = 2, 6, 4, 4, 15
+    d_c = 4 * d_h
     q, c, kr = (f64(t) for t in synth.latent_kernel_inputs(B, Lq, H, 1, d_c, d_R, L, seed=9))
-    o, lse = A.latent_decode(q, c, kr, [L], 0.3)
-    # the same heads each computed as its own single-head GLA problem
-    for h in range(H):
-        oh, lh = A.latent_decode(q[:, :, h:h + 1], c, kr, [L], 0.3)
-        np.testing.assert_array_equal(oh[:, :, 0], o[:, :, h])
+    sl = [L, 9]
+    o, lse = A.latent_decode(q, c, kr, sl, 0.3, causal=causal)
+    for b in range(B):
+        pos = np.arange(sl[b])
+        K = np.concatenate([c[b, :sl[b], 0], kr[b, :sl[b]]], 1)
+        V = c[b, :sl[b], 0]
+        qt = np.arange(Lq)
+        mask = (pos[None, :] <= (sl[b] - Lq + qt)[:, None]) if causal else np.ones((Lq, sl[b]), bool)
+        for h in range(H):
+            np.testing.assert_allclose(o[b, :, h], _sdpa(q[b, :, h], K, V, 0.3, mask), atol=1e-12)
+            # lse against the log-sum-exp of the masked scores (numpy, fp64)
+            s = 0.3 * (q[b, :, h] @ K.T)
+            s = np.where(mask, s, -np.inf)
+            np.testing.assert_allclose(lse[b, :, h], np.log(np.exp(s).sum(-1)), atol=1e-12)
 
 
 def test_gta_structure_and_gqa_equivalence():
@@ -381,6 +394,19 @@ def test_paging_round_trip_and_invariance(page_size):
         assert np.all(dense[b, sl[b]:] == 0)
 
 
+def test_physical_row_hand_values():
+    """P:304: token j of sequence b lives in page block_table[b][j // page] at
+    offset j % page.  Hand-computed values (not a round trip): pool rows of
+    a 4-token-page table [[3, 0, 2], [1, 4, 5]]."""
+    bt = [[3, 0, 2], [1, 4, 5]]
+    want = {(0, 0): 12, (0, 3): 15, (0, 4): 0, (0, 5): 1, (0, 9): 9, (0, 11): 11,
+            (1, 0): 4, (1, 6): 18, (1, 8): 20, (1, 10): 22}
+    for (b, j), r in want.items():
+        assert PG.physical_row(bt, 4, b, j) == r, (b, j)
+    # page size 1: the block table is the row map itself
+    assert [PG.physical_row([[7, 2, 9]], 1, 0, j) for j in range(3)] == [7, 2, 9]
+
+
 def test_cooperative_offsets_match_naive():
     rng = np.random.default_rng(0)
     for trial in range(200):
@@ -433,3 +459,29 @@ def test_absorb_query_identity_with_unabsorbed_definition():
     _, o_lat, lse_u = OA.gla_unabsorbed(x["q_nope"], x["q_pe"], x["c"], x["k_pe"], x["W_UK"], x["W_UV"], sl, 0.3)
     np.testing.assert_allclose(o, o_lat, atol=1e-12)
     np.testing.assert_allclose(lse, lse_u, atol=1e-12)
+
+
+def test_rope_cache_rows_start_offset():
+    """oracle.attention.rope_cache_rows at start > 0 (the append position of
+    a decode step): (a) appending in chunks at their start offsets equals one
+    bulk append from 0; (b) one row at start s equals the rotation of each
+    pair (x0, x1) as the complex number x0 + i x1 times e^{i s theta_k}
+    (independent complex arithmetic, R5: theta_k = 10000^(-2k/d)); (c) the
+    latent part is copied unchanged."""
+    from oracle import attention as OA
+    rng = np.random.default_rng(11)
+    B, n, h_c, d_c, d_R = 2, 9, 2, 4, 6
+    c = rng.standard_normal((B, n, h_c, d_c))
+    kp = rng.standard_normal((B, n, d_R))
+    bulk = OA.rope_cache_rows(c, kp, np.zeros(B))
+    parts = [OA.rope_cache_rows(c[:, a:e], kp[:, a:e], np.full(B, a)) for a, e in ((0, 2), (2, 3), (3, 9))]
+    np.testing.assert_allclose(np.concatenate(parts, axis=1), bulk, atol=1e-12)
+    start = np.array([5, 1234])
+    rows = OA.rope_cache_rows(c[:, :1], kp[:, :1], start)
+    for b in range(B):
+        z = kp[b, 0, 0::2] + 1j * kp[b, 0, 1::2]
+        th = 10000.0 ** (-2.0 * np.arange(d_R // 2) / d_R)
+        w = z * np.exp(1j * start[b] * th)
+        np.testing.assert_allclose(rows[b, 0, h_c * d_c::2], w.real, atol=1e-12)
+        np.testing.assert_allclose(rows[b, 0, h_c * d_c + 1::2], w.imag, atol=1e-12)
+        np.testing.assert_array_equal(rows[b, 0, :h_c * d_c], c[b, 0].reshape(-1))

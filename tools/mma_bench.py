@@ -6,9 +6,17 @@ import sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch  # noqa: E402
 
-from paper_2505_21487_b200 import glad  # noqa: E402
-
-lib = glad.lib()
+# The microbenchmark kernels are not part of libglad.so: built here into
+# tools/microbench/libmicrobench.so (nvcc, sm_100a) on first use.
+HERE = os.path.dirname(os.path.abspath(__file__))
+SO = os.path.join(HERE, "microbench", "libmicrobench.so")
+if not os.path.exists(SO):
+    import subprocess
+    subprocess.run(["/usr/local/cuda/bin/nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-std=c++17",
+                    "--expt-relaxed-constexpr", "-Xcompiler", "-fPIC", "-shared", "-cudart", "static",
+                    "-I" + os.path.join(os.path.dirname(HERE), "paper_2505_21487_b200", "csrc"),
+                    os.path.join(HERE, "microbench", "microbench.cu"), "-o", SO], check=True)
+lib = ctypes.CDLL(SO)
 lib.glad_debug_mma_bench.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_void_p]
 out = torch.zeros(3, dtype=torch.int64, device="cuda")
 names = {0: "A K-SW128 / B K-SW128 (QK)", 1: "A MN-SW128 / B MN-noswz (PV now)", 2: "A MN-SW128 / B MN-SW128",
