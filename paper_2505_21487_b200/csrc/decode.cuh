@@ -110,6 +110,18 @@ struct DecodeParams {
 #ifndef GLAD_NS_CAP
 #define GLAD_NS_CAP 4
 #endif
+#ifndef GLAD_TRACE
+#define GLAD_TRACE 0
+#endif
+#ifndef GLAD_REGS_SPLIT
+#define GLAD_REGS_SPLIT 0  // measured: warpgroup 0 needs > 100 registers, the split adds spills
+#endif
+#ifndef GLAD_REGS_LOW
+#define GLAD_REGS_LOW 64
+#endif
+#ifndef GLAD_REGS_HIGH
+#define GLAD_REGS_HIGH 224  // 128 x 64 + 256 x 224 = 65536
+#endif
 #ifndef GLAD_MMA_BACKOFF_NS
 #define GLAD_MMA_BACKOFF_NS 0
 #endif
@@ -170,8 +182,8 @@ struct DecodeCfg {
   static constexpr int NWG = 2;
   static constexpr int CW = ROWS ? 32 : NQ / NWG;
   static constexpr int HC = CW;  // columns per softmax thread (one token row)
-  static constexpr int MAXSEG = 128;  // per-CTA segment table entries (aux + 3072)
-  static constexpr int AUX = 3072 + MAXSEG * 16 + T * 4 + (ROWS ? 1024 : 0);  // + cp.async row table (+ rows: row-sum exchange)
+  static constexpr int MAXSEG = 64;  // per-CTA segment table entries (aux + 3072), 32 B each
+  static constexpr int AUX = 3072 + MAXSEG * 32 + T * 4 + (ROWS ? 1024 : 0);  // + cp.async row table (+ rows: row-sum exchange)
   static constexpr int AVAIL = 227 * 1024 - 1024 - AUX;
   // bytes the M = 128 QK may read past the end of the last stage (rows >= T)
   static constexpr int OVER_RAW = ROWS ? 0 : (16 * LGRP > OFF_R + 16384 ? 16 * LGRP : OFF_R + 16384) - STAGE;
@@ -322,15 +334,17 @@ __device__ __forceinline__ void seg_unit(const DecodeParams& p, int pi, int L, S
   }
 }
 
+// (noinline: the on-the-fly path after a segment-table overflow is rare;
+// its ~20 runtime integer divisions stay out of every warp role's code)
 template <int NQ>
-__device__ __forceinline__ Seg make_seg(const DecodeParams& p, int u, int cta_t0, int cta_t1) {
+__device__ __noinline__ void make_seg(const DecodeParams& p, int u, int cta_t0, int cta_t1, Seg* out) {
   Seg s;
   seg_unit<NQ>(p, u, __ldg(p.seqlens + ((u * p.cl_n) / p.n_qblk) % p.B), s);
   const int pu0 = __ldg(p.plan + u), pu1 = __ldg(p.plan + u + 1);
   s.t0 = max(cta_t0, pu0) - pu0;
   s.t1 = min(cta_t1, pu1) - pu0;
   s.whole = (s.t0 == 0 && s.t1 == pu1 - pu0);
-  return s;
+  *out = s;
 }
 
 // Flattened tile range of CTA c (units are head-major).  With head groups,
@@ -367,14 +381,31 @@ __device__ __host__ __forceinline__ int cta_of_tile(int t, int G, int total, int
   return t / per;
 }
 
-// Segment from a table entry (u, t0, t1, L) without global loads.
+// Segment table entry (32 B, built once in the prologue so that no warp role
+// runs the divisions of seg_unit): e0 = (plan entry, t0, t1, L | whole << 30),
+// e1 = (b | head << 20, n0, kv_end, ld_end).
 template <int NQ>
-__device__ __forceinline__ Seg seg_from_entry(const DecodeParams& p, int4 e) {
+__device__ __forceinline__ void seg_to_entry(const Seg& s, int4* dst) {
+  dst[0] = make_int4(s.pi, s.t0, s.t1, s.L | ((s.whole ? 1 : 0) << 30));
+  dst[1] = make_int4(s.b | (s.head << 20), s.n0, s.kv_end, s.ld_end);
+}
+template <int NQ>
+__device__ __forceinline__ Seg seg_from_entry(const DecodeParams& p, const int4* e) {
+  const int4 e0 = e[0], e1 = e[1];
   Seg s;
-  seg_unit<NQ>(p, e.x, e.w & 0x3FFFFFFF, s);
-  s.t0 = e.y;
-  s.t1 = e.z;
-  s.whole = (e.w >> 30) & 1;
+  s.pi = e0.x;
+  s.u = e0.x * p.cl_n + static_cast<int>(blockIdx.x) % p.cl_n;
+  s.t0 = e0.y;
+  s.t1 = e0.z;
+  s.L = e0.w & 0x3FFFFFFF;
+  s.whole = (e0.w >> 30) & 1;
+  s.b = e1.x & 0xFFFFF;
+  s.head = e1.x >> 20;
+  s.n0 = e1.y;
+  s.qb = e1.y / NQ;
+  s.nq = min(NQ, p.Lq * p.g_q - e1.y);
+  s.kv_end = e1.z;
+  s.ld_end = e1.w;
   return s;
 }
 
@@ -403,8 +434,8 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
   uint64_t* qn_full = bars + 30;   // [1] rows mode: Q state part of segment s written to TMEM (8 warps)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(aux + 256);
   int* range_s = reinterpret_cast<int*>(aux + 264);        // [4] cta tile range, #segments, overflow unit
-  int4* segtab = reinterpret_cast<int4*>(aux + 3072);      // [MAXSEG] (u, t0, t1, L | whole << 30)
-  int* rowtab = reinterpret_cast<int*>(aux + 3072 + C::MAXSEG * 16);  // [T] pool row per tile row (cp path)
+  int4* segtab = reinterpret_cast<int4*>(aux + 3072);      // [MAXSEG][2] (seg_to_entry)
+  int* rowtab = reinterpret_cast<int*>(aux + 3072 + C::MAXSEG * 32);  // [T] pool row per tile row (cp path)
   int* vend_s = reinterpret_cast<int*>(aux + 320);         // [NQ] visible-key end per query column
   float* m_run = reinterpret_cast<float*>(aux + 640);      // [NQ] running max (log2 units)
   float* nm_s = reinterpret_cast<float*>(aux + 896);       // [NQ] -m_run (0 while m_run = -inf)
@@ -413,7 +444,7 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int cta = blockIdx.x;
-  if (p.trace && threadIdx.x == 0) p.trace[static_cast<size_t>(cta) * kTraceStride + 7] = globaltimer();
+  if (GLAD_TRACE && p.trace && threadIdx.x == 0) p.trace[static_cast<size_t>(cta) * kTraceStride + 7] = globaltimer();
 
   // ------------------------------------------------------------- setup
   if (warp == 0) {
@@ -447,7 +478,14 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
         const unsigned hm = __ballot_sync(0xffffffffu, has);
         const int pos = nseg + __popc(hm & ((1u << lane) - 1));
         const int whole = (st0 == 0 && st1 == pu1 - pu0) ? 1 : 0;
-        if (has && pos < C::MAXSEG) segtab[pos] = make_int4(u, st0, st1, L | (whole << 30));
+        if (has && pos < C::MAXSEG) {
+          Seg sg;
+          seg_unit<NQ>(p, u, L, sg);
+          sg.t0 = st0;
+          sg.t1 = st1;
+          sg.whole = whole != 0;
+          seg_to_entry<NQ>(sg, segtab + 2 * pos);
+        }
         const int cnt = __popc(hm);
         if (nseg + cnt > C::MAXSEG) {  // table full: the rest is walked on the fly
           const unsigned keep = C::MAXSEG - nseg;
@@ -508,9 +546,16 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
   __syncthreads();
   if (p.cl_n > 1) cluster_sync();  // peers' barriers initialised before any remote arrive / multicast
   tc_fence_after();
+#if GLAD_REGS_SPLIT
+  // 384 threads x 168 registers at launch; warpgroup 0 (producer, MMA
+  // issuer, Q loader) needs few, the two softmax warpgroups many.
+  if (warp < 4) setmaxnreg_dec<GLAD_REGS_LOW>();
+  else setmaxnreg_inc<GLAD_REGS_HIGH>();
+#endif
   const uint32_t tmem = *tmem_slot;
   const int cta_t0 = range_s[0], cta_t1 = range_s[1], nseg_tab = range_s[2], u_more = range_s[3];
-  uint64_t* trace = p.trace ? p.trace + static_cast<size_t>(cta) * kTraceStride : nullptr;
+  // debug timeline: compiled in only with -DGLAD_TRACE=1 (libglad_trace.so, tools/trace.py)
+  uint64_t* trace = (GLAD_TRACE && p.trace) ? p.trace + static_cast<size_t>(cta) * kTraceStride : nullptr;
   if (trace && threadIdx.x == 0) trace[0] = globaltimer();
 
   // All roles walk the same sequence of segments: entries of the table,
@@ -518,7 +563,7 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
   // `k` counts segments, `u` is the on-the-fly cursor.
   auto next_seg = [&](int& k, int& u, Seg& s) -> bool {
     if (k < nseg_tab) {
-      s = seg_from_entry<NQ>(p, segtab[k++]);
+      s = seg_from_entry<NQ>(p, segtab + 2 * k++);
       return true;
     }
     if (u_more < 0) return false;
@@ -526,7 +571,9 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
     for (;; ++u) {
       if (u >= p.n_units) return false;
       if (__ldg(p.plan + u) >= cta_t1) return false;
-      s = make_seg<NQ>(p, u, cta_t0, cta_t1);
+      Seg tmp;
+      make_seg<NQ>(p, u, cta_t0, cta_t1, &tmp);
+      s = tmp;
       if (s.t1 > s.t0) { ++u; ++k; return true; }
     }
   };
@@ -577,6 +624,7 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
 #pragma unroll
         for (int j = 0; j < RPW; ++j) {
           if (32 * j + 31 < row_lo || 32 * j >= row_hi) continue;
+#pragma unroll 1  // (not unrolled: keeps the kernel's code small; this is the phase-mask-32 fallback path)
           for (int rr = 0; rr < 32; ++rr) {
             const int r = 32 * j + rr;
             const int row = __shfl_sync(0xffffffffu, rowreg[j], rr);
@@ -1071,7 +1119,7 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
     const uint32_t lane_addr = static_cast<uint32_t>(wq * 32) << 16;
     const uint32_t pair_bar = 4 + wq;
     float* mx_x = red;                                                   // [2 wg][128] partial row max
-    float* l_x = reinterpret_cast<float*>(aux + 3072 + C::MAXSEG * 16 + T * 4);  // [2 wg][128] partial row sums
+    float* l_x = reinterpret_cast<float*>(aux + 3072 + C::MAXSEG * 32 + T * 4);  // [2 wg][128] partial row sums
     const float sl2 = p.scale_log2;
     // Q state part of segment sq's row n (this WG's half of D_KN) -> TMEM
     // (A operand of the TS-mode QK: lane = row, 2 bf16 per column).  Called
