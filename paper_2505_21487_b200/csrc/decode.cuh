@@ -110,6 +110,9 @@ struct DecodeParams {
 #ifndef GLAD_NS_CAP
 #define GLAD_NS_CAP 4
 #endif
+#ifndef GLAD_SPLIT_STAGES
+#define GLAD_SPLIT_STAGES 1
+#endif
 #ifndef GLAD_TRACE
 #define GLAD_TRACE 0
 #endif
@@ -133,6 +136,22 @@ constexpr int kTraceStride = 8 + 12 * kTraceTiles;
 template <int D_V, int T>
 __host__ __device__ constexpr bool rows_fits() {
   return T <= 96 && 2 * T + D_V + D_V / 2 <= 512;
+}
+
+// KV stages of the unsplit (interleaved) stage layout; mirrors the NS
+// computation in DecodeCfg with NLO = NCH_V.
+template <int D_V, int D_KN, int D_R, int NQ, int T>
+__host__ __device__ constexpr int ns_nosplit() {
+  constexpr bool rows = (NQ == 128);
+  constexpr int nch_v = D_V / 64, nch = nch_v + 1, nqch = D_KN / 64 + 1;
+  constexpr int chunk = T * 128, stage = nch * chunk, lgrp = nch_v * 1024, off_r = nch_v * chunk;
+  constexpr int qbytes = rows ? NQ * 128 : nqch * NQ * 128;
+  constexpr int aux = 3072 + 64 * 32 + T * 4 + (rows ? 1024 : 0);
+  constexpr int avail = 227 * 1024 - 1024 - aux;
+  constexpr int over = rows ? 0 : (16 * lgrp > off_r + 16384 ? 16 * lgrp : off_r + 16384) - stage;
+  constexpr int xtra = over - qbytes - aux > 0 ? over - qbytes - aux : 0;
+  constexpr int pbuf = rows ? ((T + 63) / 64) * NQ * 128 : 0;
+  return (avail - qbytes - 2 * pbuf - xtra) / stage;
 }
 
 template <int D_V_, int D_KN_, int D_R_, int NQ_, int T_ = 128>
@@ -162,11 +181,34 @@ struct DecodeCfg {
   static constexpr int RK = D_R / 16;
   static constexpr int CHUNK = T * 128;  // one [T tokens x 64 cols] bf16 box set
   static constexpr int STAGE = NCH * CHUNK;
-  // Stage layout: latent [T/8 row groups][NCH_V chunks][8 rows][128 B] (one
-  // 1-KB SW128 atom per (group, chunk): a page run's whole latent slice is
-  // one TMA box), then the RoPE chunk [T rows][128 B] (later P^T).
-  static constexpr int LGRP = NCH_V * 1024;  // latent row-group stride
+  // Stage layout.  Swap-AB ("split" stages): the latent columns in two
+  // halves, lo = chunks [0, NLO) and hi = chunks [NLO, NCH_V), each
+  // [T/8 row groups][NLO chunks][8 rows][128 B] (one 1-KB SW128 atom per
+  // (group, chunk): a page run's half slice is one TMA box), then the RoPE
+  // chunk [T rows][128 B] (later P^T).  The halves are filled and released
+  // separately (kv_full/kv_empty = lo, kv_full_hi/kv_empty_hi = hi + RoPE):
+  // PV's first output blocks read only lo, so lo is refilled while PV still
+  // runs on hi, and QK(i+2) starts on lo before hi has landed.
+  // Rows mode: one interleaved latent [T/8][NCH_V][8][128 B] (its PV reads
+  // all d columns as one N = D_V operand with a uniform 1-KB chunk stride).
+  // Split only where the stage count is the bottleneck: 128-token tiles with
+  // at most two stages (C2 GLA-2 and the GLA-8 shards: 0.2458 -> 0.2362 ms).
+  // Measured slower with three or more stages (C4 GTA 0.391 -> 0.421 ms:
+  // the extra TMA issues and barrier round trips cost more than the earlier
+  // refill gains) and for MLA's 64-token tiles (0.553 -> 0.594 ms).
+  static constexpr int NS_NOSPLIT = ns_nosplit<D_V_, D_KN_, D_R_, NQ_, T_>();
+  static constexpr bool SPLIT = !ROWS && T == 128 && NS_NOSPLIT <= 2 && GLAD_SPLIT_STAGES;
+  static constexpr int NLO = SPLIT ? NCH_V / 2 : NCH_V;  // chunks per half (per stage when not split)
+  static constexpr int LO_BYTES = NLO * CHUNK;
+  static constexpr int LGRP = NLO * 1024;  // latent row-group stride (within a half)
   static constexpr int OFF_R = NCH_V * CHUNK;
+  // byte offset of (64-column) latent chunk c within a stage (row group 0)
+  static constexpr int chunk_off(int c) { return c < NLO ? c * 1024 : LO_BYTES + (c - NLO) * 1024; }
+  // PV output block blk (d in [128 blk, 128 blk + 128)) = chunks 2 blk, 2 blk + 1:
+  // distance between them (the MN-major descriptor's LBO)
+  static constexpr int PV_LBO = NLO >= 2 ? 1024 : LO_BYTES;
+  // last PV output block that reads lo chunks (kv_empty committed after it)
+  static constexpr int BLK_LO_LAST = SPLIT && NLO >= 2 ? NLO / 2 - 1 : D_V / 128 - 1;
   static constexpr int QCHUNK = NQ * 128;
   // Rows mode keeps the query's state part (D_KN) in TMEM (A of a TS-mode
   // QK, written by the softmax warps); only its RoPE chunk is staged in
@@ -182,11 +224,12 @@ struct DecodeCfg {
   static constexpr int NWG = 2;
   static constexpr int CW = ROWS ? 32 : NQ / NWG;
   static constexpr int HC = CW;  // columns per softmax thread (one token row)
-  static constexpr int MAXSEG = 64;  // per-CTA segment table entries (aux + 3072), 32 B each
+  static constexpr int MAXSEG = 64;  // per-CTA segment table entries (aux + 3072), 32 B each (ns_nosplit mirrors it)
   static constexpr int AUX = 3072 + MAXSEG * 32 + T * 4 + (ROWS ? 1024 : 0);  // + cp.async row table (+ rows: row-sum exchange)
   static constexpr int AVAIL = 227 * 1024 - 1024 - AUX;
   // bytes the M = 128 QK may read past the end of the last stage (rows >= T)
-  static constexpr int OVER_RAW = ROWS ? 0 : (16 * LGRP > OFF_R + 16384 ? 16 * LGRP : OFF_R + 16384) - STAGE;
+  static constexpr int OVER_LAT = (SPLIT ? LO_BYTES : 0) + 16 * LGRP;
+  static constexpr int OVER_RAW = ROWS ? 0 : (OVER_LAT > OFF_R + 16384 ? OVER_LAT : OFF_R + 16384) - STAGE;
   static constexpr int XTRA = OVER_RAW - QBYTES - AUX > 0 ? OVER_RAW - QBYTES - AUX : 0;
   // Rows mode: P (bf16 [128 rows x T]) in two shared-memory buffers, K-major
   // 128B-swizzled in 64-token chunks (A of an SS PV), so an S buffer is free
@@ -233,6 +276,7 @@ struct DecodeCfg {
   static_assert(TMEM_USED <= 512, "TMEM budget");
   static_assert(QCHUNK % 1024 == 0, "Q chunk alignment");
   static_assert(T == 128 || T == 96 || T == 64, "tile height");
+  static_assert(!SPLIT || NCH_V % 2 == 0, "split stages need an even number of latent chunks");
 };
 
 // Column reduction over groups of LANES lanes (32, or 16 for the halves of a
@@ -432,6 +476,8 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
   uint64_t* o_empty = bars + 24;   // [2] epilogue read O buffer (s & 1) (8 arrivals)
   uint64_t* cl_empty = bars + 26;  // [4] cluster: stage free in all cl_n CTAs (leader's copy is used)
   uint64_t* qn_full = bars + 30;   // [1] rows mode: Q state part of segment s written to TMEM (8 warps)
+  uint64_t* kv_full_hi = reinterpret_cast<uint64_t*>(aux + 2560);   // [4] split stages: hi half + RoPE landed
+  uint64_t* kv_empty_hi = reinterpret_cast<uint64_t*>(aux + 2592);  // [4] split stages: hi half + P^T free
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(aux + 256);
   int* range_s = reinterpret_cast<int*>(aux + 264);        // [4] cta tile range, #segments, overflow unit
   int4* segtab = reinterpret_cast<int4*>(aux + 3072);      // [MAXSEG][2] (seg_to_entry)
@@ -511,6 +557,8 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
     for (int i = 0; i < NS; ++i) {
       mbar_init(&kv_full[i], p.cp_kv ? (p.q_tma ? 64 : 32) : 1);
       mbar_init(&kv_empty[i], 1);
+      mbar_init(&kv_full_hi[i], p.cp_kv ? (p.q_tma ? 64 : 32) : 1);
+      mbar_init(&kv_empty_hi[i], 1);
       mbar_init(&p_full[i], C::ROWS ? 4 * GLAD_ROWS_WG : 8);  // softmax warps
     }
     for (int i = 0; i < 2; ++i) {
@@ -556,7 +604,12 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
   const int cta_t0 = range_s[0], cta_t1 = range_s[1], nseg_tab = range_s[2], u_more = range_s[3];
   // debug timeline: compiled in only with -DGLAD_TRACE=1 (libglad_trace.so, tools/trace.py)
   uint64_t* trace = (GLAD_TRACE && p.trace) ? p.trace + static_cast<size_t>(cta) * kTraceStride : nullptr;
-  if (trace && threadIdx.x == 0) trace[0] = globaltimer();
+  if (trace && threadIdx.x == 0) {
+    trace[0] = globaltimer();
+    uint32_t smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    trace[kTraceStride - 1] = smid;  // (overlaps tile 127's last slot: only CTAs with < 128 tiles)
+  }
 
   // All roles walk the same sequence of segments: entries of the table,
   // then (only if it overflowed) units walked on the fly from u_more.
@@ -619,6 +672,7 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
                                      : -1;
         }
         mbar_wait(&kv_empty[stage], ((it / NS) & 1) ^ 1);
+        if (C::SPLIT) mbar_wait(&kv_empty_hi[stage], ((it / NS) & 1) ^ 1);
         if (trace && pw == 0 && lane == 0 && it < kTraceTiles) trace[13 + 12 * it] = globaltimer();
         const uint32_t sdst = sbase + stage * C::STAGE;
 #pragma unroll
@@ -636,13 +690,14 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
             for (int u0 = 0; u0 < C::NCH_V * 8; u0 += 32) {
               const int un = u0 + lane;
               if (un < C::NCH_V * 8)
-                cp_async16(ldst + (un >> 3) * 1024 + (((un & 7) ^ (r & 7)) << 4), base_h + roff + u0 * 8, 16);
+                cp_async16(ldst + C::chunk_off(un >> 3) + (((un & 7) ^ (r & 7)) << 4), base_h + roff + u0 * 8, 16);
             }
             if (lane < C::D_R / 8)  // RoPE chunk
               cp_async16(sdst + C::OFF_R + r * 128 + ((lane ^ (r & 7)) << 4), base_r + roff, 16);
           }
         }
         cp_async_mbar_arrive(&kv_full[stage]);
+        if (C::SPLIT) cp_async_mbar_arrive(&kv_full_hi[stage]);
         if (trace && pw == 0 && lane == 0 && it < kTraceTiles) trace[8 + 12 * it] = globaltimer();
         if (pvalid) {  // L2 prefetch of tile it + NS: each row's latent slice and RoPE
           const int* pbt = p.block_table + static_cast<size_t>(ps.b) * p.bt_stride;
@@ -667,15 +722,18 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
     named_bar_sync(3, 96);  // the first Q load is issued first: QK needs Q, not a second tile
     if (trace && lane == 0 && warp == 0) trace[4] = globaltimer();
     const int box_rows = p.box_rows;
-    // Two boxes per page run of a tile: item 2*box = the latent slice (4-D
-    // map, all NCH_V chunks in one box), item 2*box + 1 = the RoPE chunk
-    // (2-D map).  Issued into smem (completing on kv_full[stage]) or as an
-    // L2 prefetch.  Items are spread over the 32 lanes.
+    // Boxes per page run of a tile: the latent slice (4-D map: NLO chunks
+    // per box, so split stages take one box per half, others one for all
+    // NCH_V chunks) and the RoPE chunk (2-D map).  Issued into smem
+    // (completing on the half's full barrier) or as an L2 prefetch (bar =
+    // nullptr).  item: 0 = latent lo (all chunks if not split), 1 = RoPE,
+    // 2 = latent hi.
     const uint16_t mc_mask = static_cast<uint16_t>((1u << p.cl_n) - 1u);
     auto issue_item = [&](const Seg& s, int row, int box, int item, uint32_t stage_addr, uint64_t* bar) {
-      if (item == 0) {
-        const int c = s.head * (p.d_head >> 6);
-        const uint32_t dst = stage_addr + box * (box_rows >> 3) * C::LGRP;
+      if (item != 1) {
+        const int half = item == 2 ? 1 : 0;
+        const int c = s.head * (p.d_head >> 6) + half * C::NLO;
+        const uint32_t dst = stage_addr + half * C::LO_BYTES + box * (box_rows >> 3) * C::LGRP;
         if (!bar) tma_prefetch_4d(&lmap, 0, 0, c, row >> 3);
         else if (p.cl_n > 1) tma_load_4d_mc(dst, &lmap, bar, 0, 0, c, row >> 3, mc_mask);
         else tma_load_4d(dst, &lmap, bar, 0, 0, c, row >> 3);
@@ -698,8 +756,9 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
       const int p0 = tl * T;
       const int ntok = min(T, s.ld_end - p0);
       const int nbox = (ntok + box_rows - 1) / box_rows;
-      for (int bx = lane; bx < nbox * 2; bx += 32)
-        issue_item(s, item_row(bt_row, p0, bx >> 1), bx >> 1, bx & 1, sbase + stage * C::STAGE,
+      constexpr int NIT = C::SPLIT ? 3 : 2;
+      for (int bx = lane; bx < nbox * NIT; bx += 32)
+        issue_item(s, item_row(bt_row, p0, bx / NIT), bx / NIT, bx % NIT, sbase + stage * C::STAGE,
                    prefetch ? nullptr : &kv_full[stage]);
       return nbox;
     };
@@ -727,18 +786,22 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
         const int p0 = tl * T;
         const int ntok = min(T, s.ld_end - p0);
         const int nbox = (ntok + box_rows - 1) / box_rows;
-        const int nitem = nbox * 2;
-        // the page lookup of this lane's first item is done before the stage
+        // the page lookup of this lane's page run is done before the stage
         // wait: after the release only the TMA issue remains on the critical path
-        const int row0 = (loader && !p.g4 && lane < nitem) ? item_row(bt_row, p0, lane >> 1) : 0;
+        constexpr int NIT0 = C::SPLIT ? 1 : 2;  // first-issue items per page run (split: lo; else latent + RoPE)
+        const int row0 = (loader && !p.g4 && lane < nbox * NIT0) ? item_row(bt_row, p0, lane / NIT0) : 0;
         if (trace && lane == 0 && warp == 0 && it == 0) {
           if (row0 == 0x7fffffff) __nanosleep(1);  // debug: wait for the lookup itself
           trace[6] = globaltimer();
         }
-        mbar_wait(&kv_empty[stage], ((it / NS) & 1) ^ 1);
+        const uint32_t ph = ((it / NS) & 1) ^ 1;
+        mbar_wait(&kv_empty[stage], ph);
+        // cluster multicast and gather4 fill the whole stage at once
+        const bool whole_stage = !C::SPLIT || p.cl_n > 1 || p.g4;
+        if (C::SPLIT && whole_stage) mbar_wait(&kv_empty_hi[stage], ph);
         if (trace && lane == 0 && warp == 0 && it < kTraceTiles) trace[13 + 12 * it] = globaltimer();
         if (lane == 0 && !p.g4)
-          mbar_arrive_expect_tx(&kv_full[stage], static_cast<uint32_t>(nbox * box_rows * C::NCH * 128));
+          mbar_arrive_expect_tx(&kv_full[stage], static_cast<uint32_t>(nbox * box_rows * (C::SPLIT ? C::NLO : C::NCH) * 128));
         if (p.cl_n > 1) {  // stage free here -> tell the loader; the loader waits for every CTA
           if (lane == 0) mbar_arrive_cluster(&cl_empty[stage], 0);
           if (loader) mbar_wait(&cl_empty[stage], (it / NS) & 1);
@@ -752,9 +815,12 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
           // (rows past the visible end repeat the last visible row: they
           // are zeroed / masked by the softmax like any unloaded row)
           const int ngrp = (ntok + 3) >> 2;
-          if (lane == 0 && warp == 0)
-            mbar_arrive_expect_tx(&kv_full[stage], static_cast<uint32_t>(ngrp * C::NCH * 512));
+          if (lane == 0 && warp == 0) {
+            mbar_arrive_expect_tx(&kv_full[stage], static_cast<uint32_t>(ngrp * (C::SPLIT ? C::NLO : C::NCH) * 512));
+            if (C::SPLIT) mbar_arrive_expect_tx(&kv_full_hi[stage], static_cast<uint32_t>(ngrp * (C::NCH - C::NLO) * 512));
+          }
           __syncwarp();
+          uint64_t* bar_hi = C::SPLIT ? &kv_full_hi[stage] : &kv_full[stage];
           const int npw = (p.q_tma ? 2 : 1), pw = warp == 0 ? 0 : 1;
           for (int g = lane + 32 * pw; g < ngrp; g += 32 * npw) {
             int rr[4];
@@ -768,14 +834,36 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
             const int c_head = s.head * p.d_head;
 #pragma unroll
             for (int ch = 0; ch < C::NCH_V; ++ch)
-              tma_gather4(ldst + ch * 1024, &lmap, &kv_full[stage], c_head + ch * 64, rr[0], rr[1], rr[2], rr[3]);
-            tma_gather4(stage_addr + C::OFF_R + r * 128, &lmap, &kv_full[stage], p.rope_col, rr[0], rr[1], rr[2],
-                        rr[3]);
+              tma_gather4(ldst + C::chunk_off(ch), &lmap, ch < C::NLO ? &kv_full[stage] : bar_hi, c_head + ch * 64,
+                          rr[0], rr[1], rr[2], rr[3]);
+            tma_gather4(stage_addr + C::OFF_R + r * 128, &lmap, bar_hi, p.rope_col, rr[0], rr[1], rr[2], rr[3]);
           }
-        } else if (loader) {
-          if (lane < nitem) issue_item(s, row0, lane >> 1, lane & 1, stage_addr, &kv_full[stage]);
-          for (int bx = lane + 32; bx < nitem; bx += 32)  // small pages: more boxes than lanes
-            issue_item(s, item_row(bt_row, p0, bx >> 1), bx >> 1, bx & 1, stage_addr, &kv_full[stage]);
+        } else {
+          // latent lo (or the whole latent) + (not split) RoPE, one page run per lane
+          if (loader) {
+            if (lane < nbox * NIT0) issue_item(s, row0, lane / NIT0, lane % NIT0, stage_addr, &kv_full[stage]);
+            for (int bx = lane + 32; bx < nbox * NIT0; bx += 32)  // more boxes than lanes
+              issue_item(s, item_row(bt_row, p0, bx / NIT0), bx / NIT0, bx % NIT0, stage_addr, &kv_full[stage]);
+          }
+          if (C::SPLIT) {
+            // hi half + RoPE once PV(it - NS) has read them (P^T lives in the RoPE chunk)
+            if (!whole_stage) mbar_wait(&kv_empty_hi[stage], ph);
+            if (lane == 0)
+              mbar_arrive_expect_tx(&kv_full_hi[stage],
+                                    static_cast<uint32_t>(nbox * box_rows * (C::NCH - C::NLO) * 128));
+            __syncwarp();
+            if (loader) {
+              if (lane < nbox) {
+                issue_item(s, row0, lane, 2, stage_addr, &kv_full_hi[stage]);
+                issue_item(s, row0, lane, 1, stage_addr, &kv_full_hi[stage]);
+              }
+              for (int bx = lane + 32; bx < nbox; bx += 32) {
+                const int rw = item_row(bt_row, p0, bx);
+                issue_item(s, rw, bx, 2, stage_addr, &kv_full_hi[stage]);
+                issue_item(s, rw, bx, 1, stage_addr, &kv_full_hi[stage]);
+              }
+            }
+          }
         }
         if (trace && lane == 0 && warp == 0 && it < kTraceTiles) trace[8 + 12 * it] = globaltimer();
         if (C::L2PF && !p.g4 && loader && !pf_ready) {
@@ -947,9 +1035,14 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
       auto probe = [&](uint64_t* bar, int parity) { return warp_uniform(mbar_test_wait(smem_u32(bar), parity)); };
       bool qk_left = advance(cq), pv_left = advance(cp);
       int next_qk = 0, next_pv = 0;
+      int qk_part = 0;  // split stages: 1 = lo part of QK(next_qk) issued, hi part pending
       // Descriptors are built once per stage / Q buffer; each MMA only adds a
       // compile-time byte offset (>> 4) to the start-address field.
-      auto issue_qk = [&]() {
+      // QK in two parts (split stages): part 0 = the key chunks of the lo
+      // half (issued once lo has landed), part 1 = the remaining key chunks
+      // + the RoPE chunk (once hi has landed); s_full is committed after part 1.
+      constexpr int QK_LO = C::NCH_QK < C::NLO ? C::NCH_QK : C::NLO;  // key chunks in lo
+      auto issue_qk = [&](int part) {
         const int stage = next_qk % NS;
         const int sb = next_qk & 1;
         tc_fence_after();
@@ -958,26 +1051,37 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
         const uint64_t ad = desc_kmajor_sw128(sbase + stage * C::STAGE, C::LGRP);
         const uint64_t rd = desc_kmajor_sw128(sbase + stage * C::STAGE + C::OFF_R);
         const uint64_t bd = desc_kmajor_sw128(sbase + C::OFF_Q + (cq.seg % C::NQB) * C::QBYTES);
+        if (part == 0) {
 #pragma unroll
-        for (int c = 0; c < C::NCH_QK; ++c) {
+          for (int c = 0; c < QK_LO; ++c) {
 #pragma unroll
-          for (int k = 0; k < 4; ++k)
-            umma_f16_ss_warp(d, ad + static_cast<uint64_t>((c * 1024 + k * 32) >> 4),
-                             bd + static_cast<uint64_t>((c * C::QCHUNK + k * 32) >> 4), idesc_qk, (c | k) != 0);
+            for (int k = 0; k < 4; ++k)
+              umma_f16_ss_warp(d, ad + static_cast<uint64_t>((C::chunk_off(c) + k * 32) >> 4),
+                               bd + static_cast<uint64_t>((c * C::QCHUNK + k * 32) >> 4), idesc_qk, (c | k) != 0);
+          }
         }
+        if (part == 1 || !C::SPLIT) {
 #pragma unroll
-        for (int k = 0; k < C::RK; ++k)
-          umma_f16_ss_warp(d, rd + static_cast<uint64_t>((k * 32) >> 4),
-                           bd + static_cast<uint64_t>((C::NCH_QK * C::QCHUNK + k * 32) >> 4), idesc_qk, 1u);
-        umma_commit_warp(&s_full[sb]);
-        if (cq.tl + 1 == cq.t1) umma_commit_warp(&q_empty[cq.seg % C::NQB]);  // last QK of the segment: Q free
+          for (int c = C::SPLIT ? QK_LO : C::NCH_QK; c < C::NCH_QK; ++c) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              umma_f16_ss_warp(d, ad + static_cast<uint64_t>((C::chunk_off(c) + k * 32) >> 4),
+                               bd + static_cast<uint64_t>((c * C::QCHUNK + k * 32) >> 4), idesc_qk, 1u);
+          }
+#pragma unroll
+          for (int k = 0; k < C::RK; ++k)
+            umma_f16_ss_warp(d, rd + static_cast<uint64_t>((k * 32) >> 4),
+                             bd + static_cast<uint64_t>((C::NCH_QK * C::QCHUNK + k * 32) >> 4), idesc_qk, 1u);
+          umma_commit_warp(&s_full[sb]);
+          if (cq.tl + 1 == cq.t1) umma_commit_warp(&q_empty[cq.seg % C::NQB]);  // last QK of the segment: Q free
+        }
       };
       auto issue_pv = [&]() {
         tc_fence_after();
         const int j = next_pv;
         const int stage = j % NS;
         const uint32_t kv = sbase + stage * C::STAGE;
-        const uint64_t ad = desc_mnmajor_sw128(kv, 1024, C::LGRP);
+        const uint64_t ad = desc_mnmajor_sw128(kv, C::PV_LBO, C::LGRP);
         const uint64_t bd = C::P_SW128 ? desc_mnmajor_sw128(kv + C::OFF_R, 0)
                                        : desc_mnmajor_noswz(kv + C::OFF_R, 128, T * 16);
         const uint32_t obuf = tm + C::TMEM_O + (cp.seg % C::NOB) * C::OCOLS;
@@ -986,11 +1090,13 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
         for (int blk = 0; blk < C::NBLK_O; ++blk) {
 #pragma unroll
           for (int k = 0; k < T / 16; ++k)
-            umma_f16_ss_warp(obuf + blk * NQ, ad + static_cast<uint64_t>((2 * blk * 1024 + k * 2 * C::LGRP) >> 4),
+            umma_f16_ss_warp(obuf + blk * NQ, ad + static_cast<uint64_t>((C::chunk_off(2 * blk) + k * 2 * C::LGRP) >> 4),
                              bd + static_cast<uint64_t>((C::P_SW128 ? k * 2048 : k * 256) >> 4), idesc_pv,
                              (!first || k > 0) ? 1u : 0u);
+          // lo half read by every block up to here: the producer may refill it
+          if (C::SPLIT && blk == C::BLK_LO_LAST) umma_commit_warp(&kv_empty[stage]);
         }
-        umma_commit_warp(&kv_empty[stage]);
+        umma_commit_warp(C::SPLIT ? &kv_empty_hi[stage] : &kv_empty[stage]);
         umma_commit_warp(&pv_done[j & 3]);
       };
       long long t0 = clock64();
@@ -1016,19 +1122,32 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
         // stages the refill itself needs PV(i) first, and greedy order wins.
         // (checked right after a PV issue too: PV(i) + QK(i+2) then go out as
         // one block, one scheduler round trip per tile)
-        if (qk_left && (NS < 3 || next_qk - next_pv <= 1) &&
+        if (qk_left && qk_part == 0 && (NS < 3 || next_qk - next_pv <= 1) &&
             probe(&kv_full[next_qk % NS], (next_qk / NS) & 1) &&
             probe(&s_empty[next_qk & 1], ((next_qk >> 1) & 1) ^ 1)) {
           const bool first = (cq.tl == cq.t0);
           if (!first || probe(&q_full[cq.seg % C::NQB], (cq.seg / C::NQB) & 1)) {
             if (trace && lane == 0 && next_qk == 0) trace[1] = globaltimer();
             if (trace && lane == 0 && next_qk < kTraceTiles) trace[9 + 12 * next_qk] = globaltimer();
-            issue_qk();
-            if (trace && lane == 0 && next_qk < kTraceTiles) trace[16 + 12 * next_qk] = globaltimer();
-            ++next_qk;
-            qk_left = advance(cq);
+            issue_qk(0);
+            if (C::SPLIT) {
+              qk_part = 1;
+            } else {
+              if (trace && lane == 0 && next_qk < kTraceTiles) trace[16 + 12 * next_qk] = globaltimer();
+              ++next_qk;
+              qk_left = advance(cq);
+            }
             did = true;
           }
+        }
+        // second part of a split QK once the hi half + RoPE have landed
+        if (C::SPLIT && qk_part == 1 && probe(&kv_full_hi[next_qk % NS], (next_qk / NS) & 1)) {
+          issue_qk(1);
+          if (trace && lane == 0 && next_qk < kTraceTiles) trace[16 + 12 * next_qk] = globaltimer();
+          qk_part = 0;
+          ++next_qk;
+          qk_left = advance(cq);
+          did = true;
         }
         if (did) {
           t0 = clock64();
@@ -1262,7 +1381,7 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
           for (int idx = wg * 128 + n; idx < T * C::NCH_V; idx += 128 * NWGR) {
             const int tr = idx / C::NCH_V, ch = idx - tr * C::NCH_V;
             if (p0 + tr >= s.kv_end) {
-              const uint32_t a = stage_base + (tr >> 3) * C::LGRP + ch * 1024 + (tr & 7) * 128;
+              const uint32_t a = stage_base + (tr >> 3) * C::LGRP + C::chunk_off(ch) + (tr & 7) * 128;
 #pragma unroll
               for (int uu = 0; uu < 8; ++uu) st_shared_v4(a + uu * 16, 0u, 0u, 0u, 0u);
             }
@@ -1548,7 +1667,7 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
 #pragma unroll
           for (int ch = 0; ch < C::NCH_V; ++ch)
 #pragma unroll
-            for (int uu = 0; uu < 8; ++uu) st_shared_v4(kvrow + ch * 1024 + uu * 16, 0u, 0u, 0u, 0u);
+            for (int uu = 0; uu < 8; ++uu) st_shared_v4(kvrow + C::chunk_off(ch) + uu * 16, 0u, 0u, 0u, 0u);
         }
         fence_proxy_async_smem();
         tc_fence_before();

@@ -25,10 +25,14 @@ bool decode_supported(const DecodeKey& k) {
   return k.d_v == 128 && k.d_kn == 64 && k.d_r == 64;  // GTA, d_h = 128
 }
 
-int decode_stages(const DecodeKey& k) {
+static int stages_and_split(const DecodeKey& k) {
   if (!decode_supported(k)) return 0;
   return k.t == 64 ? decode_stages_t<64>(k) : k.t == 96 ? decode_stages_t<96>(k) : decode_stages_t<128>(k);
 }
+
+int decode_stages(const DecodeKey& k) { return stages_and_split(k) & 0xff; }
+
+bool decode_split(const DecodeKey& k) { return (stages_and_split(k) & 0x100) != 0; }
 
 int decode_max_clusters(const DecodeKey& k, int cl_n) {
   if (!decode_supported(k)) return 0;

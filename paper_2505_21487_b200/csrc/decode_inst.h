@@ -112,7 +112,7 @@ struct StagesF {
   int* ns;
   template <class C>
   cudaError_t run() {
-    *ns = C::NS;
+    *ns = C::NS | (C::SPLIT ? 0x100 : 0);
     return cudaSuccess;
   }
 };
@@ -134,7 +134,7 @@ int decode_max_clusters_t(const DecodeKey& k, int cl_n);
   template <>                                                                                              \
   int decode_stages_t<T>(const DecodeKey& k) {                                                             \
     int ns = 0;                                                                                            \
-    return with_cfg<T>(k, StagesF{&ns}) == cudaSuccess ? ns : 0;                                           \
+    return with_cfg<T>(k, StagesF{&ns}) == cudaSuccess ? ns : 0; /* NS | SPLIT << 8 */                      \
   }                                                                                                        \
   template <>                                                                                              \
   int decode_max_clusters_t<T>(const DecodeKey& k, int cl_n) {                                             \

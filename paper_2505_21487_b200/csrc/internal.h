@@ -45,6 +45,7 @@ cudaError_t launch_decode(const DecodeKey& key, const CUtensorMap& tmap, const C
                           cudaStream_t stream);
 bool decode_supported(const DecodeKey& key);
 int decode_stages(const DecodeKey& key);                   // KV pipeline stages of the instantiation (0: unsupported)
+bool decode_split(const DecodeKey& key);                   // split (lo / hi half) stage layout (DecodeCfg::SPLIT)
 int decode_max_clusters(const DecodeKey& key, int cl_n);  // resident clusters of cl_n CTAs (0: error)
 int decode_max_nq(int d_v);
 bool decode_rows_supported(const DecodeKey& key);  // rows mode (nq = 128) exists for these dims (any t)

@@ -14,7 +14,15 @@ import argparse
 import os
 import sys
 
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+# the timeline instrumentation is compiled only into the trace build
+if "GLAD_LIB" not in os.environ:
+    import subprocess
+    so = os.path.join(ROOT, "paper_2505_21487_b200", "libglad_trace.so")
+    subprocess.run([sys.executable, "-m", "paper_2505_21487_b200.build"], cwd=ROOT, check=True,
+                   env=dict(os.environ, GLAD_EXTRA_FLAGS="-DGLAD_TRACE=1", GLAD_LIB_OUT=so), stdout=subprocess.DEVNULL)
+    os.environ["GLAD_LIB"] = so
 import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
@@ -101,6 +109,32 @@ print(f"  start (us): Q issued {np.median(tr[:, 5] - tr[:, 0]) / 1e3:.2f}, produ
       f"{np.median(tr[:, 4] - tr[:, 0]) / 1e3:.2f}, first row looked up {np.median(tr[:, 6] - tr[:, 0]) / 1e3:.2f}, "
       f"first load issued {np.median(tile[:, 0, 0] - tr[:, 0]) / 1e3:.2f}")
 print(f"  epilogue: S(last)->epi done {np.nanmedian(np.where(epi > 0, epi - tile[:, :, 2], np.nan)):.0f} ns")
+
+# end-time spread: which CTAs finish last (segments, tiles, SM id)
+_end = (tr[:, 2] - t0) / 1e3
+_nseg = tr[:, 3]
+print("end time by #segments: " + ", ".join(f"{int(k)} seg: n={int((_nseg == k).sum())} median end "
+                                            f"{np.median(_end[_nseg == k]):.1f} us" for k in np.unique(_nseg)))
+_ord = np.argsort(_end)[::-1][:8]
+print("latest CTAs (end us, start us, #seg, tiles, smid): " + "; ".join(
+    f"{_end[i]:.1f} {(tr[i, 0] - t0) / 1e3:.1f} {int(_nseg[i])} {int(ntile[i])} {int(tr[i, -1])}" for i in _ord))
+_ord = np.argsort(_end)[:4]
+print("earliest CTAs (end us, #seg, tiles, smid): " + "; ".join(
+    f"{_end[i]:.1f} {int(_nseg[i])} {int(ntile[i])} {int(tr[i, -1])}" for i in _ord))
+_rate = ntile / np.maximum((tr[:, 2] - tr[:, 0]) / 1e3, 1e-9)
+print(f"tiles per us over CTAs: min {_rate.min():.3f} p10 {np.percentile(_rate, 10):.3f} median {np.median(_rate):.3f} max {_rate.max():.3f}")
+
+if os.environ.get("TRACE_SWITCH"):
+    # raw timelines around the segment switches of the latest 3-seg and an early 2-seg CTA
+    picks = [int(np.argsort(_end)[-1]), int(np.argsort(np.where(_nseg == _nseg.min(), _end, 1e18))[len(_end) // 4 % max(1, int((_nseg == _nseg.min()).sum()))])]
+    for c in picks:
+        base = tr[c, 0]
+        print(f"CTA {c} (smid {int(tr[c, -1])}, {int(_nseg[c])} seg, end {_end[c]:.1f} us): tile: free load QK QKret S P0 PV PVret epi (us)")
+        ends = [i for i in range(ntile[c]) if tile[c, i, 7] > 0]
+        show = sorted({j for i in ends for j in range(max(0, i - 2), min(ntile[c], i + 4))} | {0, 1, 2, ntile[c] - 1})
+        for i in show:
+            print(f"  tile {i:3d}: " + "  ".join(f"{(tile[c, i, j] - base) / 1e3:8.2f}" if tile[c, i, j] else "       -"
+                                               for j in (5, 0, 1, 8, 2, 3, 4, 9, 7)))
 
 if os.environ.get("TRACE_RAW"):
     c = int(os.environ.get("TRACE_CTA", "5"))
