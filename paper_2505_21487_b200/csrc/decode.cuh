@@ -146,7 +146,7 @@ __host__ __device__ constexpr int ns_nosplit() {
   constexpr int nch_v = D_V / 64, nch = nch_v + 1, nqch = D_KN / 64 + 1;
   constexpr int chunk = T * 128, stage = nch * chunk, lgrp = nch_v * 1024, off_r = nch_v * chunk;
   constexpr int qbytes = rows ? NQ * 128 : nqch * NQ * 128;
-  constexpr int aux = 3072 + 64 * 32 + T * 4 + (rows ? 1024 : 0);
+  constexpr int aux = 3072 + 64 * 32 + T * 4 + (rows ? 1024 : 2 * NQ * 4);
   constexpr int avail = 227 * 1024 - 1024 - aux;
   constexpr int over = rows ? 0 : (16 * lgrp > off_r + 16384 ? 16 * lgrp : off_r + 16384) - stage;
   constexpr int xtra = over - qbytes - aux > 0 ? over - qbytes - aux : 0;
@@ -225,7 +225,8 @@ struct DecodeCfg {
   static constexpr int CW = ROWS ? 32 : NQ / NWG;
   static constexpr int HC = CW;  // columns per softmax thread (one token row)
   static constexpr int MAXSEG = 64;  // per-CTA segment table entries (aux + 3072), 32 B each (ns_nosplit mirrors it)
-  static constexpr int AUX = 3072 + MAXSEG * 32 + T * 4 + (ROWS ? 1024 : 0);  // + cp.async row table (+ rows: row-sum exchange)
+  // + cp.async row table (+ rows: row-sum exchange; swap-AB: 1/l of the two O buffers for the deferred epilogue)
+  static constexpr int AUX = 3072 + MAXSEG * 32 + T * 4 + (ROWS ? 1024 : 2 * NQ * 4);
   static constexpr int AVAIL = 227 * 1024 - 1024 - AUX;
   // bytes the M = 128 QK may read past the end of the last stage (rows >= T)
   static constexpr int OVER_LAT = (SPLIT ? LO_BYTES : 0) + 16 * LGRP;
@@ -1479,6 +1480,90 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
     const uint32_t a_addr = smem_u32(alpha_s + cb);
     const uint32_t ao_addr = smem_u32(alpha_s + c0);  // O^T rescale: all CW columns of the WG
     const float sl2 = p.scale_log2;
+    // Deferred epilogue: a finished segment's O is written one 128-row
+    // block per tile of the NEXT segment (after that tile's P is out, where
+    // the softmax warps would otherwise wait for S), not in one piece that
+    // stalls the pipeline at every segment switch (~5 us measured).  Its
+    // 1/l lives in einv_s[seg % NOB] until then.
+    float* einv_s = reinterpret_cast<float*>(aux + 3072 + C::MAXSEG * 32 + T * 4);  // [NOB][NQ]
+    int e_blk = C::NBLK_O;  // next block of the pending epilogue (NBLK_O = none pending)
+    int e_seg = 0, e_j = 0, e_ncols = 0, e_j0 = 0, e_slot = 0;
+    bool e_whole = false;
+    size_t e_row0 = 0;
+    auto epi_block = [&]() {
+      if (e_blk == 0) {  // the segment's last PV must have completed
+        mbar_wait(&pv_done[e_j & 3], (e_j >> 2) & 1);
+        tc_fence_after();
+      }
+      const int blk = e_blk;
+      const uint32_t eo = tmem + C::TMEM_O + (e_seg % C::NOB) * C::OCOLS;
+      float o[CW];
+      tmem_load_cols<C>(eo + lane_addr + blk * NQ + c0, o);
+      tmem_ld_wait();
+      if (blk == C::NBLK_O - 1) {  // O buffer consumed: the segment after next may reuse it
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&o_empty[e_seg % C::NOB]);
+      }
+      const uint32_t inv_addr = smem_u32(einv_s + (e_seg % C::NOB) * NQ + c0);
+      const int d = blk * 128 + r;
+      if (e_whole) {
+        // bf16 output [row][d]: a register transpose over groups of 8 lanes
+        // (8 consecutive d) turns 32 two-byte stores per thread into CW/8
+        // 16-byte ones (the epilogue was bound by store-instruction issue)
+        static_assert(CW % 8 == 0, "epilogue transpose");
+        uint32_t w[CW / 2];  // stage 0: bf16 pairs (d even, d odd) of CW/2 columns
+        {
+          float v[CW];
+#pragma unroll
+          for (int n = 0; n < CW; n += 4) {
+            const float4 a = ld_shared_f4(inv_addr + n * 4);
+            v[n] = o[n] * a.x; v[n + 1] = o[n + 1] * a.y; v[n + 2] = o[n + 2] * a.z; v[n + 3] = o[n + 3] * a.w;
+          }
+          const bool odd = lane & 1;
+#pragma unroll
+          for (int i = 0; i < CW / 2; ++i) {
+            const float rv = __shfl_xor_sync(0xffffffffu, odd ? v[i] : v[CW / 2 + i], 1);
+            w[i] = odd ? pack_bf16x2(rv, v[CW / 2 + i]) : pack_bf16x2(v[i], rv);
+          }
+        }
+        uint2 x[CW / 4];  // stage 1: 4 consecutive d of CW/4 columns
+        {
+          const bool hi = lane & 2;
+#pragma unroll
+          for (int i = 0; i < CW / 4; ++i) {
+            const uint32_t rv = __shfl_xor_sync(0xffffffffu, hi ? w[i] : w[CW / 4 + i], 2);
+            x[i] = hi ? make_uint2(rv, w[CW / 4 + i]) : make_uint2(w[i], rv);
+          }
+        }
+        const bool hi4 = lane & 4;
+        const int col_base = (lane & 1) * (CW / 2) + ((lane >> 1) & 1) * (CW / 4) + (hi4 ? CW / 8 : 0);
+        const int d8 = blk * 128 + (r & ~7);
+#pragma unroll
+        for (int i = 0; i < CW / 8; ++i) {  // stage 2: 8 consecutive d of CW/8 columns -> one 16-B store each
+          const uint32_t r0 = __shfl_xor_sync(0xffffffffu, hi4 ? x[i].x : x[CW / 8 + i].x, 4);
+          const uint32_t r1 = __shfl_xor_sync(0xffffffffu, hi4 ? x[i].y : x[CW / 8 + i].y, 4);
+          const uint4 y = hi4 ? make_uint4(r0, r1, x[CW / 8 + i].x, x[CW / 8 + i].y)
+                              : make_uint4(x[i].x, x[i].y, r0, r1);
+          const int n = col_base + i;
+          if (n < e_ncols) {
+            const size_t row = e_row0 + n + static_cast<size_t>((e_j0 + n) / p.g_q) * (p.H - p.g_q);
+            *reinterpret_cast<uint4*>(p.out + row * C::D_V + d8) = y;
+          }
+        }
+      } else {
+        float* dst = p.o_part + (static_cast<size_t>(e_slot) * NQ + c0) * C::D_V + d;
+#pragma unroll
+        for (int n = 0; n < CW; n += 4) {
+          const float4 a = ld_shared_f4(inv_addr + n * 4);
+          if (n < e_ncols) dst[n * C::D_V] = o[n] * a.x;
+          if (n + 1 < e_ncols) dst[(n + 1) * C::D_V] = o[n + 1] * a.y;
+          if (n + 2 < e_ncols) dst[(n + 2) * C::D_V] = o[n + 2] * a.z;
+          if (n + 3 < e_ncols) dst[(n + 3) * C::D_V] = o[n + 3] * a.w;
+        }
+      }
+      ++e_blk;
+    };
     int k = 0, u = 0, seg = 0, it = 0;
     Seg s;
     while (next_seg(k, u, s)) {
@@ -1675,9 +1760,11 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
         if (lane == 0) mbar_arrive(&p_full[it % NS]);
         if (trace && threadIdx.x == 128 && it < kTraceTiles) trace[11 + 12 * it] = globaltimer();
         if (trace && threadIdx.x == 256 && it < kTraceTiles) trace[14 + 12 * it] = globaltimer();
+        if (e_blk < C::NBLK_O) epi_block();  // the previous segment's O, one block per tile
       }
 
       // ------------------------------------------------------- segment epilogue
+      while (e_blk < C::NBLK_O) epi_block();  // (a segment shorter than NBLK_O tiles)
       const float cs = warp_col_reduce<HC, false, LANES>(l, lane);
       if ((lane & ((1 << col_shift<HC, LANES>()) - 1)) == 0)
         red[(wg * 4 + wq) * 32 + (cb - c0) + ((lane & (LANES - 1)) >> col_shift<HC, LANES>())] = cs;
@@ -1699,61 +1786,33 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
           }
         }
       }
-      named_bar_sync(bar_id, 128);
-      const int j = it - 1;  // last tile of this segment
-      mbar_wait(&pv_done[j & 3], (j >> 2) & 1);
-      tc_fence_after();
-      // 1/l of this WG's columns, and (whole units) the output row of column
-      // c0: rows advance by one within a query position's g_q heads and jump
-      // to the next position's row block after g_q columns (no per-element
-      // integer division or 64-bit index math: the epilogue is on the
-      // critical path of the next segment)
-      float inv_l[CW];
-#pragma unroll
-      for (int n = 0; n < CW; n += 4) {
-        const float4 a = ld_shared_f4(ao_addr + n * 4);
-        inv_l[n] = a.x; inv_l[n + 1] = a.y; inv_l[n + 2] = a.z; inv_l[n + 3] = a.w;
-      }
-      const int ncols = min(CW, s.nq - c0);
-      int j0 = 0;
-      size_t row0 = 0;
+      // pending epilogue of this segment: 1/l to einv_s, output addressing
+      // (whole units: the output row of column c0; rows advance by one within
+      // a query position's g_q heads and jump to the next position's row
+      // block after g_q columns, no per-element division)
+      if (r < CW) einv_s[(seg % C::NOB) * NQ + c0 + r] = alpha_s[c0 + r];
+      e_blk = 0;
+      e_seg = seg;
+      e_j = it - 1;  // last tile of this segment
+      e_whole = s.whole;
+      e_slot = slot;
+      e_ncols = min(CW, s.nq - c0);
+      e_j0 = 0;
+      e_row0 = 0;
       if (s.whole) {
         const int ng = s.n0 + c0, t = ng / p.g_q;
-        j0 = ng - t * p.g_q;
-        row0 = (static_cast<size_t>(s.b) * p.Lq + t) * p.H + s.head * p.g_q + j0;
+        e_j0 = ng - t * p.g_q;
+        e_row0 = (static_cast<size_t>(s.b) * p.Lq + t) * p.H + s.head * p.g_q + e_j0;
       }
-      const int jump = (p.H - p.g_q) * C::D_V;
-#pragma unroll
-      for (int blk = 0; blk < C::NBLK_O; ++blk) {
-        float o[CW];
-        tmem_load_cols<C>(obuf + lane_addr + blk * NQ + c0, o);
-        tmem_ld_wait();
-        if (blk == C::NBLK_O - 1) {  // O buffer consumed: the segment after next may reuse it
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&o_empty[seg % C::NOB]);
-        }
-        const int d = blk * 128 + r;
-        if (s.whole) {
-          __nv_bfloat16* dst = p.out + row0 * C::D_V + d;
-          int j = j0;
-#pragma unroll
-          for (int n = 0; n < CW; ++n) {
-            if (n < ncols) *dst = __float2bfloat16(o[n] * inv_l[n]);
-            dst += C::D_V;
-            if (++j == p.g_q) { j = 0; dst += jump; }
-          }
-        } else {
-          float* dst = p.o_part + (static_cast<size_t>(slot) * NQ + c0) * C::D_V + d;
-#pragma unroll
-          for (int n = 0; n < CW; ++n)
-            if (n < ncols) dst[n * C::D_V] = o[n] * inv_l[n];
-        }
+      named_bar_sync(bar_id, 128);  // alpha_s / m_run / einv_s settled before the next segment resets them
+      // one O buffer (MLA): the next segment's first PV needs it, write it now
+      if constexpr (C::NOB == 1) {
+        while (e_blk < C::NBLK_O) epi_block();
       }
-      named_bar_sync(bar_id, 128);  // alpha_s / m_run reads done before the next segment resets them
       if (trace && threadIdx.x == 128 && it - 1 < kTraceTiles) trace[15 + 12 * (it - 1)] = globaltimer();
       ++seg;
     }
+    while (e_blk < C::NBLK_O) epi_block();  // the last segment's O
   }
 
   tc_fence_before();
