@@ -180,14 +180,18 @@ GLAD_API glad_status glad_splitkv_combine(const float* o_part, const float* lse_
  * Debug only: when device_buf != NULL every subsequent decode launch writes a
  * per-CTA timeline (globaltimer ns; layout in csrc/decode.cuh, kTraceStride
  * uint64 per CTA, CTAs in launch order) into it.  The caller sizes it for
- * the grid.  NULL turns tracing off (the default).  Not thread-safe.
+ * the grid.  NULL turns tracing off (the default).  Only a library built
+ * with -DGLAD_TRACE=1 (libglad_trace.so, tools/trace.py) records anything.
+ * Not thread-safe.
  */
 GLAD_API void glad_debug_set_trace(void* device_buf);
 /* Debug/benchmark only: bit mask of the decode call's kernels to launch,
  * 1 = plan, 2 = decode, 4 = merge (default 7; used to time the decode kernel
  * alone), plus A/B switches: 8 = cluster multicast for multi-block units,
  * 16 = no rows mode (64-row swap-AB blocks), 32 = cooperative cp.async
- * producer instead of TMA gather4 for pages < 16.  Not thread-safe. */
+ * producer instead of TMA gather4 for pages < 16, 64 = load-only decode
+ * (KV tiles streamed and released, no QK / softmax / PV; the output is
+ * undefined — measures the memory side alone).  Not thread-safe. */
 GLAD_API void glad_debug_set_phase_mask(int32_t mask);
 /* Debug/benchmark only: force the KV tile height (64, 96 or 128 tokens; 0 =
  * library choice).  Results are identical up to fp32 summation order. */

@@ -332,6 +332,7 @@ glad_status decode_common(Variant v, const void* q, const void* pool, const glad
   p.causal = causal ? 1 : 0;
   p.scale_log2 = scale * 1.4426950408889634f;
   p.trace = g_trace;
+  p.dbg_load_only = (g_phase_mask & 64) ? 1 : 0;
   p.cl_n = cl_n;
 
   cudaStream_t st = static_cast<cudaStream_t>(stream);
@@ -364,7 +365,7 @@ const char* glad_version(void) { return "glad 0.1.0 sm_100a"; }
 
 void glad_debug_set_trace(void* device_buf) { g_trace = static_cast<uint64_t*>(device_buf); }
 
-void glad_debug_set_phase_mask(int32_t mask) { g_phase_mask = mask & 63; }
+void glad_debug_set_phase_mask(int32_t mask) { g_phase_mask = mask & 127; }
 
 void glad_debug_set_tile(int32_t tokens) { g_tile_override = tokens; }
 

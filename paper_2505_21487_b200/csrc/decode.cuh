@@ -70,6 +70,7 @@ struct DecodeParams {
   int32_t q_tma;            // 1: Q via the 3-D tensor map (box (64, q_box_h, q_box_t)); 0: cp.async
   int32_t q_box_h, q_box_t;
   float scale_log2;         // softmax_scale * log2(e)
+  int32_t dbg_load_only;    // debug (phase-mask bit 64): stream the KV tiles only (no QK / softmax / PV; output garbage)
   int cl_n;                 // CTAs per cluster = query blocks per (head, sequence); 1 = no cluster.
                             // With cl_n > 1 the plan is over (head, sequence) groups, the CTAs of a
                             // cluster share each KV tile (TMA multicast) and CTA rank r owns query
@@ -109,6 +110,12 @@ struct DecodeParams {
 #endif
 #ifndef GLAD_NS_CAP
 #define GLAD_NS_CAP 4
+#endif
+#ifndef GLAD_PF_BULK
+#define GLAD_PF_BULK 0  // L2 prefetch: 0 = TMA tensor prefetch of the tile's boxes, 1 = bulk page runs, 2 = bulk, head-0 CTAs only
+#endif
+#ifndef GLAD_PF_EXTRA
+#define GLAD_PF_EXTRA 0  // L2 prefetch distance beyond NS tiles
 #endif
 #ifndef GLAD_SPLIT_STAGES
 #define GLAD_SPLIT_STAGES 1
@@ -757,6 +764,15 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
       const int p0 = tl * T;
       const int ntok = min(T, s.ld_end - p0);
       const int nbox = (ntok + box_rows - 1) / box_rows;
+      if (GLAD_PF_BULK && prefetch) {
+        // L2 prefetch of whole page runs (all heads' columns + RoPE: rows of a
+        // page are contiguous), one bulk prefetch per run
+        if (GLAD_PF_BULK == 2 && s.head != 0) return nbox;
+        for (int bx = lane; bx < nbox; bx += 32)
+          prefetch_l2_bulk(p.pool + static_cast<int64_t>(item_row(bt_row, p0, bx)) * p.row_stride,
+                           static_cast<uint32_t>(box_rows * p.row_stride * 2));
+        return nbox;
+      }
       constexpr int NIT = C::SPLIT ? 3 : 2;
       for (int bx = lane; bx < nbox * NIT; bx += 32)
         issue_item(s, item_row(bt_row, p0, bx / NIT), bx / NIT, bx % NIT, sbase + stage * C::STAGE,
@@ -869,7 +885,7 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
         if (trace && lane == 0 && warp == 0 && it < kTraceTiles) trace[8 + 12 * it] = globaltimer();
         if (C::L2PF && !p.g4 && loader && !pf_ready) {
           pf_advance();
-          for (int i = 0; i < NS + it && pvalid; ++i) pf_advance();
+          for (int i = 0; i < NS + GLAD_PF_EXTRA + it && pvalid; ++i) pf_advance();
           pf_ready = true;
           if (trace && lane == 0 && warp == 0) trace[kTraceStride - 6] = globaltimer();  // debug: prefetch cursor ready
         }
@@ -879,6 +895,28 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
         }
       }
     }
+  } else if (warp == 1 && p.dbg_load_only) {
+    // debug: the memory side alone — release every stage as soon as it landed
+    int k = 0, u = 0, it = 0, seg = 0;
+    Seg s;
+    while (next_seg(k, u, s)) {
+      for (int tl = s.t0; tl < s.t1; ++tl, ++it) {
+        const int stage = it % NS;
+        mbar_wait(&kv_full[stage], (it / NS) & 1);
+        if (C::SPLIT) mbar_wait(&kv_full_hi[stage], (it / NS) & 1);
+        if (lane == 0) {
+          mbar_arrive(&kv_empty[stage]);
+          if (C::SPLIT) mbar_arrive(&kv_empty_hi[stage]);
+        }
+        __syncwarp();
+      }
+      mbar_wait(&q_full[seg % C::NQB], (seg / C::NQB) & 1);  // the Q loader's buffer cycle
+      if (lane == 0) mbar_arrive(&q_empty[seg % C::NQB]);
+      __syncwarp();
+      ++seg;
+    }
+  } else if (warp >= 4 && p.dbg_load_only) {
+    // debug load-only mode: no softmax
   } else if (warp == 1) {
     // ========================= UMMA issuer (warp 1, one elected lane issues) =========================
     // The whole warp runs the scheduler with warp-uniform control flow (every
