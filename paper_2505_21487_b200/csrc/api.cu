@@ -46,17 +46,7 @@ int num_sms() {
   return n;
 }
 
-PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
-  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
-    void* ptr = nullptr;
-    cudaDriverEntryPointQueryResult qr;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &qr) != cudaSuccess ||
-        qr != cudaDriverEntryPointSuccess)
-      return static_cast<PFN_cuTensorMapEncodeTiled_v12000>(nullptr);
-    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
-  }();
-  return fn;
-}
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() { return glad::tensor_map_encoder(); }
 
 glad_status check_layout(const glad_cache_layout* L) {
   if (!L) return fail(GLAD_ERR_INVALID_ARG, "layout is NULL");
@@ -464,9 +454,9 @@ glad_status glad_gla_absorb_query(const void* q_nope, const void* q_pe, const vo
     return fail(GLAD_ERR_UNSUPPORTED, "absorb: no kernel for d_h=%d d_c=%d", d_h, d_c);
   if (B == 0) return GLAD_OK;
   if (!q_nope || !q_pe || !w_uk || !seqlens || !q_out) return fail(GLAD_ERR_INVALID_ARG, "NULL pointer");
-  if (!aligned16(q_nope) || !aligned16(w_uk) || (reinterpret_cast<uintptr_t>(q_out) & 3u) ||
-      (reinterpret_cast<uintptr_t>(q_pe) & 3u))
-    return fail(GLAD_ERR_INVALID_ARG, "q_nope / w_uk must be 16-byte aligned, q_pe / q_out 4-byte aligned");
+  if (d_rope % 8) return fail(GLAD_ERR_INVALID_ARG, "absorb: d_rope=%d must be a multiple of 8", d_rope);
+  if (!aligned16(q_nope) || !aligned16(w_uk) || !aligned16(q_out) || (reinterpret_cast<uintptr_t>(q_pe) & 3u))
+    return fail(GLAD_ERR_INVALID_ARG, "q_nope / w_uk / q_out must be 16-byte aligned, q_pe 4-byte aligned");
   cudaError_t e = glad::launch_absorb_query(q_nope, q_pe, w_uk, seqlens, B, Lq, H, d_h, d_c, d_rope, rope_base, q_out,
                                             static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return fail(GLAD_ERR_CUDA, "absorb launch failed: %s", cudaGetErrorString(e));

@@ -1,13 +1,12 @@
 // The step right before the decode hot path: form the
 // kernel's inputs from the model's raw per-step tensors.
 //
-//  * absorb_query_kernel: q = [ W_UK[h] q_nope  ||  RoPE(q_pe, p_t) ]
+//  * absorbed query: q = [ W_UK[h] q_nope  ||  RoPE(q_pe, p_t) ]
 //    (weight absorption: the per-head key up-projection is folded into
 //    the query so keys never materialise; the decoupled RoPE part is rotated
-//    at the query's position p_t = L_b - Lq + t, R2/R5).  A small batched
-//    GEMM per head (rows = B*Lq, K = d_h, N = d_c) bound by reading W_UK once
-//    per step; warp-level bf16 mma.sync with fp32 accumulation is enough for
-//    it (0.5 GFLOP at C2 vs 8 MB of weights).
+//    at the query's position p_t = L_b - Lq + t, R2/R5): the batched
+//    tcgen05 GEMM of gemm.cuh (TMA-staged operands, TMEM accumulator) with
+//    the RoPE pairs in its epilogue.
 //  * append_rope_kernel: cache row = [ latent || RoPE(k_pe, p) ] written into
 //    the paged pool at position p = seqlens_before[b] + i.
 //
@@ -16,6 +15,7 @@
 // ~4e-3 rad).
 #include <cuda_bf16.h>
 
+#include "gemm.cuh"
 #include "internal.h"
 
 namespace glad {
@@ -33,101 +33,6 @@ __device__ __forceinline__ void rope_pair(float x0, float x1, int pos, int i, in
   sincos(a, &s, &c);
   y0 = static_cast<float>(x0 * c - x1 * s);
   y1 = static_cast<float>(x0 * s + x1 * c);
-}
-
-__device__ __forceinline__ uint32_t ld_b32(const __nv_bfloat16* p) { return *reinterpret_cast<const uint32_t*>(p); }
-
-__device__ __forceinline__ void mma_bf16_16816(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
-                                               uint32_t b0, uint32_t b1) {
-  asm volatile(
-      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
-      "{%0,%1,%2,%3};"
-      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
-      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
-}
-
-constexpr int kRowsPerCta = 64;
-constexpr int kAbsorbThreads = 256;
-
-// CTA = (head h, 64 query rows).  Shared memory: the rows' q_nope [64][d_h]
-// and W_UK[h] [d_c][d_h] (rows padded by 8 elements against bank conflicts).
-// Warp w: rows 16 (w & 3) .. +16, output columns (w >> 2) * d_c / 2 .. + d_c / 2.
-template <int DH, int DC>
-__global__ void __launch_bounds__(kAbsorbThreads) absorb_query_kernel(
-    const __nv_bfloat16* __restrict__ q_nope, const __nv_bfloat16* __restrict__ q_pe,
-    const __nv_bfloat16* __restrict__ w_uk, const int32_t* __restrict__ seqlens, int32_t B, int32_t Lq, int32_t H,
-    int32_t d_R, float rope_base, __nv_bfloat16* __restrict__ q_out) {
-  constexpr int LD = DH + 8;  // padded row (elements)
-  constexpr int NSUB = DC / 2 / 8;
-  extern __shared__ __align__(16) uint8_t smem_raw[];
-  __nv_bfloat16* sq = reinterpret_cast<__nv_bfloat16*>(smem_raw);  // [64][LD]
-  __nv_bfloat16* sw = sq + kRowsPerCta * LD;                       // [DC][LD]
-  const int h = blockIdx.y;
-  const int r0 = blockIdx.x * kRowsPerCta;
-  const int rows = B * Lq;
-  const int nrows = min(kRowsPerCta, rows - r0);
-  const int tid = threadIdx.x;
-  const int DQ = DC + d_R;
-  // stage q_nope rows and W_UK[h] (16-B vectors)
-  constexpr int VR = DH / 8;
-  // (fully unrolled: all of a thread's 16-B loads are in flight at once —
-  // a rolled load -> st.shared loop paid one memory latency per iteration)
-#pragma unroll
-  for (int idx = tid; idx < kRowsPerCta * VR; idx += kAbsorbThreads) {
-    const int r = idx / VR, v = idx - r * VR;
-    uint4 x = make_uint4(0u, 0u, 0u, 0u);
-    if (r < nrows) x = __ldg(reinterpret_cast<const uint4*>(q_nope + (static_cast<int64_t>(r0 + r) * H + h) * DH) + v);
-    *reinterpret_cast<uint4*>(sq + r * LD + v * 8) = x;
-  }
-  const __nv_bfloat16* wh = w_uk + static_cast<int64_t>(h) * DC * DH;
-#pragma unroll
-  for (int idx = tid; idx < DC * VR; idx += kAbsorbThreads) {
-    const int c = idx / VR, v = idx - c * VR;
-    *reinterpret_cast<uint4*>(sw + c * LD + v * 8) = __ldg(reinterpret_cast<const uint4*>(wh + c * DH) + v);
-  }
-  __syncthreads();
-  const int warp = tid >> 5, lane = tid & 31;
-  const int g = lane >> 2, t = lane & 3;
-  const int m0 = 16 * (warp & 3);
-  const int n0 = (warp >> 2) * (DC / 2);
-  float acc[NSUB][4];
-#pragma unroll
-  for (int j = 0; j < NSUB; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.f;
-#pragma unroll
-  for (int k0 = 0; k0 < DH; k0 += 16) {
-    const uint32_t a0 = ld_b32(sq + (m0 + g) * LD + k0 + 2 * t);
-    const uint32_t a1 = ld_b32(sq + (m0 + g + 8) * LD + k0 + 2 * t);
-    const uint32_t a2 = ld_b32(sq + (m0 + g) * LD + k0 + 2 * t + 8);
-    const uint32_t a3 = ld_b32(sq + (m0 + g + 8) * LD + k0 + 2 * t + 8);
-#pragma unroll
-    for (int j = 0; j < NSUB; ++j) {
-      const __nv_bfloat16* wb = sw + (n0 + 8 * j + g) * LD + k0 + 2 * t;
-      mma_bf16_16816(acc[j], a0, a1, a2, a3, ld_b32(wb), ld_b32(wb + 8));
-    }
-  }
-  // absorbed part: rows m0 + g and m0 + g + 8, columns n0 + 8 j + 2 t (+1)
-#pragma unroll
-  for (int half = 0; half < 2; ++half) {
-    const int r = m0 + g + 8 * half;
-    if (r < nrows) {
-      __nv_bfloat16* dst = q_out + (static_cast<int64_t>(r0 + r) * H + h) * DQ + n0 + 2 * t;
-#pragma unroll
-      for (int j = 0; j < NSUB; ++j)
-        *reinterpret_cast<uint32_t*>(dst + 8 * j) = pack_bf16x2(acc[j][2 * half], acc[j][2 * half + 1]);
-    }
-  }
-  // RoPE part of the same rows of head h
-  const double lb = log(static_cast<double>(rope_base));
-  const int np = d_R / 2;
-  for (int idx = tid; idx < nrows * np; idx += kAbsorbThreads) {
-    const int r = idx / np, i = idx - r * np;
-    const int row = r0 + r, b = row / Lq, tq = row - b * Lq;
-    const int pos = seqlens[b] - Lq + tq;
-    const __nv_bfloat16* src = q_pe + (static_cast<int64_t>(row) * H + h) * d_R + 2 * i;
-    float y0, y1;
-    rope_pair(__bfloat162float(src[0]), __bfloat162float(src[1]), pos, i, d_R, lb, y0, y1);
-    *reinterpret_cast<uint32_t*>(q_out + (static_cast<int64_t>(row) * H + h) * DQ + DC + 2 * i) = pack_bf16x2(y0, y1);
-  }
 }
 
 // One warp per new token row: latent copied with 16-B vectors, the RoPE key
@@ -155,36 +60,63 @@ __global__ void append_rope_kernel(__nv_bfloat16* __restrict__ pool, int64_t row
   }
 }
 
-template <int DH, int DC>
-cudaError_t launch_absorb_t(const void* q_nope, const void* q_pe, const void* w_uk, const int32_t* seqlens,
-                            int32_t B, int32_t Lq, int32_t H, int32_t d_R, float rope_base, void* q_out,
-                            cudaStream_t stream) {
-  constexpr int smem = (kRowsPerCta + DC) * (DH + 8) * 2;
-  cudaError_t e = set_func_smem_once(reinterpret_cast<const void*>(absorb_query_kernel<DH, DC>), smem);
-  if (e != cudaSuccess) return e;
-  const dim3 grid((B * Lq + kRowsPerCta - 1) / kRowsPerCta, H);
-  absorb_query_kernel<DH, DC><<<grid, kAbsorbThreads, smem, stream>>>(
-      static_cast<const __nv_bfloat16*>(q_nope), static_cast<const __nv_bfloat16*>(q_pe),
-      static_cast<const __nv_bfloat16*>(w_uk), seqlens, B, Lq, H, d_R, rope_base,
-      static_cast<__nv_bfloat16*>(q_out));
-  return cudaGetLastError();
-}
-
 }  // namespace
 
 bool absorb_supported(int d_h, int d_c) {
   return (d_h == 64 || d_h == 128) && (d_c == 128 || d_c == 256 || d_c == 512);
 }
 
+// q[b,t,h] = [ W_UK[h] q_nope[b,t,h] || RoPE(q_pe[b,t,h], L_b - Lq + t) ] as
+// a batched tcgen05 GEMM over the heads (gemm.cuh): M = B*Lq rows, N = d_c,
+// K = d_h, A = q_nope's rows of head h (3-D map [rows][H][d_h]), B = W_UK[h]
+// (K-major, 3-D map [H][d_c][d_h]); the RoPE pairs in the same epilogue.
 cudaError_t launch_absorb_query(const void* q_nope, const void* q_pe, const void* w_uk, const int32_t* seqlens,
                                 int32_t B, int32_t Lq, int32_t H, int32_t d_h, int32_t d_c, int32_t d_R,
                                 float rope_base, void* q_out, cudaStream_t stream) {
-  if (B * Lq == 0) return cudaSuccess;
-#define GLAD_ABS(DH, DC) \
-  if (d_h == DH && d_c == DC) return launch_absorb_t<DH, DC>(q_nope, q_pe, w_uk, seqlens, B, Lq, H, d_R, rope_base, q_out, stream);
-  GLAD_ABS(64, 128) GLAD_ABS(64, 256) GLAD_ABS(64, 512) GLAD_ABS(128, 128) GLAD_ABS(128, 256) GLAD_ABS(128, 512)
-#undef GLAD_ABS
-  return cudaErrorInvalidValue;
+  const int64_t rows = static_cast<int64_t>(B) * Lq;
+  if (rows == 0) return cudaSuccess;
+  auto enc = tensor_map_encoder();
+  if (!enc) return cudaErrorNotSupported;
+  CUtensorMap ta, tb;
+  {
+    cuuint64_t dims[3] = {static_cast<cuuint64_t>(d_h), static_cast<cuuint64_t>(H), static_cast<cuuint64_t>(rows)};
+    cuuint64_t str[2] = {static_cast<cuuint64_t>(d_h) * 2, static_cast<cuuint64_t>(H) * d_h * 2};
+    cuuint32_t box[3] = {64u, 1u, 128u};
+    cuuint32_t es[3] = {1u, 1u, 1u};
+    if (enc(&ta, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(q_nope), dims, str, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return cudaErrorInvalidValue;
+  }
+  const int BN = 128;  // two+ N tiles per head: more CTAs in flight, the RoPE pairs split between them
+  {
+    cuuint64_t dims[3] = {static_cast<cuuint64_t>(d_h), static_cast<cuuint64_t>(d_c), static_cast<cuuint64_t>(H)};
+    cuuint64_t str[2] = {static_cast<cuuint64_t>(d_h) * 2, static_cast<cuuint64_t>(d_c) * d_h * 2};
+    cuuint32_t box[3] = {64u, static_cast<cuuint32_t>(BN), 1u};
+    cuuint32_t es[3] = {1u, 1u, 1u};
+    if (enc(&tb, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(w_uk), dims, str, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return cudaErrorInvalidValue;
+  }
+  GemmParams gp{};
+  gp.M = static_cast<int32_t>(rows);
+  gp.N = d_c;
+  gp.K = d_h;
+  gp.a_div = 1;
+  gp.out = static_cast<__nv_bfloat16*>(q_out);
+  gp.out_ld = static_cast<int64_t>(H) * (d_c + d_R);
+  gp.out_bstride = d_c + d_R;
+  gp.rope_src = static_cast<const __nv_bfloat16*>(q_pe);
+  gp.seqlens = seqlens;
+  gp.rope_ld = static_cast<int64_t>(H) * d_R;
+  gp.rope_bstride = d_R;
+  gp.rope_col = d_c;
+  gp.d_rope = d_R;
+  gp.Lq = Lq;
+  gp.log2_base = log2(static_cast<double>(rope_base));
+  const dim3 grid(static_cast<unsigned>((rows + 127) / 128), static_cast<unsigned>(d_c / BN), static_cast<unsigned>(H));
+  return d_h == 64 ? launch_gemm<128, false, 1>(ta, tb, gp, grid, stream) : launch_gemm<128, false, 2>(ta, tb, gp, grid, stream);
 }
 
 cudaError_t launch_append_rope(void* pool, int64_t row_stride, int page_size, const int32_t* block_table,
