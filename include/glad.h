@@ -241,6 +241,38 @@ GLAD_API glad_status glad_cache_append_rope(const glad_cache_layout* layout, voi
                                             const void* k_pe, int32_t B, int32_t n_new, float rope_base,
                                             void* stream);
 
+/* ---- prefill: GLA in the materialised form ---- */
+
+/*
+ * Causal self-attention over each prompt in the materialised form of P:48,
+ * sigma(Q K^T + Q_R K_R^T) V, with per-head keys and values up-projected from
+ * the latent (K_h = c_i W_UK[h], V_h = c_i W_UV[h], i = h / (H / h_c)):
+ *   out[b,t,h] = sum_{j <= t} softmax_j( scale * (q_nope[b,t,h] . K_h[j]
+ *                + RoPE(q_pe[b,t,h], t) . RoPE(k_pe[b,j], j)) ) V_h[j]
+ * for t < seqlens[b]; rows t >= seqlens[b] get out = 0, lse = -inf.
+ *  q_nope [B, Lmax, H, d_h], q_pe [B, Lmax, H, d_rope] (unrotated),
+ *  latent [B, Lmax, h_c, d_c], k_pe [B, Lmax, d_rope] (unrotated),
+ *  w_uk, w_uv [H, d_c, d_h] (latent -> per-head key / value), all bf16;
+ *  seqlens [B] int32 (device, prompt lengths <= Lmax); out [B, Lmax, H, d_h]
+ *  bf16 (head space); lse [B, Lmax, H] fp32 natural log.  RoPE as R5.
+ * Steps: two tcgen05 GEMMs materialise [K_h | V_h] rows (+ the rotated
+ * RoPE key) in the workspace, the decode kernels run in rows mode over them
+ * as a dense pool, the outputs are moved to their positions.  The
+ * workspace (glad_gla_prefill_workspace_bytes, 256-byte aligned) holds the
+ * materialised rows: B * ceil(Lmax/64)*64 * (2 H d_h + d_rope) bf16 plus q,
+ * out and the decode workspace.  Supported: d_h = 128, d_rope = 64,
+ * d_c % 64 == 0, H % h_c == 0.
+ */
+GLAD_API size_t glad_gla_prefill_workspace_bytes(int32_t B, int32_t Lmax, int32_t H, int32_t d_h, int32_t d_rope,
+                                                 int32_t num_ctas);
+/* The prefill call itself (see above); launches the two up-projection
+ * GEMMs, the RoPE / query kernels, plan + decode + merge, the output move. */
+GLAD_API glad_status glad_gla_prefill(const void* q_nope, const void* q_pe, const void* latent, const void* k_pe,
+                                      const void* w_uk, const void* w_uv, const int32_t* seqlens, int32_t B,
+                                      int32_t Lmax, int32_t H, int32_t h_c, int32_t d_c, int32_t d_h, int32_t d_rope,
+                                      float softmax_scale, float rope_base, void* out, float* lse, void* workspace,
+                                      size_t ws_bytes, int32_t num_ctas, void* stream);
+
 /* ---- sequence split (context-parallel decode, BASELINE
  * north_star "optional sequence-split for long context merged with an LSE
  * all-gather"; the paper itself splits heads only) ---- */

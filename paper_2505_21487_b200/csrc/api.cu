@@ -69,7 +69,8 @@ int64_t row_width(const glad_cache_layout* L) {
   return static_cast<int64_t>(L->n_heads_kv) * L->d_head + L->d_rope;
 }
 
-enum Variant { kGLA, kMLA, kGTA };
+// kMAT: materialised prefill rows [K_h | V_h] per query head (glad_gla_prefill)
+enum Variant { kGLA, kMLA, kGTA, kMAT };
 
 int g_tile_override = 0;  // debug: force 64 / 96 / 128-token tiles (glad_debug_set_tile)
 
@@ -104,7 +105,7 @@ int tile_tokens(const glad::DecodeKey& k0) {
 // Resident clusters per (kernel, cluster size), queried once.
 int max_clusters(const glad::DecodeKey& k, int cl_n) {
   static std::map<std::tuple<int, int, int, int, int, int>, int> cache;
-  const auto key = std::make_tuple(k.d_v, k.d_kn, k.d_r, k.nq, k.t, cl_n);
+  const auto key = std::make_tuple(k.d_v, k.d_kn, k.d_r, k.nq, k.t * 4096 + k.d_s, cl_n);
   auto it = cache.find(key);
   if (it != cache.end()) return it->second;
   const int n = glad::decode_max_clusters(k, cl_n);
@@ -128,9 +129,12 @@ glad_status decode_geom(Variant v, const glad_cache_layout* L, int32_t Lq, int32
   if (v == kGTA && L->d_rope * 2 != L->d_head)
     return fail(GLAD_ERR_INVALID_ARG, "GTA requires d_rope == d_head/2 (got d_head=%d d_rope=%d)", L->d_head,
                 L->d_rope);
+  if (v == kMAT && (L->d_head % 128 || H != L->n_heads_kv))
+    return fail(GLAD_ERR_INVALID_ARG, "materialised rows need d_head = 2 d_h and one query head per KV head");
   g->g_q = H / L->n_heads_kv;
-  g->key.d_v = L->d_head;
-  g->key.d_kn = (v == kGTA) ? L->d_head / 2 : L->d_head;
+  g->key.d_s = L->d_head;
+  g->key.d_v = (v == kMAT) ? L->d_head / 2 : L->d_head;
+  g->key.d_kn = (v == kGTA || v == kMAT) ? L->d_head / 2 : L->d_head;
   g->key.d_r = L->d_rope;
   const int64_t nq_total = static_cast<int64_t>(Lq) * g->g_q;
   const int maxnq = glad::decode_max_nq(L->d_head);
@@ -141,6 +145,7 @@ glad_status decode_geom(Variant v, const glad_cache_layout* L, int32_t Lq, int32
   glad::DecodeKey kr = g->key;
   kr.nq = 128;
   if (nq_total > 64 && !(g_phase_mask & 16) && glad::decode_rows_supported(kr)) g->key.nq = 128;
+  if (v == kMAT) g->key.nq = 128;  // materialised rows: rows mode only (shorter prompts pad the block)
   g->key.t = tile_tokens(g->key);
   g->n_qblk = static_cast<int>((nq_total + g->key.nq - 1) / g->key.nq);
   if (!glad::decode_supported(g->key))
@@ -209,7 +214,7 @@ glad_status decode_common(Variant v, const void* q, const void* pool, const glad
   const int R = head_groups ? (R0 / L->n_heads_kv) * L->n_heads_kv : R0;
   const int G = R * cl_n;
   const int64_t n_plan = U / cl_n;  // plan entries: units, or (head, sequence) groups
-  const WsLayout wl = ws_layout(U, G, g.key.nq, L->d_head);
+  const WsLayout wl = ws_layout(U, G, g.key.nq, g.key.d_v);
   if (ws == nullptr || ws_bytes < wl.total)
     return fail(GLAD_ERR_WORKSPACE, "workspace %zu bytes < required %zu", ws_bytes, wl.total);
   if (reinterpret_cast<uintptr_t>(ws) & 255u) return fail(GLAD_ERR_INVALID_ARG, "workspace must be 256-byte aligned");
@@ -257,7 +262,7 @@ glad_status decode_common(Variant v, const void* q, const void* pool, const glad
                         static_cast<cuuint64_t>(L->num_pages) * static_cast<cuuint64_t>(L->page_size) / 8};
     cuuint64_t ls[3] = {rs, 128u, 8u * rs};
     // split stages (swap-AB, DecodeCfg::SPLIT): one box per latent half
-    const int box_chunks = glad::decode_split(g.key) ? g.key.d_v / 128 : g.key.d_v / 64;
+    const int box_chunks = glad::decode_split(g.key) ? g.key.d_s / 128 : g.key.d_s / 64;
     cuuint32_t lbx[4] = {64u, 8u, static_cast<cuuint32_t>(box_chunks), static_cast<cuuint32_t>(box_rows / 8)};
     cuuint32_t le[4] = {1u, 1u, 1u, 1u};
     cr = enc(&lmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(pool), ld, ls, lbx, le,
@@ -330,7 +335,7 @@ glad_status decode_common(Variant v, const void* q, const void* pool, const glad
   cudaError_t e = cudaSuccess;
   if (g_phase_mask & 1) {
     e = glad::launch_plan(seqlens, plan, p.n_units, cl_n, B, g.key.t, g.n_qblk, g.key.nq, Lq, g.g_q, p.causal, H,
-                          L->d_head, out, lse, nullptr, st);
+                          g.key.d_v, out, lse, nullptr, st);
     if (e != cudaSuccess) return fail(GLAD_ERR_CUDA, "plan launch failed: %s", cudaGetErrorString(e));
   }
   if (g_phase_mask & 2) {
@@ -339,7 +344,7 @@ glad_status decode_common(Variant v, const void* q, const void* pool, const glad
   }
   if (g_phase_mask & 4) {
     e = glad::launch_merge_split(plan, p.o_part, p.lse_part, G, cl_n, p.n_units, g.key.nq, g.n_qblk, B,
-                                 L->n_heads_kv, head_groups, g.g_q, Lq, H, L->d_head, out, lse, st);
+                                 L->n_heads_kv, head_groups, g.g_q, Lq, H, g.key.d_v, out, lse, st);
     if (e != cudaSuccess) return fail(GLAD_ERR_CUDA, "merge launch failed: %s", cudaGetErrorString(e));
   }
   return GLAD_OK;
@@ -405,7 +410,7 @@ size_t glad_decode_workspace_bytes(const glad_cache_layout* L, int32_t B, int32_
   if (B <= 0 || decode_geom(v, L, Lq, H, &g) != GLAD_OK) return 0;
   const int64_t U = static_cast<int64_t>(B) * L->n_heads_kv * g.n_qblk;
   const int G = num_ctas > 0 ? num_ctas : num_sms();
-  return ws_layout(U, G, g.key.nq, L->d_head).total;
+  return ws_layout(U, G, g.key.nq, g.key.d_v).total;
 }
 
 glad_status glad_gla_decode(const void* q, const void* pool, const glad_cache_layout* layout,
@@ -480,6 +485,90 @@ glad_status glad_cache_append_rope(const glad_cache_layout* layout, void* pool, 
                                            seqlens_before, latent, k_pe, B, n_new, w_lat, layout->d_rope, rope_base,
                                            static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return fail(GLAD_ERR_CUDA, "append_rope launch failed: %s", cudaGetErrorString(e));
+  return GLAD_OK;
+}
+
+// ---- materialised GLA prefill (prefill.cu) ----
+namespace {
+struct PrefillWs {
+  size_t kv, q, out, lse, bt, dec, total;
+  int32_t Lpad, npg;
+  int64_t row_stride;
+  glad_cache_layout layout;
+};
+bool prefill_ws(int32_t B, int32_t Lmax, int32_t H, int32_t d_h, int32_t d_rope, int32_t num_ctas, PrefillWs* w) {
+  if (B < 1 || Lmax < 1 || H < 1 || d_h < 64 || d_rope < 2) return false;
+  auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
+  w->Lpad = (Lmax + 63) / 64 * 64;
+  w->npg = w->Lpad / 64;
+  w->row_stride = static_cast<int64_t>(H) * 2 * d_h + d_rope;
+  w->layout = glad_cache_layout{B * w->npg, 64, H, 2 * d_h, d_rope, 0, w->row_stride};
+  const size_t rows = static_cast<size_t>(B) * Lmax;
+  w->kv = 0;
+  w->q = w->kv + al(static_cast<size_t>(B) * w->Lpad * w->row_stride * 2);
+  w->out = w->q + al(rows * H * (d_h + d_rope) * 2);
+  w->lse = w->out + al(rows * H * d_h * 2);
+  w->bt = w->lse + al(rows * H * 4);
+  w->dec = w->bt + al(static_cast<size_t>(B) * w->npg * 4);
+  DecodeGeom g;
+  if (decode_geom(kMAT, &w->layout, Lmax, H, &g) != GLAD_OK) return false;
+  const int64_t U = static_cast<int64_t>(B) * H * g.n_qblk;
+  const int G = num_ctas > 0 ? num_ctas : num_sms();
+  w->total = w->dec + ws_layout(U, G, g.key.nq, g.key.d_v).total;
+  return true;
+}
+}  // namespace
+
+size_t glad_gla_prefill_workspace_bytes(int32_t B, int32_t Lmax, int32_t H, int32_t d_h, int32_t d_rope,
+                                        int32_t num_ctas) {
+  PrefillWs w;
+  return prefill_ws(B, Lmax, H, d_h, d_rope, num_ctas, &w) ? w.total : 0;
+}
+
+glad_status glad_gla_prefill(const void* q_nope, const void* q_pe, const void* latent, const void* k_pe,
+                             const void* w_uk, const void* w_uv, const int32_t* seqlens, int32_t B, int32_t Lmax,
+                             int32_t H, int32_t h_c, int32_t d_c, int32_t d_h, int32_t d_rope, float softmax_scale,
+                             float rope_base, void* out, float* lse, void* workspace, size_t ws_bytes,
+                             int32_t num_ctas, void* stream) {
+  if (B < 0 || Lmax < 0) return fail(GLAD_ERR_INVALID_ARG, "prefill B=%d Lmax=%d must be >= 0", B, Lmax);
+  if (B == 0 || Lmax == 0) return GLAD_OK;
+  if (h_c < 1 || H % h_c || d_c % 64 || d_c < 64 || !(d_h == 128) || d_rope != 64)
+    return fail(GLAD_ERR_UNSUPPORTED, "prefill: needs H %% h_c == 0, d_c %% 64 == 0, d_h = 128, d_rope = 64 "
+                "(got H=%d h_c=%d d_c=%d d_h=%d d_rope=%d)", H, h_c, d_c, d_h, d_rope);
+  if (!(softmax_scale > 0.f) || !std::isfinite(softmax_scale) || !(rope_base > 1.f))
+    return fail(GLAD_ERR_INVALID_ARG, "prefill: softmax_scale / rope_base invalid");
+  if (!q_nope || !q_pe || !latent || !k_pe || !w_uk || !w_uv || !seqlens || !out || !lse)
+    return fail(GLAD_ERR_INVALID_ARG, "prefill: NULL pointer");
+  if (!aligned16(q_nope) || !aligned16(latent) || !aligned16(w_uk) || !aligned16(w_uv) || !aligned16(out) ||
+      (reinterpret_cast<uintptr_t>(q_pe) & 3u) || (reinterpret_cast<uintptr_t>(k_pe) & 3u))
+    return fail(GLAD_ERR_INVALID_ARG, "prefill: q_nope / latent / w_uk / w_uv / out 16-byte, q_pe / k_pe 4-byte aligned");
+  PrefillWs w;
+  if (!prefill_ws(B, Lmax, H, d_h, d_rope, num_ctas, &w)) return fail(GLAD_ERR_UNSUPPORTED, "prefill: no kernel");
+  if (workspace == nullptr || ws_bytes < w.total)
+    return fail(GLAD_ERR_WORKSPACE, "prefill workspace %zu bytes < required %zu", ws_bytes, w.total);
+  if (reinterpret_cast<uintptr_t>(workspace) & 255u) return fail(GLAD_ERR_INVALID_ARG, "workspace must be 256-byte aligned");
+  char* ws = static_cast<char*>(workspace);
+  void* kv = ws + w.kv;
+  void* qf = ws + w.q;
+  void* of = ws + w.out;
+  float* lf = reinterpret_cast<float*>(ws + w.lse);
+  int32_t* bt = reinterpret_cast<int32_t*>(ws + w.bt);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const double lb = log2(static_cast<double>(rope_base));
+  cudaError_t e = glad::launch_prefill_upproj(latent, w_uk, B, Lmax, w.Lpad, h_c, d_c, H, d_h, kv, w.row_stride, 0, st);
+  if (e == cudaSuccess)
+    e = glad::launch_prefill_upproj(latent, w_uv, B, Lmax, w.Lpad, h_c, d_c, H, d_h, kv, w.row_stride, d_h, st);
+  if (e == cudaSuccess)
+    e = glad::launch_prefill_rope_k(k_pe, B, Lmax, w.Lpad, d_rope, lb, kv, w.row_stride,
+                                    static_cast<int64_t>(H) * 2 * d_h, st);
+  if (e == cudaSuccess) e = glad::launch_prefill_build_q(q_nope, q_pe, seqlens, B, Lmax, H, d_h, d_rope, lb, qf, st);
+  if (e == cudaSuccess) e = glad::launch_prefill_identity_bt(bt, B, w.npg, st);
+  if (e != cudaSuccess) return fail(GLAD_ERR_CUDA, "prefill launch failed: %s", cudaGetErrorString(e));
+  glad_status s = decode_common(kMAT, qf, kv, &w.layout, bt, w.npg, seqlens, B, Lmax, H, softmax_scale, 1, of, lf,
+                                ws + w.dec, w.total - w.dec, num_ctas, stream);
+  if (s != GLAD_OK) return s;
+  e = glad::launch_prefill_shift_out(of, lf, seqlens, B, Lmax, H, d_h, out, lse, st);
+  if (e != cudaSuccess) return fail(GLAD_ERR_CUDA, "prefill launch failed: %s", cudaGetErrorString(e));
   return GLAD_OK;
 }
 

@@ -140,17 +140,17 @@ constexpr int kTraceStride = 8 + 12 * kTraceTiles;
 
 // Rows mode (NQ = 128) fits TMEM: two S buffers [128 x T] + O [128 x D_V] +
 // the query state part [128 x D_V / 2 columns].
-template <int D_V, int T>
+template <int D_V, int D_KN, int T>
 __host__ __device__ constexpr bool rows_fits() {
-  return T <= 96 && 2 * T + D_V + D_V / 2 <= 512;
+  return T <= 96 && 2 * T + D_V + D_KN / 2 <= 512;
 }
 
 // KV stages of the unsplit (interleaved) stage layout; mirrors the NS
 // computation in DecodeCfg with NLO = NCH_V.
-template <int D_V, int D_KN, int D_R, int NQ, int T>
+template <int D_V, int D_KN, int D_R, int NQ, int T, int D_S = D_V>
 __host__ __device__ constexpr int ns_nosplit() {
   constexpr bool rows = (NQ == 128);
-  constexpr int nch_v = D_V / 64, nch = nch_v + 1, nqch = D_KN / 64 + 1;
+  constexpr int nch_v = D_S / 64, nch = nch_v + 1, nqch = D_KN / 64 + 1;
   constexpr int chunk = T * 128, stage = nch * chunk, lgrp = nch_v * 1024, off_r = nch_v * chunk;
   constexpr int qbytes = rows ? NQ * 128 : nqch * NQ * 128;
   constexpr int aux = 3072 + 64 * 32 + T * 4 + (rows ? 1024 : 2 * NQ * 4);
@@ -161,10 +161,16 @@ __host__ __device__ constexpr int ns_nosplit() {
   return (avail - qbytes - 2 * pbuf - xtra) / stage;
 }
 
-template <int D_V_, int D_KN_, int D_R_, int NQ_, int T_ = 128>
+template <int D_V_, int D_KN_, int D_R_, int NQ_, int T_ = 128, int D_S_ = D_V_>
 struct DecodeCfg {
-  static constexpr int D_V = D_V_;    // value width (= state width)
+  // Per head, each token's cache row holds a state slice of D_S columns:
+  // the key part is its first D_KN columns, the value its last D_V (GLA /
+  // MLA: the latent is both, D_KN = D_V = D_S; GTA: the tied state, key =
+  // its first half; materialised prefill: [K_h | V_h], D_S = D_KN + D_V).
+  static constexpr int D_V = D_V_;    // value width
   static constexpr int D_KN = D_KN_;  // key part taken from the state
+  static constexpr int D_S = D_S_;    // state columns loaded per head and token
+  static constexpr int V_CH0 = (D_S_ - D_V_) / 64;  // first value chunk (64 columns) of the state
   static constexpr int D_R = D_R_;    // rope width
   static constexpr int NQ = NQ_;      // query rows per unit (UMMA N; UMMA M in rows mode)
   // Rows mode (NQ = 128): query rows on UMMA M, tokens on N (S = Q K^T,
@@ -181,7 +187,7 @@ struct DecodeCfg {
   static constexpr int T = T_;
   static constexpr int LANES = 32;  // token lanes per warp quarter in S^T
   static constexpr int DQ = D_KN + D_R;
-  static constexpr int NCH_V = D_V / 64;
+  static constexpr int NCH_V = D_S / 64;  // state chunks in a stage
   static constexpr int NCH = NCH_V + 1;  // + rope chunk
   static constexpr int NCH_QK = D_KN / 64;
   static constexpr int NQCH = NCH_QK + 1;
@@ -203,7 +209,7 @@ struct DecodeCfg {
   // Measured slower with three or more stages (C4 GTA 0.391 -> 0.421 ms:
   // the extra TMA issues and barrier round trips cost more than the earlier
   // refill gains) and for MLA's 64-token tiles (0.553 -> 0.594 ms).
-  static constexpr int NS_NOSPLIT = ns_nosplit<D_V_, D_KN_, D_R_, NQ_, T_>();
+  static constexpr int NS_NOSPLIT = ns_nosplit<D_V_, D_KN_, D_R_, NQ_, T_, D_S_>();
   static constexpr bool SPLIT = !ROWS && T == 128 && NS_NOSPLIT <= 2 && GLAD_SPLIT_STAGES;
   static constexpr int NLO = SPLIT ? NCH_V / 2 : NCH_V;  // chunks per half (per stage when not split)
   static constexpr int LO_BYTES = NLO * CHUNK;
@@ -285,6 +291,8 @@ struct DecodeCfg {
   static_assert(QCHUNK % 1024 == 0, "Q chunk alignment");
   static_assert(T == 128 || T == 96 || T == 64, "tile height");
   static_assert(!SPLIT || NCH_V % 2 == 0, "split stages need an even number of latent chunks");
+  static_assert(!SPLIT || V_CH0 == 0, "split stages: value = the state's first columns");
+  static_assert(D_S % 64 == 0 && D_S >= D_V && D_S >= D_KN && (D_S == D_V || D_S == D_KN + D_V), "state layout");
 };
 
 // Column reduction over groups of LANES lanes (32, or 16 for the halves of a
@@ -964,7 +972,7 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
             tc_fence_after();
             const int j = next_pv;
             const int stage = j % NS;
-            const uint64_t bd = desc_mnmajor_sw128(sbase + stage * C::STAGE, 1024, C::LGRP);
+            const uint64_t bd = desc_mnmajor_sw128(sbase + stage * C::STAGE + C::V_CH0 * 1024, 1024, C::LGRP);
             const uint32_t obuf = tm + C::TMEM_O + (cp.seg % C::NOB) * C::OCOLS;
             const uint64_t pd = desc_kmajor_sw128(sbase + C::OFF_P + (j & 1) * C::PBUF);
 #pragma unroll
@@ -1129,7 +1137,7 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
         for (int blk = 0; blk < C::NBLK_O; ++blk) {
 #pragma unroll
           for (int k = 0; k < T / 16; ++k)
-            umma_f16_ss_warp(obuf + blk * NQ, ad + static_cast<uint64_t>((C::chunk_off(2 * blk) + k * 2 * C::LGRP) >> 4),
+            umma_f16_ss_warp(obuf + blk * NQ, ad + static_cast<uint64_t>((C::chunk_off(C::V_CH0 + 2 * blk) + k * 2 * C::LGRP) >> 4),
                              bd + static_cast<uint64_t>((C::P_SW128 ? k * 2048 : k * 256) >> 4), idesc_pv,
                              (!first || k > 0) ? 1u : 0u);
           // lo half read by every block up to here: the producer may refill it

@@ -7,6 +7,8 @@ namespace glad {
 int decode_max_nq(int) { return 64; }
 
 bool decode_rows_supported(const DecodeKey& k) {
+  if (k.d_s == 2 * k.d_v) return k.d_v == 128 && k.d_kn == 128 && k.d_r == 64;  // materialised prefill rows
+  if (k.d_kn == 64 && k.d_v == 128 && k.d_r == 64) return true;                   // GTA
   return k.d_kn == k.d_v && (k.d_v == 128 || k.d_v == 256) && (k.d_r == 32 || k.d_r == 64);
 }
 
@@ -15,7 +17,8 @@ bool decode_supported(const DecodeKey& k) {
   // rows mode: 64- and 96-token tiles whose S buffers, O and the query
   // state part fit TMEM (rows_fits; 128-token tiles faulted on the second
   // tile when they still fitted, before Q moved to TMEM)
-  if (k.nq == 128) return decode_rows_supported(k) && (k.t == 64 || k.t == 96) && 2 * k.t + k.d_v + k.d_v / 2 <= 512;
+  if (k.nq == 128) return decode_rows_supported(k) && (k.t == 64 || k.t == 96) && 2 * k.t + k.d_v + k.d_kn / 2 <= 512;
+  if (k.d_s != k.d_v) return false;  // materialised rows: rows mode only
   if (k.nq != 16 && k.nq != 32 && k.nq != 64) return false;
   if (k.nq > decode_max_nq(k.d_v)) return false;
   if (k.d_kn == k.d_v) {  // GLA / MLA: key state == value state

@@ -12,10 +12,10 @@ cudaError_t set_smem_attr() {
   return set_func_smem_once(reinterpret_cast<const void*>(decode_kernel<C>), C::SMEM_BYTES);
 }
 
-template <int DV, int DKN, int DR, int NQ, int T>
+template <int DV, int DKN, int DR, int NQ, int T, int DS>
 cudaError_t launch_one(const CUtensorMap& tmap, const CUtensorMap& lmap, const CUtensorMap& qmap,
                        const DecodeParams& p, int grid, cudaStream_t stream) {
-  using C = DecodeCfg<DV, DKN, DR, NQ, T>;
+  using C = DecodeCfg<DV, DKN, DR, NQ, T, DS>;
   cudaError_t e = set_smem_attr<C>();
   if (e != cudaSuccess) return e;
   if (p.cl_n <= 1) {
@@ -55,9 +55,15 @@ cudaError_t with_cfg(const DecodeKey& k, F&& f) {
     case 32: return f.template run<DecodeCfg<DV, DV, DR, 32, T>>();           \
     case 64: return f.template run<DecodeCfg<DV, DV, DR, 64, T>>();           \
     case 128:                                                                 \
-      if constexpr (rows_fits<DV, T>()) return f.template run<DecodeCfg<DV, DV, DR, 128, T>>(); \
+      if constexpr (rows_fits<DV, DV, T>()) return f.template run<DecodeCfg<DV, DV, DR, 128, T>>(); \
       else return cudaErrorInvalidValue;                                      \
     default: return cudaErrorInvalidValue;                                    \
+  }
+  if (k.d_s == 2 * k.d_v) {  // materialised [K_h | V_h] rows (prefill): rows mode only
+    if (k.d_v == 128 && k.d_kn == 128 && k.d_r == 64 && k.nq == 128) {
+      if constexpr (rows_fits<128, 128, T>()) return f.template run<DecodeCfg<128, 128, 64, 128, T, 256>>();
+    }
+    return cudaErrorInvalidValue;
   }
   if (k.d_kn == k.d_v) {
     if (k.d_v == 128 && k.d_r == 32) { GLAD_NQ_R(128, 32) }
@@ -65,7 +71,11 @@ cudaError_t with_cfg(const DecodeKey& k, F&& f) {
     if (k.d_v == 256 && k.d_r == 32) { GLAD_NQ_R(256, 32) }
     if (k.d_v == 256 && k.d_r == 64) { GLAD_NQ_R(256, 64) }
     if (k.d_v == 512 && k.d_r == 64) { GLAD_NQ(512, 512, 64) }
-  } else if (k.d_v == 128 && k.d_kn == 64 && k.d_r == 64) {
+  } else if (k.d_v == 128 && k.d_kn == 64 && k.d_r == 64) {  // GTA (tied state, key = its first half)
+    if (k.nq == 128) {
+      if constexpr (rows_fits<128, 64, T>()) return f.template run<DecodeCfg<128, 64, 64, 128, T>>();
+      return cudaErrorInvalidValue;
+    }
     GLAD_NQ(128, 64, 64)
   }
 #undef GLAD_NQ
@@ -80,7 +90,7 @@ struct LaunchF {
   cudaStream_t s;
   template <class C>
   cudaError_t run() {
-    return launch_one<C::D_V, C::D_KN, C::D_R, C::NQ, C::T>(tmap, lmap, qmap, p, grid, s);
+    return launch_one<C::D_V, C::D_KN, C::D_R, C::NQ, C::T, C::D_S>(tmap, lmap, qmap, p, grid, s);
   }
 };
 

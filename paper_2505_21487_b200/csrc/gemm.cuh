@@ -33,8 +33,9 @@ namespace glad {
 struct GemmParams {
   int32_t M, N, K;          // per batch
   int32_t a_div;            // A's batch coordinate = z / a_div
-  __nv_bfloat16* out;       // D[z][m][n] at out + z * out_bstride + m * out_ld + n
+  __nv_bfloat16* out;       // D[z][m][n] at out + z * out_bstride + row(m) * out_ld + n
   int64_t out_ld, out_bstride;
+  int32_t seg_len, seg_pad;  // row(m) = (m / seg_len) * seg_pad + m % seg_len (seg_len = 0: row(m) = m)
   // optional RoPE epilogue (absorbed query, R5): rows m = b * Lq + t at position
   // seqlens[b] - Lq + t; pairs of rope_src + (m * rope_ld + z * rope_bstride)
   // rotated into out + z * out_bstride + m * out_ld + rope_col
@@ -191,7 +192,8 @@ __global__ void __launch_bounds__(256)
   tc_fence_after();
   const int row = m0 + threadIdx.x;
   const uint32_t taddr = tmem + (static_cast<uint32_t>(warp * 32) << 16);
-  __nv_bfloat16* orow = p.out + static_cast<int64_t>(z) * p.out_bstride + static_cast<int64_t>(row) * p.out_ld + n0;
+  const int64_t orow_idx = p.seg_len ? static_cast<int64_t>(row / p.seg_len) * p.seg_pad + row % p.seg_len : row;
+  __nv_bfloat16* orow = p.out + static_cast<int64_t>(z) * p.out_bstride + orow_idx * p.out_ld + n0;
 #pragma unroll 1
   for (int c = 0; c < BN; c += 32) {
     float v[32];

@@ -51,6 +51,7 @@ inline PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
 // rows per CTA.
 struct DecodeKey {
   int d_v, d_kn, d_r, nq, t;  // t: tokens per KV tile (64 / 96 / 128)
+  int d_s;                    // state columns loaded per head (d_v, or d_kn + d_v for materialised K | V rows)
 };
 
 // Returns cudaErrorInvalidValue (and does not launch) if no instantiation
@@ -84,6 +85,18 @@ cudaError_t launch_append_rope(void* pool, int64_t row_stride, int page_size, co
                                int32_t bt_stride, const int32_t* seqlens_before, const void* latent,
                                const void* k_pe, int32_t B, int32_t n_new, int32_t w_lat, int32_t d_R,
                                float rope_base, cudaStream_t stream);
+// materialised GLA prefill helpers (prefill.cu)
+cudaError_t launch_prefill_upproj(const void* latent, const void* w, int32_t B, int32_t Lmax, int32_t Lpad,
+                                  int32_t h_c, int32_t d_c, int32_t H, int32_t d_h, void* kv, int64_t row_stride,
+                                  int32_t col_off, cudaStream_t s);
+cudaError_t launch_prefill_build_q(const void* q_nope, const void* q_pe, const int32_t* seqlens, int32_t B,
+                                   int32_t Lmax, int32_t H, int32_t d_h, int32_t d_R, double log2_base, void* q_full,
+                                   cudaStream_t s);
+cudaError_t launch_prefill_rope_k(const void* k_pe, int32_t B, int32_t Lmax, int32_t Lpad, int32_t d_R,
+                                  double log2_base, void* kv, int64_t row_stride, int64_t rope_col, cudaStream_t s);
+cudaError_t launch_prefill_identity_bt(int32_t* bt, int32_t B, int32_t npg, cudaStream_t s);
+cudaError_t launch_prefill_shift_out(const void* out_full, const float* lse_full, const int32_t* seqlens, int32_t B,
+                                     int32_t Lmax, int32_t H, int32_t d_h, void* out, float* lse, cudaStream_t s);
 cudaError_t launch_lse_rescale(const float* lse_all, int32_t P, int32_t rank, const void* o, int64_t rows,
                                int32_t d_v, void* o_out, float* lse_out, cudaStream_t stream);
 cudaError_t launch_combine(const float* o_part, const float* lse_part, int32_t S, int64_t rows, int32_t d_v,

@@ -79,6 +79,9 @@ def _sig(lib):
         "glad_seq_split_rescale": ([_VP, ctypes.c_int32, ctypes.c_int32, _VP, ctypes.c_int64, ctypes.c_int32, _VP, _VP,
                                     _VP], S),
         "glad_kv_bytes_per_token_per_device": ([ctypes.c_int32] * 6, ctypes.c_int64),
+        "glad_gla_prefill_workspace_bytes": ([ctypes.c_int32] * 6, ctypes.c_size_t),
+        "glad_gla_prefill": ([_VP] * 7 + [ctypes.c_int32] * 7 + [ctypes.c_float, ctypes.c_float, _VP, _VP, _VP,
+                                                                  ctypes.c_size_t, ctypes.c_int32, _VP], S),
     }
     for name, (args, res) in table.items():
         f = getattr(lib, name)
@@ -103,7 +106,7 @@ def exported_symbols():
             "glad_decode_workspace_bytes", "glad_gla_decode", "glad_mla_decode",
             "glad_gta_decode", "glad_splitkv_combine", "glad_tp_duplication", "glad_tp_shard",
             "glad_seq_split_range", "glad_seq_split_rescale", "glad_gla_absorb_query", "glad_cache_append_rope",
-            "glad_kv_bytes_per_token_per_device"]
+            "glad_kv_bytes_per_token_per_device", "glad_gla_prefill_workspace_bytes", "glad_gla_prefill"]
 
 
 def _check(status):
@@ -282,6 +285,44 @@ def cache_append_rope(layout, pool, block_table, seqlens_before, latent, k_pe, r
     _check(lib().glad_cache_append_rope(ctypes.byref(layout), _ptr(pool), _ptr(block_table),
                                         block_table.shape[-1], _ptr(seqlens_before), _ptr(latent),
                                         _ptr(k_pe), B, n, float(rope_base), _stream(stream)))
+
+
+def gla_prefill_workspace_bytes(B, Lmax, H, d_h, d_rope, num_ctas=0):
+    return lib().glad_gla_prefill_workspace_bytes(B, Lmax, H, d_h, d_rope, num_ctas)
+
+
+def gla_prefill(q_nope, q_pe, latent, k_pe, w_uk, w_uv, seqlens, softmax_scale, rope_base=10000.0, out=None,
+                lse=None, num_ctas=0, workspace=None, stream=None):
+    """Causal GLA prefill in the materialised form (glad_gla_prefill).  q_nope [B,L,H,d_h], q_pe [B,L,H,d_R],
+    latent [B,L,h_c,d_c], k_pe [B,L,d_R] (unrotated), w_uk / w_uv [H,d_c,d_h] bf16, seqlens [B] int32 (device).
+    Returns out [B,L,H,d_h] bf16 (head space), lse [B,L,H] fp32."""
+    for t, n in ((q_nope, "q_nope"), (q_pe, "q_pe"), (latent, "latent"), (k_pe, "k_pe"), (w_uk, "w_uk"),
+                 (w_uv, "w_uv")):
+        _need(t, torch.bfloat16, n)
+    _need(seqlens, torch.int32, "seqlens")
+    B, L, H, d_h = q_nope.shape
+    h_c, d_c = latent.shape[2], latent.shape[3]
+    d_R = q_pe.shape[-1]
+    if tuple(q_pe.shape[:3]) != (B, L, H) or tuple(latent.shape[:2]) != (B, L) or tuple(k_pe.shape) != (B, L, d_R):
+        raise ValueError("q_pe / latent / k_pe shapes do not match q_nope")
+    if tuple(w_uk.shape) != (H, d_c, d_h) or tuple(w_uv.shape) != (H, d_c, d_h):
+        raise ValueError(f"w_uk / w_uv must be (H, d_c, d_h) = ({H}, {d_c}, {d_h})")
+    if tuple(seqlens.shape) != (B,):
+        raise ValueError("seqlens must be [B]")
+    if out is None:
+        out = torch.empty(B, L, H, d_h, dtype=torch.bfloat16, device=q_nope.device)
+    if lse is None:
+        lse = torch.empty(B, L, H, dtype=torch.float32, device=q_nope.device)
+    nbytes = gla_prefill_workspace_bytes(B, L, H, d_h, d_R, num_ctas)
+    if nbytes == 0:
+        raise GladError(GLAD_ERR_UNSUPPORTED, "prefill: unsupported shape")
+    if workspace is None:
+        workspace = Workspace(q_nope.device)
+    ws = workspace.get(nbytes)
+    _check(lib().glad_gla_prefill(_ptr(q_nope), _ptr(q_pe), _ptr(latent), _ptr(k_pe), _ptr(w_uk), _ptr(w_uv),
+                                  _ptr(seqlens), B, L, H, h_c, d_c, d_h, d_R, float(softmax_scale), float(rope_base),
+                                  _ptr(out), _ptr(lse), _ptr(ws), nbytes, num_ctas, _stream(stream)))
+    return out, lse
 
 
 def seq_split_range(L, page_size, Lq, P, rank):
