@@ -40,6 +40,8 @@ class Workload:
     scale: float = 1.0
     seed: int = 1
     description: str = ""
+    kind: str = "decode"  # "decode" | "prefill_mat" (glad_gla_prefill, materialised K / V)
+    d_h: int = 128        # per-head width of the materialised prefill
 
     @property
     def d_qk(self):
@@ -83,6 +85,12 @@ WORKLOADS = {w.name: w for w in [
     # prefill in the absorbed form: every prompt token is a query (Lq = L)
     Workload("c6_prefill_gla2", "gla", 2, 4096, 128, 2, 256, 64, 4096, page=64, scale=1 / math.sqrt(192), seed=6,
              description="GLA-2 prefill as a full-length causal query: B=2, L=Lq=4096, h_q=128, 2x256 + 64"),
+    # prefill in the materialised form: per-head K / V up-projected, then attention over them
+    Workload("c6_prefill_gla2_mat", "gla", 2, 4096, 128, 2, 256, 64, 4096, page=64, scale=1 / math.sqrt(192), seed=6,
+             kind="prefill_mat", d_h=128,
+             description="GLA-2 prefill, materialised K/V (d_h 128 + RoPE 64): B=2, L=4096, h_q=128, d_c=256"),
+    Workload("c7_prefill_gta", "gta", 2, 4096, 64, 8, 128, 64, 4096, page=64, scale=1 / math.sqrt(128), seed=7,
+             description="GTA prefill as a full-length causal query: B=2, L=Lq=4096, h_q=64, 8 tied heads d_h=128"),
     # page-size ablation (page 1 vs 64 for GLA 2x256+64)
     Workload("c2_gla2_p1", "gla", 128, 1, 128, 2, 256, 64, 8192, page=1, scale=1 / math.sqrt(192), seed=1,
              description="C2 GLA-2 with page size 1 (prefix caching, P:316)"),
@@ -106,18 +114,44 @@ def visible_counts(seqlens, Lq, causal):
 
 
 def algorithmic_bytes(wl, seqlens):
+    if wl.kind == "prefill_mat":  # raw inputs once + weights + output
+        n = int(np.sum(seqlens))
+        return int(2 * (n * wl.H * (wl.d_h + wl.d_R) + n * (wl.h_c * wl.d_c + wl.d_R) + 2 * wl.H * wl.d_c * wl.d_h
+                        + n * wl.H * wl.d_h) + 4 * n * wl.H)
     rows = wl.B * wl.Lq * wl.H
     return int(np.sum(seqlens, dtype=np.int64) * wl.width * 2 + rows * wl.d_qk * 2 + rows * wl.d_v * 2 + rows * 4)
 
 
 def algorithmic_flops(wl, seqlens):
-    return int(2 * wl.H * (wl.d_qk + wl.d_v) * visible_counts(seqlens, wl.Lq, wl.causal).sum())
+    vis = visible_counts(seqlens, wl.Lq, wl.causal).sum()
+    if wl.kind == "prefill_mat":  # attention over d_h + d_R keys, d_h values, plus the K / V up-projections
+        return int(2 * wl.H * (2 * wl.d_h + wl.d_R) * vis + 2 * 2 * int(np.sum(seqlens)) * wl.H * wl.d_c * wl.d_h)
+    return int(2 * wl.H * (wl.d_qk + wl.d_v) * vis)
+
+
+def build_prefill_state(wl, seed=None, device="cuda", num_ctas=0):
+    """Raw GLA tensors of a prompt batch, drawn on the device (materialised prefill)."""
+    seed = wl.seed if seed is None else seed
+    sl = wl.seqlens()
+    B, L, H = wl.B, wl.L, wl.H
+    g = lambda shape, k, std=1.0: synth.normal_bf16(shape, seed * 11 + k, std=std, device=device)
+    st = dict(q_nope=g((B, L, H, wl.d_h), 1), q_pe=g((B, L, H, wl.d_R), 2), c=g((B, L, wl.h_c, wl.d_c), 3),
+              k_pe=g((B, L, wl.d_R), 4), W_UK=g((H, wl.d_c, wl.d_h), 5, 1.0 / math.sqrt(wl.d_c)),
+              W_UV=g((H, wl.d_c, wl.d_h), 6, 1.0 / math.sqrt(wl.d_c)),
+              seqlens=torch.from_numpy(sl.astype(np.int32)).to(device), seqlens_host=sl, num_ctas=num_ctas,
+              out=torch.empty(B, L, H, wl.d_h, dtype=torch.bfloat16, device=device),
+              lse=torch.empty(B, L, H, dtype=torch.float32, device=device), workspace=glad.Workspace(device))
+    st["workspace"].get(glad.gla_prefill_workspace_bytes(B, L, H, wl.d_h, wl.d_R, num_ctas))
+    st["q"] = st["q_nope"]
+    return st
 
 
 def build_device_state(wl, seed=None, device="cuda", num_ctas=0):
     """Seeded synthetic device state: pool of N(0,1) bf16 rows (pages are a
     random permutation), block table, seqlens, queries, preallocated outputs
     and split workspace (so the step is CUDA-graph capturable)."""
+    if wl.kind == "prefill_mat":
+        return build_prefill_state(wl, seed, device, num_ctas)
     seed = wl.seed if seed is None else seed
     sl = wl.seqlens()
     bt, num_pages = synth.block_table(sl, wl.page, seed=seed)
@@ -136,6 +170,10 @@ def build_device_state(wl, seed=None, device="cuda", num_ctas=0):
 
 def run(wl, st, stream=None, q=None):
     """One decode step through the C ABI (plan + decode + merge kernels)."""
+    if wl.kind == "prefill_mat":
+        return glad.gla_prefill(st["q_nope"] if q is None else q, st["q_pe"], st["c"], st["k_pe"], st["W_UK"],
+                                st["W_UV"], st["seqlens"], wl.scale, out=st["out"], lse=st["lse"],
+                                num_ctas=st["num_ctas"], workspace=st["workspace"], stream=stream)
     fn = {"gla": glad.gla_decode, "mla": glad.mla_decode, "gta": glad.gta_decode}[wl.variant]
     return fn(st["q"] if q is None else q, st["pool"], st["layout"], st["block_table"], st["seqlens"], wl.scale,
               causal=wl.causal, out=st["out"], lse=st["lse"], num_ctas=st["num_ctas"], workspace=st["workspace"],
