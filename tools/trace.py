@@ -33,8 +33,10 @@ ap.add_argument("--workload", default="c2_gla2")
 ap.add_argument("--ctas", type=int, default=0)
 ap.add_argument("--tile", type=int, default=0)
 ap.add_argument("--ns", type=int, default=2, help="KV stages of the instantiation (for PV->load)")
+ap.add_argument("--mask", type=int, default=7, help="glad_debug_set_phase_mask value")
 a = ap.parse_args()
 wl = workloads.get(a.workload)
+glad.debug_set_phase_mask(a.mask)
 if a.tile:
     glad.debug_set_tile(a.tile)
 st = workloads.build_device_state(wl, num_ctas=a.ctas)
