@@ -97,7 +97,8 @@ def main():
                   f"{traffic:,.0f} B (ratio {traffic / abytes:.3f})."]
         tp = os.path.join(os.path.dirname(a.out), "traffic.json")
         d = json.load(open(tp)) if os.path.exists(tp) else {}
-        d[a.workload] = traffic
+        d[a.workload] = {"bytes": traffic, "source": os.path.relpath(a.out, os.path.dirname(os.path.dirname(
+            os.path.abspath(__file__))))}
         json.dump(d, open(tp, "w"), indent=1, sort_keys=True)
     ls = launches(a.launches)
     if ls:
