@@ -136,7 +136,7 @@ struct DecodeParams {
 #define GLAD_MMA_BACKOFF_NS 0
 #endif
 constexpr int kTraceTiles = 128;
-constexpr int kTraceStride = 8 + 12 * kTraceTiles;
+constexpr int kTraceStride = 8 + 12 * kTraceTiles + 32;  // + 32 per-CTA debug slots at the end
 
 // Rows mode (NQ = 128) fits TMEM: two S buffers [128 x T] + O [128 x D_V] +
 // the query state part [128 x D_V / 2 columns].
@@ -997,6 +997,12 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
         if (!qk_go && qk_left && next_qk - next_pv <= GLAD_ROWS_QK_AHEAD && probe(&kv_full[next_qk % NS], (next_qk / NS) & 1) &&
             probe(&s_empty[next_qk & 1], ((next_qk >> 1) & 1) ^ 1)) {
           const bool first = (cq.tl == cq.t0);
+          if (trace && first && cq.seg > 0 && cq.seg < 8 && lane == 0) {  // debug: when each Q barrier flips
+            const int sl = kTraceStride - 32 + 3 * cq.seg;
+            if (trace[sl] == 0 && mbar_test_wait(smem_u32(&q_full[cq.seg % C::NQB]), (cq.seg / C::NQB) & 1)) trace[sl] = globaltimer();
+            if (trace[sl + 1] == 0 && mbar_test_wait(smem_u32(qn_full), cq.seg & 1)) trace[sl + 1] = globaltimer();
+            if (trace[sl + 2] == 0) trace[sl + 2] = globaltimer();  // first probe of this segment's first QK
+          }
           if (!first || (probe(&q_full[cq.seg % C::NQB], (cq.seg / C::NQB) & 1) && probe(qn_full, cq.seg & 1))) {
             qk_go = true;
             if (trace && lane == 0 && next_qk == 0) trace[1] = globaltimer();
@@ -1450,6 +1456,7 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
       Seg sn;
       const bool have_n = next_seg(k, u, sn);
       if (have_n) load_q(sn);
+      if (trace && threadIdx.x == 128 && it - 1 < kTraceTiles) trace[18 + 12 * (it - 1)] = globaltimer();  // next Q in TMEM
       // ---- segment epilogue: O / l, lse (natural log); each WG writes its O half
       float ls = l2.x + l2.y;
       if constexpr (NWGR == 2) {

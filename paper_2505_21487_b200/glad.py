@@ -353,7 +353,7 @@ def kv_bytes_per_token_per_device(variant, n_kv_heads, d_head, d_rope, N, dtype_
     return lib().glad_kv_bytes_per_token_per_device(variant, n_kv_heads, d_head, d_rope, N, dtype_bytes)
 
 
-TRACE_STRIDE = 8 + 12 * 128
+TRACE_STRIDE = 8 + 12 * 128 + 32
 
 
 def debug_set_trace(buf):

@@ -61,8 +61,8 @@ print(f"kernel entry -> CTA start (setup) us: median {np.median(tr[:, 0] - tr[:,
       f"entry spread {(tr[:, 7].max() - tr[:, 7].min()) / 1e3:.1f}")
 print(f"CTA lifetime median {np.median(tr[:, 2] - tr[:, 0]) / 1e3:.1f} us, start->Q ready "
       f"{np.median(tr[:, 1] - tr[:, 0]) / 1e3:.2f} us")
-T = (tr.shape[1] - 8) // 12
-tile = tr[:, 8:].reshape(len(tr), T, 12)  # load, qk, s, p, pv, free, p_wg1, epi, qk_ret, pv_ret, landed, -
+T = (tr.shape[1] - 8 - 32) // 12
+tile = tr[:, 8:8 + 12 * T].reshape(len(tr), T, 12)  # load, qk, s, p, pv, free, p_wg1, epi, qk_ret, pv_ret, landed, -
 valid = tile[:, :, 1] > 0
 ntile = valid.sum(1)
 
@@ -131,12 +131,23 @@ if os.environ.get("TRACE_SWITCH"):
     picks = [int(np.argsort(_end)[-1]), int(np.argsort(np.where(_nseg == _nseg.min(), _end, 1e18))[len(_end) // 4 % max(1, int((_nseg == _nseg.min()).sum()))])]
     for c in picks:
         base = tr[c, 0]
-        print(f"CTA {c} (smid {int(tr[c, -1])}, {int(_nseg[c])} seg, end {_end[c]:.1f} us): tile: free load QK QKret S P0 PV PVret epi (us)")
+        print(f"CTA {c} (smid {int(tr[c, -1])}, {int(_nseg[c])} seg, end {_end[c]:.1f} us): tile: free load QK QKret S P0 PV PVret epi nextQ (us)")
         ends = [i for i in range(ntile[c]) if tile[c, i, 7] > 0]
         show = sorted({j for i in ends for j in range(max(0, i - 2), min(ntile[c], i + 4))} | {0, 1, 2, ntile[c] - 1})
         for i in show:
             print(f"  tile {i:3d}: " + "  ".join(f"{(tile[c, i, j] - base) / 1e3:8.2f}" if tile[c, i, j] else "       -"
-                                               for j in (5, 0, 1, 8, 2, 3, 4, 9, 7)))
+                                               for j in (5, 0, 1, 8, 2, 3, 4, 9, 7, 10)))
+
+if os.environ.get("TRACE_QSEG"):
+    c = int(np.argsort(_end)[-1])
+    base = tr[c, 0]
+    print(f"CTA {c}: per segment (us): first QK probe, q_full seen, qn_full seen")
+    for sg in range(1, 8):
+        sl = tr.shape[1] - 32 + 3 * sg
+        v = tr[c, sl:sl + 3]
+        if v[2]:
+            print(f"  seg {sg}: probe {(v[2] - base) / 1e3:8.2f}  q_full {(v[0] - base) / 1e3 if v[0] else -1:8.2f}  "
+                  f"qn_full {(v[1] - base) / 1e3 if v[1] else -1:8.2f}")
 
 if os.environ.get("TRACE_RAW"):
     c = int(os.environ.get("TRACE_CTA", "5"))
