@@ -335,8 +335,25 @@ def _events_time(stream, fn, K, world, dev):
     return ms, per
 
 
+class _Eager:
+    """Stands in for a CUDA graph when graphs are off (--debug-one-gpu: gloo
+    collectives cannot be captured)."""
+
+    def __init__(self, stream, fn):
+        self.stream, self.fn = stream, fn
+
+    def replay(self):
+        self.fn(self.stream)
+
+
+_NO_GRAPH = False
+
+
 def _capture(dev, stream, fn):
     import torch
+
+    if _NO_GRAPH:
+        return _Eager(stream, fn)
 
     g = torch.cuda.CUDAGraph()
     s2 = torch.cuda.Stream(dev)
@@ -517,7 +534,7 @@ def run_ours(args, rank, world, local_rank):
                                        f"tp shard of {name.split('_tp')[1]}" if is_tp else
                                        f"dp{world} (independent batches)"),
                        "l2": f"inputs larger than L2 ({abytes / 1e9:.2f} GB algorithmic per step > 126 MB); "
-                             "no flush", "cuda_graph": True},
+                             "no flush", "cuda_graph": not _NO_GRAPH},
             "tbps": gbs / 1e3, "tflops": tfs,
             "roofline": roof, "cpu_baseline": cpu,
             "e2e": {"value": total_tokens / (e2e_ms * 1e-3), "unit": "tokens/s", "ms_per_step": e2e_ms,
@@ -591,7 +608,7 @@ def _tp1_base(name, dev, stream, steps):
     decode + o_proj, no all-reduce), CUDA graph, on this rank's GPU."""
     import torch
 
-    from paper_2505_21487_b200 import tp, workloads
+    from paper_2505_21487_b200 import workloads
 
     wl = workloads.get(name)
     st = workloads.build_device_state(wl, device=dev)
@@ -600,9 +617,9 @@ def _tp1_base(name, dev, stream, steps):
         torch.bfloat16)
     y = torch.empty(wl.B * wl.Lq, D_MODEL, dtype=torch.bfloat16, device=dev)
 
-    def step(s):
+    def step(s):  # rank-local: o_proj over all heads, no collective (the other ranks wait at a barrier)
         out, _ = workloads.run(wl, st, stream=s)
-        tp.oproj_allreduce(out.view(wl.B * wl.Lq, wl.H, wl.d_v), w_vo, out=y)
+        torch.matmul(out.view(wl.B * wl.Lq, wl.H * wl.d_v), w_vo, out=y)
 
     for _ in range(3):
         step(stream)
@@ -630,6 +647,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ctas", type=int, default=0, help="persistent CTA count (0 = one per SM)")
     ap.add_argument("--tile", type=int, default=0, help="debug: force the KV tile height (0 = library choice)")
+    ap.add_argument("--debug-one-gpu", action="store_true",
+                    help="validation only: every rank on cuda:0, gloo instead of NCCL, no CUDA graphs (the N>1 control "
+                         "flow on a one-GPU box; numbers are not bench values)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -640,11 +660,18 @@ def main():
         return
     import torch.distributed as dist
 
+    if args.debug_one_gpu:
+        global _NO_GRAPH
+        _NO_GRAPH = True
+        local_rank = 0
     if world > 1:
         import torch
 
         torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if args.debug_one_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     try:
         run_ours(args, rank, world, local_rank)
     finally:
