@@ -191,7 +191,9 @@ GLAD_API void glad_debug_set_trace(void* device_buf);
  * 16 = no rows mode (64-row swap-AB blocks), 32 = cooperative cp.async
  * producer instead of TMA gather4 for pages < 16, 64 = load-only decode
  * (KV tiles streamed and released, no QK / softmax / PV; the output is
- * undefined — measures the memory side alone).  Not thread-safe. */
+ * undefined — measures the memory side alone), 128 = no (head, query
+ * block) CTA groups (multi-block units walked in the ((head, b), block)
+ * order).  Not thread-safe. */
 GLAD_API void glad_debug_set_phase_mask(int32_t mask);
 /* Debug/benchmark only: force the KV tile height (64, 96 or 128 tokens; 0 =
  * library choice).  Results are identical up to fp32 summation order. */

@@ -207,11 +207,24 @@ glad_status decode_common(Variant v, const void* q, const void* pool, const glad
   }
   // Ranges (one per CTA, or per cluster): one equal group per KV head when
   // there are enough, so the heads of a sequence advance in lockstep and
-  // their shared RoPE rows hit L2.
+  // their shared RoPE rows hit L2.  Several query blocks per unit (MLA's two
+  // 64-head blocks, q_len >= 2) without clusters: one group per (head, query
+  // block) instead (qb_outer unit order), so the blocks reading the same KV
+  // tiles run at the same time and the tiles come from HBM once (C2 MLA:
+  // ncu DRAM 2.0x -> ~1x algorithmic); skipped when the groups would get
+  // fewer than 16 CTAs each (prefill's many query blocks) or with phase-mask
+  // bit 128 (A/B).
   int R0 = G0 / cl_n;
   if (cl_n > 1 && num_ctas == 0) R0 = std::min(R0, max_clusters(g.key, cl_n));
-  const int head_groups = (L->n_heads_kv > 1 && R0 >= L->n_heads_kv) ? 1 : 0;
-  const int R = head_groups ? (R0 / L->n_heads_kv) * L->n_heads_kv : R0;
+  int qb_outer = 0, n_groups = 0;
+  const int64_t ngq = static_cast<int64_t>(L->n_heads_kv) * g.n_qblk;
+  if (cl_n == 1 && g.n_qblk > 1 && !(g_phase_mask & 128) && ngq <= 16 && R0 >= 16 * ngq) {
+    qb_outer = 1;
+    n_groups = static_cast<int>(ngq);
+  } else if (L->n_heads_kv > 1 && R0 >= L->n_heads_kv) {
+    n_groups = L->n_heads_kv;
+  }
+  const int R = n_groups > 1 ? (R0 / n_groups) * n_groups : R0;
   const int G = R * cl_n;
   const int64_t n_plan = U / cl_n;  // plan entries: units, or (head, sequence) groups
   const WsLayout wl = ws_layout(U, G, g.key.nq, g.key.d_v);
@@ -300,7 +313,8 @@ glad_status decode_common(Variant v, const void* q, const void* pool, const glad
   // cycles of issue each; the cooperative cp.async producer wins (measured)
   p.cp_kv = (L->page_size < 16 && !g4) ? 1 : 0;
   p.g4 = g4 ? 1 : 0;
-  p.head_groups = head_groups;
+  p.n_groups = n_groups;
+  p.qb_outer = qb_outer;
   p.q_box_h = q_box_h;
   p.q_box_t = q_box_t;
   p.q = static_cast<const __nv_bfloat16*>(q);
@@ -334,7 +348,7 @@ glad_status decode_common(Variant v, const void* q, const void* pool, const glad
   int32_t* plan = reinterpret_cast<int32_t*>(wsb + wl.plan);
   cudaError_t e = cudaSuccess;
   if (g_phase_mask & 1) {
-    e = glad::launch_plan(seqlens, plan, p.n_units, cl_n, B, g.key.t, g.n_qblk, g.key.nq, Lq, g.g_q, p.causal, H,
+    e = glad::launch_plan(seqlens, plan, p.n_units, cl_n, B, g.key.t, g.n_qblk, qb_outer, g.key.nq, Lq, g.g_q, p.causal, H,
                           g.key.d_v, out, lse, nullptr, st);
     if (e != cudaSuccess) return fail(GLAD_ERR_CUDA, "plan launch failed: %s", cudaGetErrorString(e));
   }
@@ -343,8 +357,8 @@ glad_status decode_common(Variant v, const void* q, const void* pool, const glad
     if (e != cudaSuccess) return fail(GLAD_ERR_CUDA, "decode launch failed: %s", cudaGetErrorString(e));
   }
   if (g_phase_mask & 4) {
-    e = glad::launch_merge_split(plan, p.o_part, p.lse_part, G, cl_n, p.n_units, g.key.nq, g.n_qblk, B,
-                                 L->n_heads_kv, head_groups, g.g_q, Lq, H, g.key.d_v, out, lse, st);
+    e = glad::launch_merge_split(plan, p.o_part, p.lse_part, G, cl_n, p.n_units, g.key.nq, g.n_qblk, qb_outer, B,
+                                 n_groups, g.g_q, Lq, H, g.key.d_v, out, lse, st);
     if (e != cudaSuccess) return fail(GLAD_ERR_CUDA, "merge launch failed: %s", cudaGetErrorString(e));
   }
   return GLAD_OK;
@@ -360,7 +374,7 @@ const char* glad_version(void) { return "glad 0.1.0 sm_100a"; }
 
 void glad_debug_set_trace(void* device_buf) { g_trace = static_cast<uint64_t*>(device_buf); }
 
-void glad_debug_set_phase_mask(int32_t mask) { g_phase_mask = mask & 127; }
+void glad_debug_set_phase_mask(int32_t mask) { g_phase_mask = mask & 255; }
 
 void glad_debug_set_tile(int32_t tokens) { g_tile_override = tokens; }
 

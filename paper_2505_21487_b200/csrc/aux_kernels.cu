@@ -90,7 +90,7 @@ __global__ void combine_kernel(const float* __restrict__ o_part, const float* __
 // the output of units with no visible key (zeros, lse = -inf), which no
 // decode CTA visits.
 __global__ void plan_kernel(const int32_t* __restrict__ seqlens, int32_t* __restrict__ plan, int U, int cl_n,
-                            int B, int tile, int n_qblk, int nq_blk, int Lq, int g_q,
+                            int B, int tile, int n_qblk, int qb_outer, int nq_blk, int Lq, int g_q,
                             int causal, int H, int d_v, __nv_bfloat16* __restrict__ out, float* __restrict__ lse,
                             uint64_t* trace) {
   if (trace && threadIdx.x == 0) trace[0] = globaltimer();
@@ -106,8 +106,8 @@ __global__ void plan_kernel(const int32_t* __restrict__ seqlens, int32_t* __rest
       // plan entry u: unit u, or with clusters the (head, sequence) group of
       // cl_n units whose tiles are those of its last query block (most keys)
       const int ul = u * cl_n + cl_n - 1;
-      const int qb = ul % n_qblk;
-      const int b = (ul / n_qblk) % B;  // head-major unit order
+      const UnitIdx ui = unit_idx(ul, B, n_qblk, qb_outer);
+      const int qb = ui.qb, b = ui.b;
       const int n0 = qb * nq_blk;
       const int nq = min(nq_blk, Lq * g_q - n0);
       const int L = seqlens[b];
@@ -115,8 +115,8 @@ __global__ void plan_kernel(const int32_t* __restrict__ seqlens, int32_t* __rest
       if (causal) kv_end = max(0, min(L, L - Lq + (n0 + nq - 1) / g_q + 1));
       tiles = (kv_end + tile - 1) / tile;
       if (tiles == 0) {  // no visible key: no decode CTA visits the unit(s) (rare; one thread per entry)
-        const int head = (ul / n_qblk) / B;
-        const int n_first = (ul - (cl_n - 1)) % n_qblk * nq_blk;
+        const int head = ui.head;
+        const int n_first = (qb - (cl_n - 1)) * nq_blk;  // clusters (qb_outer = 0): the entry's first block
         for (int n = n_first; n < n0 + nq; ++n) {
           const int t = n / g_q, h = head * g_q + (n - t * g_q);
           const int64_t row = (static_cast<int64_t>(b) * Lq + t) * H + h;
@@ -156,9 +156,9 @@ __global__ void plan_kernel(const int32_t* __restrict__ seqlens, int32_t* __rest
 }
 
 cudaError_t launch_plan(const int32_t* seqlens, int32_t* plan, int U, int cl_n, int B, int tile, int n_qblk,
-                        int nq_blk, int Lq, int g_q, int causal, int H, int d_v, void* out, float* lse,
+                        int qb_outer, int nq_blk, int Lq, int g_q, int causal, int H, int d_v, void* out, float* lse,
                         uint64_t* trace, cudaStream_t stream) {
-  plan_kernel<<<1, 1024, 0, stream>>>(seqlens, plan, U, cl_n, B, tile, n_qblk, nq_blk, Lq, g_q, causal, H, d_v,
+  plan_kernel<<<1, 1024, 0, stream>>>(seqlens, plan, U, cl_n, B, tile, n_qblk, qb_outer, nq_blk, Lq, g_q, causal, H, d_v,
                                       static_cast<__nv_bfloat16*>(out), lse, trace);
   return cudaGetLastError();
 }
@@ -178,7 +178,7 @@ constexpr int kMergeThreads = 256;
 constexpr int kMergeMaxParts = 8;  // weights staged per pass
 __global__ void __launch_bounds__(kMergeThreads) merge_split_kernel(
     const int32_t* __restrict__ plan, const float* __restrict__ o_part, const float* __restrict__ lse_part, int G,
-    int cl_n, int U, int nq_blk, int n_qblk, int B, int n_heads, int head_groups, int g_q, int Lq, int H, int d_v,
+    int cl_n, int U, int nq_blk, int n_qblk, int qb_outer, int B, int n_groups, int g_q, int Lq, int H, int d_v,
     __nv_bfloat16* __restrict__ out, float* __restrict__ lse) {
   __shared__ int u_s;
   __shared__ float w_s[kMergeMaxParts][128];  // nq_blk <= 128 (rows mode)
@@ -186,8 +186,7 @@ __global__ void __launch_bounds__(kMergeThreads) merge_split_kernel(
   const int GR = G / cl_n;                     // ranges
   const int b_cta = blockIdx.x / cl_n + 1;     // boundary between ranges b-1 and b
   const int rank = blockIdx.x % cl_n;
-  const int total = __ldg(plan + U);
-  const CtaRange rg = cta_range(b_cta, GR, total, n_heads, head_groups);
+  const CtaRange rg = cta_range(b_cta, GR, plan, U, n_groups);
   if (rg.t0 >= rg.t1) return;
   const int t = rg.t0;
   // unit containing tile t: 32-ary search by warp 0 (last u with plan[u] <= t)
@@ -208,18 +207,19 @@ __global__ void __launch_bounds__(kMergeThreads) merge_split_kernel(
   const int pe = u_s;  // plan entry
   const int pu0 = __ldg(plan + pe), pu1 = __ldg(plan + pe + 1);
   if (pu0 == t) return;  // the entry starts at this boundary: not cut here
-  const int cf = cta_of_tile(pu0, GR, total, n_heads, head_groups);
+  const int cf = cta_of_tile(pu0, GR, plan, U, n_groups);
   if (cf != b_cta - 1) return;  // an earlier boundary cuts it: that block merges
-  const int cl = cta_of_tile(pu1 - 1, GR, total, n_heads, head_groups);
+  const int cl = cta_of_tile(pu1 - 1, GR, plan, U, n_groups);
   const int u = pe * cl_n + rank;
-  const int qb = u % n_qblk, hb = u / n_qblk, b = hb % B, head = hb / B;
+  const UnitIdx ui = unit_idx(u, B, n_qblk, qb_outer);
+  const int qb = ui.qb, b = ui.b, head = ui.head;
   const int n0 = qb * nq_blk;
   const int nq = min(nq_blk, Lq * g_q - n0);
   if (nq <= 0) return;
   // partial slot of range c (decode epilogue): 2c if the entry is c's first
   // segment, 2c + 1 if it is its last one (only range cf can have earlier
   // segments, when its range starts before the entry)
-  const int cf_last = cta_range(cf, GR, total, n_heads, head_groups).t0 < pu0 ? 1 : 0;
+  const int cf_last = cta_range(cf, GR, plan, U, n_groups).t0 < pu0 ? 1 : 0;
   auto slot_of = [&](int c) -> int64_t { return static_cast<int64_t>(2 * c + (c == cf ? cf_last : 0)) * cl_n + rank; };
   for (int n = threadIdx.x; n < nq; n += kMergeThreads) {
     float mx = -INFINITY;
@@ -282,11 +282,11 @@ __global__ void __launch_bounds__(kMergeThreads) merge_split_kernel(
 }
 
 cudaError_t launch_merge_split(const int32_t* plan, const float* o_part, const float* lse_part, int G, int cl_n,
-                               int U, int nq_blk, int n_qblk, int B, int n_heads, int head_groups, int g_q, int Lq,
+                               int U, int nq_blk, int n_qblk, int qb_outer, int B, int n_groups, int g_q, int Lq,
                                int H, int d_v, void* out, float* lse, cudaStream_t stream) {
   if (G / cl_n < 2) return cudaSuccess;
   merge_split_kernel<<<dim3((G / cl_n - 1) * cl_n, GLAD_MERGE_SPLIT), kMergeThreads, 0, stream>>>(
-      plan, o_part, lse_part, G, cl_n, U, nq_blk, n_qblk, B, n_heads, head_groups, g_q, Lq, H, d_v,
+      plan, o_part, lse_part, G, cl_n, U, nq_blk, n_qblk, qb_outer, B, n_groups, g_q, Lq, H, d_v,
       static_cast<__nv_bfloat16*>(out), lse);
   return cudaGetLastError();
 }

@@ -62,7 +62,8 @@ struct DecodeParams {
   int32_t page_size, log2_page, box_rows;
   int32_t n_qblk, n_units;  // query blocks per head, U = n_heads_kv * B * n_qblk (head-major)
   int32_t causal;
-  int32_t head_groups;      // 1: CTAs form n_heads_kv equal groups, one per head (see cta_range)
+  int32_t n_groups;         // > 1: CTAs form n_groups equal groups, one per unit group (see cta_range)
+  int32_t qb_outer;         // unit order: 1 = ((head, query block), b), 0 = ((head, b), query block)
   const __nv_bfloat16* pool;  // paged cache (cp.async producer path)
   int64_t row_stride;       // elements
   int32_t cp_kv;            // 1: small pages -> cooperative cp.async producer instead of TMA
@@ -352,9 +353,35 @@ __device__ __forceinline__ void tmem_store_cols(uint32_t taddr, const float (&x)
   }
 }
 
-// One unit u = ((head * B) + b) * n_qblk + qb (head-major, so the RoPE rows a
-// sequence's heads share are read by concurrently running CTAs and hit L2)
-// and the part of its
+// Unit index -> (head, sequence, query block).  Two orders, both head-major
+// (so the RoPE rows a sequence's heads share are read by concurrently running
+// CTA groups and hit L2):
+//  qb_outer = 0: u = ((head * B) + b) * n_qblk + qb — a sequence's query
+//    blocks are consecutive units (clusters: one plan entry per (head, b));
+//  qb_outer = 1: u = ((head * n_qblk) + qb) * B + b — every (head, query
+//    block) is one CTA group (cta_range), so the n_qblk blocks that read the
+//    same KV tiles (MLA's two 64-head blocks, q_len >= 2) stream the same
+//    sequence at the same time and the second read of each tile hits L2.
+struct UnitIdx {
+  int head, b, qb;
+};
+__device__ __forceinline__ UnitIdx unit_idx(int u, int B, int n_qblk, int qb_outer) {
+  UnitIdx r;
+  if (qb_outer) {
+    r.b = u % B;
+    const int g = u / B;
+    r.qb = g % n_qblk;
+    r.head = g / n_qblk;
+  } else {
+    r.qb = u % n_qblk;
+    const int hb = u / n_qblk;
+    r.b = hb % B;
+    r.head = hb / B;
+  }
+  return r;
+}
+
+// One unit u and the part of its
 // tile range [t0, t1) that falls in this CTA's flattened range.
 struct Seg {
   int u, b, head, qb;
@@ -378,10 +405,10 @@ __device__ __forceinline__ void seg_unit(const DecodeParams& p, int pi, int L, S
   s.pi = pi;
   const int rank = static_cast<int>(blockIdx.x) % p.cl_n;
   s.u = pi * p.cl_n + rank;
-  s.qb = s.u % p.n_qblk;
-  const int hb = s.u / p.n_qblk;  // head-major: CTAs in different head ranges stream the same b together
-  s.b = hb % p.B;
-  s.head = hb / p.B;
+  const UnitIdx ui = unit_idx(s.u, p.B, p.n_qblk, p.qb_outer);
+  s.qb = ui.qb;
+  s.b = ui.b;
+  s.head = ui.head;
   const int nq_total = p.Lq * p.g_q;
   s.n0 = s.qb * NQ;
   s.nq = min(NQ, nq_total - s.n0);
@@ -399,7 +426,7 @@ __device__ __forceinline__ void seg_unit(const DecodeParams& p, int pi, int L, S
 template <int NQ>
 __device__ __noinline__ void make_seg(const DecodeParams& p, int u, int cta_t0, int cta_t1, Seg* out) {
   Seg s;
-  seg_unit<NQ>(p, u, __ldg(p.seqlens + ((u * p.cl_n) / p.n_qblk) % p.B), s);
+  seg_unit<NQ>(p, u, __ldg(p.seqlens + unit_idx(u * p.cl_n, p.B, p.n_qblk, p.qb_outer).b), s);
   const int pu0 = __ldg(p.plan + u), pu1 = __ldg(p.plan + u + 1);
   s.t0 = max(cta_t0, pu0) - pu0;
   s.t1 = min(cta_t1, pu1) - pu0;
@@ -407,22 +434,26 @@ __device__ __noinline__ void make_seg(const DecodeParams& p, int u, int cta_t0, 
   *out = s;
 }
 
-// Flattened tile range of CTA c (units are head-major).  With head groups,
-// the G CTAs form n_heads_kv equal groups and group h splits head h's tiles
-// evenly, so CTA (h, k) works on the same sequences as (h', k) at the same
-// time and the RoPE rows the heads share are served from L2.
+// Flattened tile range of CTA c.  With n_groups > 1 the G CTAs form
+// n_groups equal groups over equal unit counts (KV heads, or (head, query
+// block) pairs with qb_outer) and group g splits its own tiles [plan[g U/n],
+// plan[(g+1) U/n]) evenly, so CTA (g, k) works on the same sequences as
+// (g', k) at the same time: the RoPE rows the heads share, and with
+// qb_outer the KV tiles the query blocks share, are served from L2.
 struct CtaRange {
   int t0, t1;
 };
-__device__ __host__ __forceinline__ CtaRange cta_range(int c, int G, int total, int n_heads, int head_groups) {
+__device__ __forceinline__ CtaRange cta_range(int c, int G, const int32_t* plan, int U, int n_groups) {
   CtaRange r;
-  if (head_groups) {
-    const int Gh = G / n_heads, total_h = total / n_heads;
-    const int per = (total_h + Gh - 1) / Gh;
-    const int h = c / Gh, k = c - h * Gh;
-    r.t0 = h * total_h + min(total_h, k * per);
-    r.t1 = h * total_h + min(total_h, (k + 1) * per);
+  if (n_groups > 1) {
+    const int Gh = G / n_groups, upg = U / n_groups;
+    const int g = c / Gh, k = c - g * Gh;
+    const int gs = __ldg(plan + g * upg), n = __ldg(plan + (g + 1) * upg) - gs;
+    const int per = (n + Gh - 1) / Gh;
+    r.t0 = gs + min(n, k * per);
+    r.t1 = gs + min(n, (k + 1) * per);
   } else {
+    const int total = __ldg(plan + U);
     const int per = (total + G - 1) / G;
     r.t0 = min(total, c * per);
     r.t1 = min(total, r.t0 + per);
@@ -430,13 +461,16 @@ __device__ __host__ __forceinline__ CtaRange cta_range(int c, int G, int total, 
   return r;
 }
 // CTA whose range contains tile t (inverse of cta_range).
-__device__ __host__ __forceinline__ int cta_of_tile(int t, int G, int total, int n_heads, int head_groups) {
-  if (head_groups) {
-    const int Gh = G / n_heads, total_h = total / n_heads;
-    const int per = (total_h + Gh - 1) / Gh;
-    const int h = t / total_h;
-    return h * Gh + (t - h * total_h) / per;
+__device__ __forceinline__ int cta_of_tile(int t, int G, const int32_t* plan, int U, int n_groups) {
+  if (n_groups > 1) {
+    const int Gh = G / n_groups, upg = U / n_groups;
+    int g = 0;
+    while (g + 1 < n_groups && __ldg(plan + (g + 1) * upg) <= t) ++g;
+    const int gs = __ldg(plan + g * upg), n = __ldg(plan + (g + 1) * upg) - gs;
+    const int per = (n + Gh - 1) / Gh;
+    return g * Gh + (t - gs) / per;
   }
+  const int total = __ldg(plan + U);
   const int per = (total + G - 1) / G;
   return t / per;
 }
@@ -513,8 +547,7 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
     // Work range of this CTA and its segment table, with warp-parallel loads
     // (a serial search over the plan would cost one L2 round trip per step).
     const int U = p.n_units;
-    const int total = __ldg(p.plan + U);
-    const CtaRange rg = cta_range(cta / p.cl_n, gridDim.x / p.cl_n, total, p.n_heads_kv, p.head_groups);
+    const CtaRange rg = cta_range(cta / p.cl_n, gridDim.x / p.cl_n, p.plan, U, p.n_groups);
     const int t0 = rg.t0, t1 = rg.t1;
     int lo = 0, hi = U - 1;  // last unit with plan[u] <= t0 (plan[0] = 0)
     while (lo < hi) {
@@ -536,7 +569,7 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
         const int st0 = max(t0, pu0) - pu0, st1 = min(t1, pu1) - pu0;
         const bool has = in && st1 > st0;
         int L = 0;
-        if (has) L = __ldg(p.seqlens + ((u * p.cl_n) / p.n_qblk) % p.B);
+        if (has) L = __ldg(p.seqlens + unit_idx(u * p.cl_n, p.B, p.n_qblk, p.qb_outer).b);
         const unsigned hm = __ballot_sync(0xffffffffu, has);
         const int pos = nseg + __popc(hm & ((1u << lane) - 1));
         const int whole = (st0 == 0 && st1 == pu1 - pu0) ? 1 : 0;
