@@ -193,7 +193,9 @@ GLAD_API void glad_debug_set_trace(void* device_buf);
  * (KV tiles streamed and released, no QK / softmax / PV; the output is
  * undefined — measures the memory side alone), 128 = no (head, query
  * block) CTA groups (multi-block units walked in the ((head, b), block)
- * order).  Not thread-safe. */
+ * order), 256 = pages < 16 through TMA gather4 alone (default: gather4
+ * for most rows of a tile + 16-B cp.async by a second producer warp for the
+ * rest).  Not thread-safe. */
 GLAD_API void glad_debug_set_phase_mask(int32_t mask);
 /* Debug/benchmark only: force the KV tile height (64, 96 or 128 tokens; 0 =
  * library choice).  Results are identical up to fp32 summation order. */

@@ -312,7 +312,7 @@ glad_status decode_common(Variant v, const void* q, const void* pool, const glad
   // pages shorter than 16 tokens: one TMA per page run per chunk costs ~100
   // cycles of issue each; the cooperative cp.async producer wins (measured)
   p.cp_kv = (L->page_size < 16 && !g4) ? 1 : 0;
-  p.g4 = g4 ? 1 : 0;
+  p.g4 = g4 ? ((g_phase_mask & 256) ? 1 : 2) : 0;  // bit 256: gather4 alone (no LSU rows)
   p.n_groups = n_groups;
   p.qb_outer = qb_outer;
   p.q_box_h = q_box_h;
@@ -374,7 +374,7 @@ const char* glad_version(void) { return "glad 0.1.0 sm_100a"; }
 
 void glad_debug_set_trace(void* device_buf) { g_trace = static_cast<uint64_t*>(device_buf); }
 
-void glad_debug_set_phase_mask(int32_t mask) { g_phase_mask = mask & 255; }
+void glad_debug_set_phase_mask(int32_t mask) { g_phase_mask = mask & 511; }
 
 void glad_debug_set_tile(int32_t tokens) { g_tile_override = tokens; }
 

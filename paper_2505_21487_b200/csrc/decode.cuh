@@ -67,7 +67,8 @@ struct DecodeParams {
   const __nv_bfloat16* pool;  // paged cache (cp.async producer path)
   int64_t row_stride;       // elements
   int32_t cp_kv;            // 1: small pages -> cooperative cp.async producer instead of TMA
-  int32_t g4;               // 1: small pages -> TMA gather4 of 4 token rows per instruction (lmap = row map, box (64, 1))
+  int32_t g4;               // small pages -> TMA gather4 of 4 token rows per instruction (lmap = row map, box (64, 1));
+                            // 2: + the LSU warp loading part of every tile (hybrid producer), 1: gather4 only
   int32_t q_tma;            // 1: Q via the 3-D tensor map (box (64, q_box_h, q_box_t)); 0: cp.async
   int32_t q_box_h, q_box_t;
   float scale_log2;         // softmax_scale * log2(e)
@@ -135,6 +136,14 @@ struct DecodeParams {
 #endif
 #ifndef GLAD_MMA_BACKOFF_NS
 #define GLAD_MMA_BACKOFF_NS 0
+#endif
+#ifndef GLAD_G4_LSU_PCT
+#define GLAD_G4_LSU_PCT 44  // pages < 16: % of each tile's rows loaded by the LSU warp next to gather4 (0: gather4 only);
+                            // A/B (C2 page 1 / C3 q_len 2 page 1 decode ms): 0: 0.723 / 0.449, 31: 0.565 / 0.374,
+                            // 37: 0.528 / 0.354, 44: 0.510 / 0.316, 50: 0.558 / 0.317
+#endif
+#ifndef GLAD_MMA_IDLE_WAIT
+#define GLAD_MMA_IDLE_WAIT 0  // swap-AB MMA scheduler: ns suspend hint on the next expected barrier when idle (0: spin)
 #endif
 constexpr int kTraceTiles = 128;
 constexpr int kTraceStride = 8 + 12 * kTraceTiles + 32;  // + 32 per-CTA debug slots at the end
@@ -540,6 +549,9 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int cta = blockIdx.x;
+  // small pages with TMA-loaded Q: gather4 + LSU hybrid producer (warps 0 + 3)
+  constexpr int G4_LSU_ROWS = (C::T * GLAD_G4_LSU_PCT / 100) & ~3;
+  const bool g4_lsu = G4_LSU_ROWS > 0 && p.g4 == 2 && p.q_tma;
   if (GLAD_TRACE && p.trace && threadIdx.x == 0) p.trace[static_cast<size_t>(cta) * kTraceStride + 7] = globaltimer();
 
   // ------------------------------------------------------------- setup
@@ -604,9 +616,10 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
   }
   if (threadIdx.x == 0) {
     for (int i = 0; i < NS; ++i) {
-      mbar_init(&kv_full[i], p.cp_kv ? (p.q_tma ? 64 : 32) : 1);
+      const int nfull = p.cp_kv ? (p.q_tma ? 64 : 32) : (g4_lsu ? 33 : 1);  // cp.async lanes (+ the expect_tx arrival)
+      mbar_init(&kv_full[i], nfull);
       mbar_init(&kv_empty[i], 1);
-      mbar_init(&kv_full_hi[i], p.cp_kv ? (p.q_tma ? 64 : 32) : 1);
+      mbar_init(&kv_full_hi[i], nfull);
       mbar_init(&kv_empty_hi[i], 1);
       mbar_init(&p_full[i], C::ROWS ? 4 * GLAD_ROWS_WG : 8);  // softmax warps
     }
@@ -873,28 +886,62 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
           // (rows past the visible end repeat the last visible row: they
           // are zeroed / masked by the softmax like any unloaded row)
           const int ngrp = (ntok + 3) >> 2;
-          if (lane == 0 && warp == 0) {
-            mbar_arrive_expect_tx(&kv_full[stage], static_cast<uint32_t>(ngrp * (C::SPLIT ? C::NLO : C::NCH) * 512));
-            if (C::SPLIT) mbar_arrive_expect_tx(&kv_full_hi[stage], static_cast<uint32_t>(ngrp * (C::NCH - C::NLO) * 512));
-          }
-          __syncwarp();
-          uint64_t* bar_hi = C::SPLIT ? &kv_full_hi[stage] : &kv_full[stage];
-          const int npw = (p.q_tma ? 2 : 1), pw = warp == 0 ? 0 : 1;
-          for (int g = lane + 32 * pw; g < ngrp; g += 32 * npw) {
-            int rr[4];
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              const int pos = p0 + min(4 * g + j, ntok - 1);
-              rr[j] = __ldg(bt_row + (pos >> p.log2_page)) * p.page_size + (pos & (p.page_size - 1));
+          // hybrid producer (g4_lsu): gather4 (warp 0) takes the first row
+          // groups, the LSU path (warp 3: 16-B cp.async per lane)
+          // the last G4_LSU_ROWS rows — the two run on different units
+          // (TMA engine op rate / LSU), so their rates add
+          const int ng4 = g4_lsu ? min(ngrp, (T - G4_LSU_ROWS) / 4) : ngrp;
+          if (warp == 0 || !g4_lsu) {
+            if (lane == 0 && warp == 0) {
+              mbar_arrive_expect_tx(&kv_full[stage], static_cast<uint32_t>(ng4 * (C::SPLIT ? C::NLO : C::NCH) * 512));
+              if (C::SPLIT) mbar_arrive_expect_tx(&kv_full_hi[stage], static_cast<uint32_t>(ng4 * (C::NCH - C::NLO) * 512));
             }
-            const int r = 4 * g;
-            const uint32_t ldst = stage_addr + (r >> 3) * C::LGRP + (r & 7) * 128;
-            const int c_head = s.head * p.d_head;
+            __syncwarp();
+            uint64_t* bar_hi = C::SPLIT ? &kv_full_hi[stage] : &kv_full[stage];
+            const int npw = (p.q_tma && !g4_lsu ? 2 : 1), pw = warp == 0 ? 0 : 1;
+            for (int g = lane + 32 * pw; g < ng4; g += 32 * npw) {
+              int rr[4];
 #pragma unroll
-            for (int ch = 0; ch < C::NCH_V; ++ch)
-              tma_gather4(ldst + C::chunk_off(ch), &lmap, ch < C::NLO ? &kv_full[stage] : bar_hi, c_head + ch * 64,
-                          rr[0], rr[1], rr[2], rr[3]);
-            tma_gather4(stage_addr + C::OFF_R + r * 128, &lmap, bar_hi, p.rope_col, rr[0], rr[1], rr[2], rr[3]);
+              for (int j = 0; j < 4; ++j) {
+                const int pos = p0 + min(4 * g + j, ntok - 1);
+                rr[j] = __ldg(bt_row + (pos >> p.log2_page)) * p.page_size + (pos & (p.page_size - 1));
+              }
+              const int r = 4 * g;
+              const uint32_t ldst = stage_addr + (r >> 3) * C::LGRP + (r & 7) * 128;
+              const int c_head = s.head * p.d_head;
+#pragma unroll
+              for (int ch = 0; ch < C::NCH_V; ++ch)
+                tma_gather4(ldst + C::chunk_off(ch), &lmap, ch < C::NLO ? &kv_full[stage] : bar_hi, c_head + ch * 64,
+                            rr[0], rr[1], rr[2], rr[3]);
+              tma_gather4(stage_addr + C::OFF_R + r * 128, &lmap, bar_hi, p.rope_col, rr[0], rr[1], rr[2], rr[3]);
+            }
+          } else {
+            // LSU rows [4 ng4, ntok): each lane resolves one row's pool row,
+            // then per row the warp copies the latent slice (lane = 16-B unit)
+            // and the RoPE part into the same 128B-swizzled layout
+            const __nv_bfloat16* base_h = p.pool + s.head * p.d_head + lane * 8;
+            const __nv_bfloat16* base_r = p.pool + p.rope_col + (lane & 7) * 8;
+            for (int rb = 4 * ng4; rb < ntok; rb += 32) {
+              const int myr = rb + lane;
+              const int pos = p0 + min(myr, ntok - 1);
+              const int myrow = __ldg(bt_row + (pos >> p.log2_page)) * p.page_size + (pos & (p.page_size - 1));
+              const int nr = min(32, ntok - rb);
+#pragma unroll 4
+              for (int j = 0; j < nr; ++j) {
+                const int r = rb + j;
+                const int64_t roff = static_cast<int64_t>(__shfl_sync(0xffffffffu, myrow, j)) * p.row_stride;
+                const uint32_t ldst = stage_addr + (r >> 3) * C::LGRP + (r & 7) * 128;
+#pragma unroll
+                for (int u0 = 0; u0 < C::NCH_V * 8; u0 += 32) {
+                  const int un = u0 + lane;
+                  if (un < C::NCH_V * 8)
+                    cp_async16(ldst + C::chunk_off(un >> 3) + (((un & 7) ^ (r & 7)) << 4), base_h + roff + u0 * 8, 16);
+                }
+                if (lane < C::D_R / 8) cp_async16(stage_addr + C::OFF_R + r * 128 + ((lane ^ (r & 7)) << 4), base_r + roff, 16);
+              }
+            }
+            cp_async_mbar_arrive(&kv_full[stage]);
+            if (C::SPLIT) cp_async_mbar_arrive(&kv_full_hi[stage]);
           }
         } else {
           // latent lo (or the whole latent) + (not split) RoPE, one page run per lane
@@ -1041,7 +1088,7 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
             if (trace && lane == 0 && next_qk == 0) trace[1] = globaltimer();
             if (trace && lane == 0 && next_qk < kTraceTiles) trace[9 + 12 * next_qk] = globaltimer();
             tc_fence_after();
-            if (p.cp_kv) fence_proxy_async_smem();
+            if (p.cp_kv || g4_lsu) fence_proxy_async_smem();
           }
         }
         if (qk_go) {
@@ -1132,7 +1179,7 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
         const int stage = next_qk % NS;
         const int sb = next_qk & 1;
         tc_fence_after();
-        if (p.cp_kv) fence_proxy_async_smem();  // cp.async (generic proxy) writes -> UMMA (async proxy) reads
+        if (p.cp_kv || g4_lsu) fence_proxy_async_smem();  // cp.async (generic proxy) writes -> UMMA (async proxy) reads
         const uint32_t d = tm + sb * NQ;
         const uint64_t ad = desc_kmajor_sw128(sbase + stage * C::STAGE, C::LGRP);
         const uint64_t rd = desc_kmajor_sw128(sbase + stage * C::STAGE + C::OFF_R);
@@ -1239,6 +1286,16 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
           t0 = clock64();
         } else {
           if (GLAD_MMA_BACKOFF_NS > 0) __nanosleep(GLAD_MMA_BACKOFF_NS);
+          if (GLAD_MMA_IDLE_WAIT > 0) {
+            // sleep on the barrier that gates the stage-refill chain first
+            if (next_pv < next_qk)
+              mbar_try_wait_hint(smem_u32(&p_full[next_pv % NS]), (next_pv / NS) & 1, GLAD_MMA_IDLE_WAIT);
+            else if (C::SPLIT && qk_part == 1)
+              mbar_try_wait_hint(smem_u32(&kv_full_hi[next_qk % NS]), (next_qk / NS) & 1, GLAD_MMA_IDLE_WAIT);
+            else if (qk_left)
+              mbar_try_wait_hint(smem_u32(&kv_full[next_qk % NS]), (next_qk / NS) & 1, GLAD_MMA_IDLE_WAIT);
+            __syncwarp();
+          }
           if (warp_uniform(clock64() - t0 > (1ll << 34))) {
             if (lane == 0) printf("glad: MMA scheduler watchdog (cta %d qk %d pv %d)\n", cta, next_qk, next_pv);
             __trap();

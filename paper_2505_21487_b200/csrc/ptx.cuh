@@ -42,6 +42,18 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t addr, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
+// try_wait with an explicit suspend-time hint (ns): the warp sleeps until the
+// phase completes or the hint expires (idle scheduler warps stop stealing
+// issue slots from the softmax warps on their SM sub-partition).
+__device__ __forceinline__ bool mbar_try_wait_hint(uint32_t addr, uint32_t parity, uint32_t ns) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(addr), "r"(parity), "r"(ns)
+      : "memory");
+  return ok != 0;
+}
 // Non-suspending probe (for schedulers that poll several barriers).
 __device__ __forceinline__ bool mbar_test_wait(uint32_t addr, uint32_t parity) {
   uint32_t ok;

@@ -196,6 +196,43 @@ def test_cp_async_producer_path(cfg, tile):
     check(out, lse, o_ref, lse_ref, what=f"cp.async {cfg}")
 
 
+@pytest.mark.parametrize("mask", [7, 7 | 256], ids=["hybrid", "gather4_only"])
+@pytest.mark.parametrize("cfg", [(2, 1, 128, 2, 256, 64, [1024, 777], 1, 3),
+                                 (3, 2, 16, 2, 128, 32, [300, 129, 5], 2, 2),
+                                 (2, 2, 128, 2, 256, 64, [513, 700], 4, 0),
+                                 (2, 1, 64, 1, 512, 64, [640, 100], 8, 2),
+                                 (2, 4, 64, 2, 256, 64, [1111, 37], 1, 0)])
+def test_small_page_producers(cfg, mask, tile):
+    """Pages < 16 tokens: the default hybrid producer (TMA gather4 for the
+    first row groups of each tile, 16-B cp.async by a second warp for the
+    last rows) and phase-mask bit 256 (gather4 alone), against the oracle."""
+    B, Lq, H, h_c, d_c, d_R, lens, page, ctas = cfg
+    glad.debug_set_phase_mask(mask)
+    try:
+        out, lse, o_ref, lse_ref = run_latent(B, Lq, H, h_c, d_c, d_R, np.array(lens), page, ctas=ctas, seed=31)
+    finally:
+        glad.debug_set_phase_mask(7)
+    check(out, lse, o_ref, lse_ref, what=f"mask={mask} {cfg}")
+
+
+@pytest.mark.parametrize("mask", [7, 7 | 128], ids=["qb_groups", "qb_inner"])
+@pytest.mark.parametrize("cfg", [(4, 1, 128, 1, 512, 64, [900, 333, 1, 2048], 64, 64),   # MLA: 2 query blocks
+                                 (3, 2, 128, 1, 512, 64, [700, 1500, 64], 16, 0),        # MLA q_len 2: 4 blocks
+                                 (4, 4, 128, 2, 256, 64, [1300, 5, 640, 999], 64, 128),  # GLA-2 q_len 4: 2 blocks
+                                 (2, 1, 128, 1, 512, 64, [4096, 4095], 64, 37)])         # groups with 18 CTAs
+def test_query_block_groups(cfg, mask):
+    """Several query blocks per unit: the (head, query block) CTA groups
+    (qb_outer unit order, per-group tile ranges from the plan) and phase-mask
+    bit 128 (the ((head, b), block) order), against the oracle."""
+    B, Lq, H, h_c, d_c, d_R, lens, page, ctas = cfg
+    glad.debug_set_phase_mask(mask)
+    try:
+        out, lse, o_ref, lse_ref = run_latent(B, Lq, H, h_c, d_c, d_R, np.array(lens), page, ctas=ctas, seed=37)
+    finally:
+        glad.debug_set_phase_mask(7)
+    check(out, lse, o_ref, lse_ref, what=f"mask={mask} {cfg}")
+
+
 @pytest.mark.parametrize("Lq,H", [(1, 16), (2, 16), (1, 128)])
 def test_mla_baseline(Lq, H, tile):
     out, lse, o_ref, lse_ref = run_latent(2, Lq, H, 1, 512, 64, np.array([700, 300]), 64, seed=Lq + H)

@@ -55,6 +55,14 @@ def child(a):
 
     glad.debug_set_phase_mask(a.base_mask)
     gs = graph(a.base_mask)
+    if a.soak > 0:  # power-capped clock state, as bench.py times it
+        import time
+        t_end = time.time() + a.soak
+        with torch.cuda.stream(s):
+            while time.time() < t_end:
+                for _ in range(100):
+                    gs.replay()
+                torch.cuda.synchronize()
     glad.debug_set_phase_mask(1 | (a.base_mask & ~7))
     workloads.run(wl, st, stream=s)
     gd = graph(2 | (a.base_mask & ~7))
@@ -70,6 +78,7 @@ def main():
     ap.add_argument("--tile", type=int, default=0)
     ap.add_argument("--ctas", type=int, default=0)
     ap.add_argument("--base-mask", type=int, default=7)
+    ap.add_argument("--soak", type=float, default=0.0, help="seconds of step replays before timing")
     ap.add_argument("--child", action="store_true")
     a = ap.parse_args()
     if a.child:
@@ -80,7 +89,7 @@ def main():
         for lib in a.libs:
             env = dict(os.environ, GLAD_LIB=os.path.abspath(lib))
             r = subprocess.run([sys.executable, __file__, "--child", "--workload", a.workload, "--tile", str(a.tile),
-                                "--ctas", str(a.ctas), "--base-mask", str(a.base_mask)],
+                                "--ctas", str(a.ctas), "--base-mask", str(a.base_mask), "--soak", str(a.soak)],
                                env=env, capture_output=True, text=True, timeout=600)
             line = [x for x in r.stdout.splitlines() if x.startswith("RESULT ")]
             if not line:

@@ -34,6 +34,7 @@ ap.add_argument("--ctas", type=int, default=0)
 ap.add_argument("--tile", type=int, default=0)
 ap.add_argument("--ns", type=int, default=2, help="KV stages of the instantiation (for PV->load)")
 ap.add_argument("--mask", type=int, default=7, help="glad_debug_set_phase_mask value")
+ap.add_argument("--soak", type=float, default=0.0, help="seconds of back-to-back steps before the traced one (power-capped clock)")
 a = ap.parse_args()
 wl = workloads.get(a.workload)
 glad.debug_set_phase_mask(a.mask)
@@ -43,6 +44,13 @@ st = workloads.build_device_state(wl, num_ctas=a.ctas)
 for _ in range(3):
     workloads.run(wl, st)
 torch.cuda.synchronize()
+if a.soak > 0:
+    import time
+    t_end = time.time() + a.soak
+    while time.time() < t_end:
+        for _ in range(200):
+            workloads.run(wl, st)
+        torch.cuda.synchronize()
 n_ctas = 70000
 buf = torch.zeros(n_ctas * glad.TRACE_STRIDE, dtype=torch.int64, device="cuda")
 glad.debug_set_trace(buf)
