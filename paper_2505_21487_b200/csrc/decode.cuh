@@ -138,9 +138,18 @@ struct DecodeParams {
 #define GLAD_MMA_BACKOFF_NS 0
 #endif
 #ifndef GLAD_G4_LSU_PCT
-#define GLAD_G4_LSU_PCT 44  // pages < 16: % of each tile's rows loaded by the LSU warp next to gather4 (0: gather4 only);
-                            // A/B (C2 page 1 / C3 q_len 2 page 1 decode ms): 0: 0.723 / 0.449, 31: 0.565 / 0.374,
-                            // 37: 0.528 / 0.354, 44: 0.510 / 0.316, 50: 0.558 / 0.317
+#define GLAD_G4_LSU_PCT 62  // pages < 16: % of each tile's rows loaded by the LSU warps next to gather4 (0: gather4 only);
+                            // A/B (C2 page 1 / C3 q_len 2 page 1 decode ms), one LSU warp: 0: 0.723 / 0.449,
+                            // 31: 0.565 / 0.374, 37: 0.528 / 0.354, 44: 0.510 / 0.316, 50: 0.558 / 0.317;
+                            // two LSU warps: 50: 0.444 / 0.291, 56: 0.424 / 0.291, 62: 0.391 / 0.274, 69: 0.448 / 0.294;
+                            // warp 0 as a third (after its gather4 issues): 0.510-0.540 / 0.320-0.345 (slower)
+#endif
+#ifndef GLAD_G4_LSU_WARPS
+#define GLAD_G4_LSU_WARPS 2  // LSU warps of the hybrid producer (2: the Q loader warp copies rows too; the LSU
+                             // path is per-warp issue-bound, so its rate scales with the warps)
+#endif
+#ifndef GLAD_G4_LSU_W0
+#define GLAD_G4_LSU_W0 0  // hybrid producer: warp 0 copies LSU rows too after its gather4 issues
 #endif
 #ifndef GLAD_MMA_IDLE_WAIT
 #define GLAD_MMA_IDLE_WAIT 0  // swap-AB MMA scheduler: ns suspend hint on the next expected barrier when idle (0: spin)
@@ -552,6 +561,7 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
   // small pages with TMA-loaded Q: gather4 + LSU hybrid producer (warps 0 + 3)
   constexpr int G4_LSU_ROWS = (C::T * GLAD_G4_LSU_PCT / 100) & ~3;
   const bool g4_lsu = G4_LSU_ROWS > 0 && p.g4 == 2 && p.q_tma;
+  const bool g4_lsu2 = g4_lsu && GLAD_G4_LSU_WARPS == 2;  // warp 2 (Q loader) copies LSU rows too
   if (GLAD_TRACE && p.trace && threadIdx.x == 0) p.trace[static_cast<size_t>(cta) * kTraceStride + 7] = globaltimer();
 
   // ------------------------------------------------------------- setup
@@ -616,7 +626,7 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
   }
   if (threadIdx.x == 0) {
     for (int i = 0; i < NS; ++i) {
-      const int nfull = p.cp_kv ? (p.q_tma ? 64 : 32) : (g4_lsu ? 33 : 1);  // cp.async lanes (+ the expect_tx arrival)
+      const int nfull = p.cp_kv ? (p.q_tma ? 64 : 32) : (g4_lsu ? 1 + 32 * (1 + (g4_lsu2 ? 1 : 0) + (GLAD_G4_LSU_W0 ? 1 : 0)) : 1);  // cp.async lanes (+ the expect_tx arrival)
       mbar_init(&kv_full[i], nfull);
       mbar_init(&kv_empty[i], 1);
       mbar_init(&kv_full_hi[i], nfull);
@@ -777,11 +787,13 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
         }
       }
     }
-  } else if (warp == 0 || (warp == 3 && p.g4 && p.q_tma)) {
+  } else if (warp == 0 || (warp == 3 && p.g4 && p.q_tma) || (warp == 2 && g4_lsu2)) {
     // ========================= TMA producer (all 32 lanes issue) =========================
     // (gather4 mode with TMA-loaded Q: warp 3 is a second producer warp that
     // issues half of every tile's row groups)
-    named_bar_sync(3, 96);  // the first Q load is issued first: QK needs Q, not a second tile
+    // the first Q load is issued first: QK needs Q, not a second tile (with
+    // two LSU warps, warp 2 is the Q loader and arrives once it issued Q(0))
+    if (warp != 2) named_bar_sync(3, 96);
     if (trace && lane == 0 && warp == 0) trace[4] = globaltimer();
     const int box_rows = p.box_rows;
     // Boxes per page run of a tile: the latent slice (4-D map: NLO chunks
@@ -848,10 +860,29 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
     // the prefetch cursor is positioned after the first stage load is out
     // (kernel start is latency-bound: the first load must not wait for it)
     bool pf_ready = false;
-    int k = 0, u = 0, it = 0;
+    int k = 0, u = 0, it = 0, seg = 0;
     Seg s;
     while (next_seg(k, u, s)) {
       const int* bt_row = p.block_table + static_cast<size_t>(s.b) * p.bt_stride;
+      if (warp == 2) {  // (g4_lsu2) this segment's Q by TMA, as the Q loader does
+        const int qbuf = seg % C::NQB;
+        if (seg >= C::NQB) mbar_wait(&q_empty[qbuf], ((seg - C::NQB) / C::NQB) & 1);
+        if (lane == 0) {
+          constexpr int QCH0 = C::ROWS ? C::NCH_QK : 0;
+          const uint32_t qdst = sbase + C::OFF_Q + qbuf * C::QBYTES;
+          mbar_arrive_expect_tx(&q_full[qbuf], static_cast<uint32_t>(C::QBYTES));
+          const int c1 = s.head * p.g_q + (p.q_box_t == 1 ? s.n0 % p.g_q : 0);
+          const int c2 = s.b * p.Lq + s.n0 / p.g_q;
+#pragma unroll
+          for (int ch = QCH0; ch < C::NQCH; ++ch) {
+            const int col = ch < C::NCH_QK ? ch * 64 : C::D_KN;
+            tma_load_3d(qdst + (ch - QCH0) * C::QCHUNK, &qmap, &q_full[qbuf], col, c1, c2);
+          }
+        }
+        __syncwarp();
+        if (seg == 0) named_bar_arrive(3, 96);
+      }
+      ++seg;
       for (int tl = s.t0; tl < s.t1; ++tl, ++it) {
         const int stage = it % NS;
         const int p0 = tl * T;
@@ -915,17 +946,24 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
                             rr[0], rr[1], rr[2], rr[3]);
               tma_gather4(stage_addr + C::OFF_R + r * 128, &lmap, bar_hi, p.rope_col, rr[0], rr[1], rr[2], rr[3]);
             }
-          } else {
+          }
+          if (g4_lsu && (warp != 0 || GLAD_G4_LSU_W0)) {
             // LSU rows [4 ng4, ntok): each lane resolves one row's pool row,
             // then per row the warp copies the latent slice (lane = 16-B unit)
             // and the RoPE part into the same 128B-swizzled layout
             const __nv_bfloat16* base_h = p.pool + s.head * p.d_head + lane * 8;
             const __nv_bfloat16* base_r = p.pool + p.rope_col + (lane & 7) * 8;
-            for (int rb = 4 * ng4; rb < ntok; rb += 32) {
+            // LSU warps 3 (, 2 with g4_lsu2, 0 with GLAD_G4_LSU_W0 after its
+            // gather4 issues) copy equal contiguous parts of the rows
+            constexpr int NLW = 1 + (GLAD_G4_LSU_WARPS == 2 ? 1 : 0) + (GLAD_G4_LSU_W0 ? 1 : 0);
+            const int li = warp == 3 ? 0 : (warp == 2 ? 1 : NLW - 1);
+            const int h = (ntok - 4 * ng4 + NLW - 1) / NLW;
+            const int r_lo = min(ntok, 4 * ng4 + li * h), r_hi = min(ntok, r_lo + h);
+            for (int rb = r_lo; rb < r_hi; rb += 32) {
               const int myr = rb + lane;
               const int pos = p0 + min(myr, ntok - 1);
               const int myrow = __ldg(bt_row + (pos >> p.log2_page)) * p.page_size + (pos & (p.page_size - 1));
-              const int nr = min(32, ntok - rb);
+              const int nr = min(32, r_hi - rb);
 #pragma unroll 4
               for (int j = 0; j < nr; ++j) {
                 const int r = rb + j;
@@ -983,6 +1021,7 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
         }
       }
     }
+    if (warp == 2 && seg == 0) named_bar_arrive(3, 96);  // no work: release the other producer warps
   } else if (warp == 1 && p.dbg_load_only) {
     // debug: the memory side alone — release every stage as soon as it landed
     int k = 0, u = 0, it = 0, seg = 0;
@@ -1304,7 +1343,7 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
       }
       if (trace && lane == 0) trace[3] = cp.seg + 1;
     }
-  } else if (warp < 4 && !(warp == 3 && (p.cp_kv || p.g4) && p.q_tma)) {
+  } else if (warp < 4 && !(warp == 3 && (p.cp_kv || p.g4) && p.q_tma) && !(warp == 2 && g4_lsu2)) {
     // ========================= Q loader: TMA (one thread) or cp.async (64 threads) =========================
     const int tid = threadIdx.x - 64;
     constexpr int QCH0 = C::ROWS ? C::NCH_QK : 0;  // first Q chunk staged in shared memory
