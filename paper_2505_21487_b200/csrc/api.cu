@@ -15,6 +15,10 @@
 #include "../../include/glad.h"
 #include "internal.h"
 
+#ifndef GLAD_MIN_GROUP_CTAS
+#define GLAD_MIN_GROUP_CTAS 8
+#endif
+
 namespace {
 
 thread_local char g_err[512] = "no error";
@@ -221,7 +225,9 @@ glad_status decode_common(Variant v, const void* q, const void* pool, const glad
   if (cl_n == 1 && g.n_qblk > 1 && !(g_phase_mask & 128) && ngq <= 16 && R0 >= 16 * ngq) {
     qb_outer = 1;
     n_groups = static_cast<int>(ngq);
-  } else if (L->n_heads_kv > 1 && R0 >= L->n_heads_kv) {
+  } else if (L->n_heads_kv > 1 && R0 >= GLAD_MIN_GROUP_CTAS * L->n_heads_kv) {
+    // (not with fewer than GLAD_MIN_GROUP_CTAS CTAs per head: the
+    // materialised prefill's 128 "heads" would leave 20 of 148 SMs idle)
     n_groups = L->n_heads_kv;
   }
   const int R = n_groups > 1 ? (R0 / n_groups) * n_groups : R0;

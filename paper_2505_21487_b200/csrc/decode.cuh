@@ -98,6 +98,17 @@ struct DecodeParams {
 #ifndef GLAD_PF_MAX_NS
 #define GLAD_PF_MAX_NS 2
 #endif
+// Rows mode, measured slower and off (A/B, decode ms; no-change / QNB2 / QNB2 + defer / defer):
+// C6 materialised prefill 2.83 / 2.95 / 2.91 / 2.90, C7 GTA prefill 1.04 / 1.14 / 1.09 / 1.06:
+// the early next-Q load stalls the softmax warps on its global loads in the
+// first tile of every segment, and the piecewise epilogue adds TMEM reads to
+// the per-tile softmax path.
+#ifndef GLAD_ROWS_QNB2
+#define GLAD_ROWS_QNB2 0  // two TMEM Q state-part buffers (next segment's Q written during this one)
+#endif
+#ifndef GLAD_ROWS_DEFER
+#define GLAD_ROWS_DEFER 0  // segment epilogue deferred into the next segment's tiles (two O buffers)
+#endif
 #ifndef GLAD_ROWS_NS_CAP
 #define GLAD_ROWS_NS_CAP 4
 #endif
@@ -296,7 +307,15 @@ struct DecodeCfg {
   static constexpr int QNCOLS = ROWS ? D_KN / 2 : 0;  // rows mode: Q state part, 2 bf16 per column
   static constexpr int NOB = (2 * SCOLS + 2 * OCOLS + QNCOLS <= 512) ? 2 : 1;
   static constexpr int QN_COL = 2 * SCOLS + NOB * OCOLS;
-  static constexpr int TMEM_USED = QN_COL + QNCOLS;
+  // rows mode: two Q state-part buffers when TMEM allows (D_V = 128: the
+  // materialised prefill, GTA), so the next segment's Q is written during
+  // this segment and its first QK follows this segment's last one at once
+  static constexpr int QNB = (ROWS && GLAD_ROWS_QNB2 && QN_COL + 2 * QNCOLS <= 512) ? 2 : 1;
+  // rows mode with two O buffers: the segment epilogue is deferred into the
+  // next segment's tiles (one 32-column piece per tile) instead of stalling
+  // the softmax warps at every segment switch
+  static constexpr bool RDEFER = ROWS && NOB == 2 && GLAD_ROWS_DEFER;
+  static constexpr int TMEM_USED = QN_COL + QNB * QNCOLS;
   static constexpr int TMEM_COLS =
       TMEM_USED <= 32 ? 32 : TMEM_USED <= 64 ? 64 : TMEM_USED <= 128 ? 128 : TMEM_USED <= 256 ? 256 : 512;
   static constexpr int NTHREADS = 384;
@@ -543,7 +562,7 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
   uint64_t* q_empty = bars + 22;   // [2] last QK of segment s done: Q buffer (s % NQB) free
   uint64_t* o_empty = bars + 24;   // [2] epilogue read O buffer (s & 1) (8 arrivals)
   uint64_t* cl_empty = bars + 26;  // [4] cluster: stage free in all cl_n CTAs (leader's copy is used)
-  uint64_t* qn_full = bars + 30;   // [1] rows mode: Q state part of segment s written to TMEM (8 warps)
+  uint64_t* qn_full = bars + 30;   // [2] rows mode: Q state part of segment s written to TMEM buffer s % QNB (8 warps)
   uint64_t* kv_full_hi = reinterpret_cast<uint64_t*>(aux + 2560);   // [4] split stages: hi half + RoPE landed
   uint64_t* kv_empty_hi = reinterpret_cast<uint64_t*>(aux + 2592);  // [4] split stages: hi half + P^T free
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(aux + 256);
@@ -640,7 +659,7 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
     }
     for (int i = 0; i < 4; ++i) mbar_init(&pv_done[i], 1);
     for (int i = 0; i < 4; ++i) mbar_init(&cl_empty[i], p.cl_n);
-    mbar_init(qn_full, 4 * GLAD_ROWS_WG);
+    for (int i = 0; i < 2; ++i) mbar_init(&qn_full[i], 4 * GLAD_ROWS_WG);
     for (int i = 0; i < 2; ++i) {
       mbar_init(&q_full[i], p.q_tma ? 1 : 64);
       mbar_init(&q_empty[i], 1);
@@ -1119,10 +1138,11 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
           if (trace && first && cq.seg > 0 && cq.seg < 8 && lane == 0) {  // debug: when each Q barrier flips
             const int sl = kTraceStride - 32 + 3 * cq.seg;
             if (trace[sl] == 0 && mbar_test_wait(smem_u32(&q_full[cq.seg % C::NQB]), (cq.seg / C::NQB) & 1)) trace[sl] = globaltimer();
-            if (trace[sl + 1] == 0 && mbar_test_wait(smem_u32(qn_full), cq.seg & 1)) trace[sl + 1] = globaltimer();
+            if (trace[sl + 1] == 0 && mbar_test_wait(smem_u32(&qn_full[cq.seg % C::QNB]), (cq.seg / C::QNB) & 1)) trace[sl + 1] = globaltimer();
             if (trace[sl + 2] == 0) trace[sl + 2] = globaltimer();  // first probe of this segment's first QK
           }
-          if (!first || (probe(&q_full[cq.seg % C::NQB], (cq.seg / C::NQB) & 1) && probe(qn_full, cq.seg & 1))) {
+          if (!first || (probe(&q_full[cq.seg % C::NQB], (cq.seg / C::NQB) & 1) &&
+                         probe(&qn_full[cq.seg % C::QNB], (cq.seg / C::QNB) & 1))) {
             qk_go = true;
             if (trace && lane == 0 && next_qk == 0) trace[1] = globaltimer();
             if (trace && lane == 0 && next_qk < kTraceTiles) trace[9 + 12 * next_qk] = globaltimer();
@@ -1145,7 +1165,7 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
             for (int e = e0; e < (e0 + QK_CHUNK < NQK ? e0 + QK_CHUNK : NQK); ++e) {
               if (e < C::NCH_QK * 4) {
                 if (GLAD_DBG_NO_TS) continue;
-                umma_f16_ts_warp(d, tm + C::QN_COL + e * 8,
+                umma_f16_ts_warp(d, tm + C::QN_COL + (cq.seg % C::QNB) * C::QNCOLS + e * 8,
                                  kd + static_cast<uint64_t>(((e >> 2) * 1024 + (e & 3) * 32) >> 4), idesc_qk, e != 0);
               } else {
                 umma_f16_ss_warp(d, qd + static_cast<uint64_t>(((e - C::NCH_QK * 4) * 32) >> 4),
@@ -1424,8 +1444,8 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
     const float sl2 = p.scale_log2;
     // Q state part of segment sq's row n (this WG's half of D_KN) -> TMEM
     // (A operand of the TS-mode QK: lane = row, 2 bf16 per column).  Called
-    // once the previous segment's last QK has completed (its S was read).
-    auto load_q = [&](const Seg& sq) {
+    // once the last QK that read buffer qb has completed (its S was read).
+    auto load_q = [&](const Seg& sq, int qb) {
       constexpr int NV = C::D_KN / (8 * NWGR);  // 16-B vectors of this thread's part of the row
       uint4 v[NV];
       if (n < sq.nq) {
@@ -1438,13 +1458,13 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
 #pragma unroll
         for (int i = 0; i < NV; ++i) v[i] = make_uint4(0u, 0u, 0u, 0u);
       }
-      const uint32_t qa = tmem + lane_addr + C::QN_COL + wg * (C::D_KN / (2 * NWGR));
+      const uint32_t qa = tmem + lane_addr + C::QN_COL + qb * C::QNCOLS + wg * (C::D_KN / (2 * NWGR));
 #pragma unroll
       for (int i = 0; i < NV; i += 4) tmem_st16_u32(qa + i * 4, reinterpret_cast<const uint32_t*>(v + i));
       tmem_st_wait();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(qn_full);
+      if (lane == 0) mbar_arrive(&qn_full[qb]);
     };
     // debug phase timer (warp 4 of a traced launch): cycles spent between
     // softmax checkpoints, summed over tiles, written at the end
@@ -1455,7 +1475,45 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
     int k = 0, u = 0, seg = 0, it = 0;
     Seg s;
     bool have = next_seg(k, u, s);
-    if (have) load_q(s);
+    if (have) load_q(s, 0);
+    // pending (deferred) epilogue of the previous segment (RDEFER): O buffer,
+    // 1/l, destination row, next 32-column piece (DH = none pending)
+    int e_c = DH, e_j = 0, e_seg = 0;
+    bool e_valid = false, e_whole = false;
+    float e_inv = 0.f;
+    uint32_t e_obuf = 0;
+    __nv_bfloat16* e_orow = nullptr;
+    float* e_prow = nullptr;
+    auto epi_piece = [&]() {
+      if (e_c == 0) {  // the segment's last PV must have completed
+        mbar_wait(&pv_done[e_j & 3], (e_j >> 2) & 1);
+        tc_fence_after();
+      }
+      const int c = e_c;
+      float o[32];
+      tmem_ld32(e_obuf + c, o);
+      tmem_ld_wait();
+      if (c + 32 == DH) {  // O consumed: the segment after next may reuse the buffer
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&o_empty[e_seg % C::NOB]);
+      }
+      if (e_valid) {
+        if (e_whole) {
+#pragma unroll
+          for (int q = 0; q < 32; q += 8)
+            *reinterpret_cast<uint4*>(e_orow + c + q) =
+                make_uint4(pack_bf16x2(o[q] * e_inv, o[q + 1] * e_inv), pack_bf16x2(o[q + 2] * e_inv, o[q + 3] * e_inv),
+                           pack_bf16x2(o[q + 4] * e_inv, o[q + 5] * e_inv), pack_bf16x2(o[q + 6] * e_inv, o[q + 7] * e_inv));
+        } else {
+#pragma unroll
+          for (int q = 0; q < 32; q += 4)
+            *reinterpret_cast<float4*>(e_prow + c + q) =
+                make_float4(o[q] * e_inv, o[q + 1] * e_inv, o[q + 2] * e_inv, o[q + 3] * e_inv);
+        }
+      }
+      e_c += 32;
+    };
     while (have) {
       int vend = 0, t_row = 0, h_row = 0;
       if (n < s.nq) {
@@ -1467,6 +1525,8 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
       float m = -INFINITY, nm = 0.f;  // running max (log2 units), -m (0 while m = -inf)
       float2 l2 = make_float2(0.f, 0.f);
       const uint32_t obuf = tmem + lane_addr + C::TMEM_O + (seg % C::NOB) * C::OCOLS + wg * DH;
+      Seg sn;
+      bool have_n = false, peeked = false;
       for (int tl = s.t0; tl < s.t1; ++tl, ++it) {
         const int sb = it & 1;
         const uint32_t sbuf = tmem + lane_addr + sb * C::SCOLS;
@@ -1579,12 +1639,23 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
         if (trace && threadIdx.x == 256 && it < kTraceTiles) trace[14 + 12 * it] = globaltimer();
         if (trace && lane == 0 && it < kTraceTiles)  // debug: last softmax warp's P arrival
           atomicMax(reinterpret_cast<unsigned long long*>(trace + 19 + 12 * it), globaltimer());
+        if (C::QNB == 2 && !peeked) {
+          // two Q buffers: the next segment's Q goes into the other one as soon
+          // as this segment's first S was seen (every QK of segment seg - 1,
+          // the buffer's last reader, has completed: the MMA pipe is in order)
+          peeked = true;
+          have_n = next_seg(k, u, sn);
+          if (have_n) load_q(sn, (seg + 1) & 1);
+        }
+        if (C::RDEFER && e_c < DH) epi_piece();  // the previous segment's O, one piece per tile
       }
-      // next segment's Q into TMEM now (this segment's last QK is done), so the
-      // load overlaps the epilogue below
-      Seg sn;
-      const bool have_n = next_seg(k, u, sn);
-      if (have_n) load_q(sn);
+      if (!peeked) {
+        // next segment's Q into TMEM now (this segment's last QK is done), so
+        // the load overlaps the epilogue below
+        have_n = next_seg(k, u, sn);
+        if (have_n) load_q(sn, (seg + 1) % C::QNB);
+      }
+      if (C::RDEFER) while (e_c < DH) epi_piece();  // (a segment with fewer tiles than pieces)
       if (trace && threadIdx.x == 128 && it - 1 < kTraceTiles) trace[18 + 12 * (it - 1)] = globaltimer();  // next Q in TMEM
       // ---- segment epilogue: O / l, lse (natural log); each WG writes its O half
       float ls = l2.x + l2.y;
@@ -1595,8 +1666,10 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
       }
       const float inv_l = ls > 0.f ? 1.f / ls : 0.f;
       const int j = it - 1;
-      mbar_wait(&pv_done[j & 3], (j >> 2) & 1);
-      tc_fence_after();
+      if (!C::RDEFER) {
+        mbar_wait(&pv_done[j & 3], (j >> 2) & 1);
+        tc_fence_after();
+      }
       // partial slot: 2 per range — the range's first segment (2c) or its
       // last one (2c + 1); only those two can be cut by a range boundary
       const int slot = (2 * (cta / p.cl_n) + (seg == 0 ? 0 : 1)) * p.cl_n + cta % p.cl_n;
@@ -1608,8 +1681,19 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
       }
       __nv_bfloat16* orow = p.out + ((static_cast<size_t>(s.b) * p.Lq + t_row) * p.H + h_row) * C::D_V + wg * DH;
       float* prow = p.o_part + (static_cast<size_t>(slot) * NQ + n) * C::D_V + wg * DH;
+      if (C::RDEFER) {  // written piecewise during the next segment's tiles (epi_piece)
+        e_c = 0;
+        e_j = j;
+        e_seg = seg;
+        e_valid = valid;
+        e_whole = s.whole;
+        e_inv = inv_l;
+        e_obuf = obuf;
+        e_orow = orow;
+        e_prow = prow;
+      }
 #pragma unroll 1
-      for (int c = 0; c < DH; c += 32) {
+      for (int c = 0; c < (C::RDEFER ? 0 : DH); c += 32) {
         float o[32];
         tmem_ld32(obuf + c, o);
         tmem_ld_wait();
@@ -1640,6 +1724,7 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
       have = have_n;
       PH(5);
     }
+    if (C::RDEFER) while (e_c < DH) epi_piece();  // the last segment's O
     if (GLAD_SOFTMAX_PHASES && trace && threadIdx.x == 128)
       for (int i = 0; i < 6; ++i) trace[kTraceStride - 14 + i] = static_cast<uint64_t>(ph_acc[i]);
     }
