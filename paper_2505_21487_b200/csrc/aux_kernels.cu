@@ -89,11 +89,13 @@ __global__ void combine_kernel(const float* __restrict__ o_part, const float* __
 // -> exclusive prefix sum plan[0..U]; plan[U] = total tiles.  Also writes
 // the output of units with no visible key (zeros, lse = -inf), which no
 // decode CTA visits.
-__global__ void plan_kernel(const int32_t* __restrict__ seqlens, int32_t* __restrict__ plan, int U, int cl_n,
+__global__ void plan_kernel(const int32_t* __restrict__ seqlens, int32_t* __restrict__ plan, int32_t* __restrict__ cnt,
+                            int U, int cl_n,
                             int B, int tile, int n_qblk, int qb_outer, int nq_blk, int Lq, int g_q,
                             int causal, int H, int d_v, __nv_bfloat16* __restrict__ out, float* __restrict__ lse,
                             uint64_t* trace) {
   if (trace && threadIdx.x == 0) trace[0] = globaltimer();
+  griddep_launch();  // (PDL) the decode kernel's prologue may start now; it waits for this grid before reading plan
   __shared__ int warp_sums[32];
   __shared__ int carry;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
@@ -102,6 +104,7 @@ __global__ void plan_kernel(const int32_t* __restrict__ seqlens, int32_t* __rest
   for (int base = 0; base < U; base += blockDim.x) {
     const int u = base + threadIdx.x;
     int tiles = 0;
+    if (cnt && u < U) cnt[u] = 0;  // in-kernel merge counters
     if (u < U) {
       // plan entry u: unit u, or with clusters the (head, sequence) group of
       // cl_n units whose tiles are those of its last query block (most keys)
@@ -155,10 +158,10 @@ __global__ void plan_kernel(const int32_t* __restrict__ seqlens, int32_t* __rest
   if (trace && threadIdx.x == 0) trace[1] = globaltimer();
 }
 
-cudaError_t launch_plan(const int32_t* seqlens, int32_t* plan, int U, int cl_n, int B, int tile, int n_qblk,
+cudaError_t launch_plan(const int32_t* seqlens, int32_t* plan, int32_t* cnt, int U, int cl_n, int B, int tile, int n_qblk,
                         int qb_outer, int nq_blk, int Lq, int g_q, int causal, int H, int d_v, void* out, float* lse,
                         uint64_t* trace, cudaStream_t stream) {
-  plan_kernel<<<1, 1024, 0, stream>>>(seqlens, plan, U, cl_n, B, tile, n_qblk, qb_outer, nq_blk, Lq, g_q, causal, H, d_v,
+  plan_kernel<<<1, 1024, 0, stream>>>(seqlens, plan, cnt, U, cl_n, B, tile, n_qblk, qb_outer, nq_blk, Lq, g_q, causal, H, d_v,
                                       static_cast<__nv_bfloat16*>(out), lse, trace);
   return cudaGetLastError();
 }
@@ -179,10 +182,11 @@ constexpr int kMergeMaxParts = 8;  // weights staged per pass
 __global__ void __launch_bounds__(kMergeThreads) merge_split_kernel(
     const int32_t* __restrict__ plan, const float* __restrict__ o_part, const float* __restrict__ lse_part, int G,
     int cl_n, int U, int nq_blk, int n_qblk, int qb_outer, int B, int n_groups, int g_q, int Lq, int H, int d_v,
-    __nv_bfloat16* __restrict__ out, float* __restrict__ lse) {
+    int pair_merged, __nv_bfloat16* __restrict__ out, float* __restrict__ lse) {
   __shared__ int u_s;
   __shared__ float w_s[kMergeMaxParts][128];  // nq_blk <= 128 (rows mode)
   __shared__ float mx_s[128], iz_s[128];
+  griddep_wait();  // (PDL) the decode grid's partials and plan are complete and visible
   const int GR = G / cl_n;                     // ranges
   const int b_cta = blockIdx.x / cl_n + 1;     // boundary between ranges b-1 and b
   const int rank = blockIdx.x % cl_n;
@@ -210,6 +214,7 @@ __global__ void __launch_bounds__(kMergeThreads) merge_split_kernel(
   const int cf = cta_of_tile(pu0, GR, plan, U, n_groups);
   if (cf != b_cta - 1) return;  // an earlier boundary cuts it: that block merges
   const int cl = cta_of_tile(pu1 - 1, GR, plan, U, n_groups);
+  if (pair_merged && cl == cf + 1) return;  // two-part unit: merged inside the decode kernel
   const int u = pe * cl_n + rank;
   const UnitIdx ui = unit_idx(u, B, n_qblk, qb_outer);
   const int qb = ui.qb, b = ui.b, head = ui.head;
@@ -283,12 +288,20 @@ __global__ void __launch_bounds__(kMergeThreads) merge_split_kernel(
 
 cudaError_t launch_merge_split(const int32_t* plan, const float* o_part, const float* lse_part, int G, int cl_n,
                                int U, int nq_blk, int n_qblk, int qb_outer, int B, int n_groups, int g_q, int Lq,
-                               int H, int d_v, void* out, float* lse, cudaStream_t stream) {
+                               int H, int d_v, int pair_merged, void* out, float* lse, cudaStream_t stream) {
   if (G / cl_n < 2) return cudaSuccess;
-  merge_split_kernel<<<dim3((G / cl_n - 1) * cl_n, GLAD_MERGE_SPLIT), kMergeThreads, 0, stream>>>(
-      plan, o_part, lse_part, G, cl_n, U, nq_blk, n_qblk, qb_outer, B, n_groups, g_q, Lq, H, d_v,
-      static_cast<__nv_bfloat16*>(out), lse);
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((G / cl_n - 1) * cl_n, GLAD_MERGE_SPLIT);
+  cfg.blockDim = dim3(kMergeThreads);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = GLAD_PDL ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, merge_split_kernel, plan, o_part, lse_part, G, cl_n, U, nq_blk, n_qblk, qb_outer, B,
+                            n_groups, g_q, Lq, H, d_v, pair_merged, static_cast<__nv_bfloat16*>(out), lse);
 }
 
 cudaError_t launch_append(void* pool, int64_t row_stride, int page_size, const int32_t* block_table,

@@ -73,6 +73,8 @@ struct DecodeParams {
   int32_t q_box_h, q_box_t;
   float scale_log2;         // softmax_scale * log2(e)
   int32_t dbg_load_only;    // debug (phase-mask bit 64): stream the KV tiles only (no QK / softmax / PV; output garbage)
+  int32_t* fix_cnt;         // [U] in-kernel split merge: parts of each cut unit written so far (nullptr:
+                            // the merge kernel combines them; zeroed by the plan kernel, reset by the merger)
   int cl_n;                 // CTAs per cluster = query blocks per (head, sequence); 1 = no cluster.
                             // With cl_n > 1 the plan is over (head, sequence) groups, the CTAs of a
                             // cluster share each KV tile (TMA multicast) and CTA rank r owns query
@@ -103,6 +105,18 @@ struct DecodeParams {
 // the early next-Q load stalls the softmax warps on its global loads in the
 // first tile of every segment, and the piecewise epilogue adds TMEM reads to
 // the per-tile softmax path.
+#ifndef GLAD_ROWS_DEFER
+#define GLAD_ROWS_DEFER 0
+#endif
+// swap-AB blocks: two-part cut units merged inside the decode kernel by
+// their first CTA when phase-mask bit 512 is set (A/B, step ms, merge kernel
+// -> in-kernel: C2 GLA-2 0.276 -> 0.270, C2 MLA 0.469 -> 0.458, C4 GTA equal,
+// but the decode kernel alone +5 %: off by default); rows mode keeps the
+// merge kernel (the mid-kernel release fence and the owner's tail reads cost
+// more there: C3 q_len 2 0.199 -> 0.211)
+#ifndef GLAD_FIXUP
+#define GLAD_FIXUP 1
+#endif
 #ifndef GLAD_ROWS_QNB2
 #define GLAD_ROWS_QNB2 0  // two TMEM Q state-part buffers (next segment's Q written during this one)
 #endif
@@ -540,6 +554,46 @@ __device__ __forceinline__ Seg seg_from_entry(const DecodeParams& p, const int4*
   return s;
 }
 
+// In-kernel merge of two-part cut units (the common split: a unit cut by
+// one CTA range boundary).  Role of this CTA's segment s: 0 = none (whole
+// unit, or cut into > 2 parts: the merge kernel combines those), 1 = owner
+// (the unit's first CTA: the unit is its LAST segment, so it ends at the end
+// of the kernel; it waits for the other part and writes the merged output),
+// 2 = second part (the next CTA's FIRST segment, finished early: writes its
+// normalised partial + lse and releases it with a fence + counter add).
+__device__ __forceinline__ int pair_role(const DecodeParams& p, const Seg& s) {
+  if (!p.fix_cnt || s.whole) return 0;
+  const int G = gridDim.x;
+  const int pu0 = __ldg(p.plan + s.pi), pu1 = __ldg(p.plan + s.pi + 1);
+  const int cf = cta_of_tile(pu0, G, p.plan, p.n_units, p.n_groups);
+  const int cl = cta_of_tile(pu1 - 1, G, p.plan, p.n_units, p.n_groups);
+  if (cl != cf + 1) return 0;
+  return static_cast<int>(blockIdx.x) == cf ? 1 : 2;
+}
+__device__ __forceinline__ void pair_wait(const DecodeParams& p, int pi, int target) {
+  const long long t0 = clock64();
+  while (ld_acquire_gpu(p.fix_cnt + pi) < target) {
+    __nanosleep(64);
+    if (clock64() - t0 > (1ll << 34)) {
+      printf("glad: split-merge wait watchdog (block %d unit %d)\n", blockIdx.x, pi);
+      __trap();
+    }
+  }
+}
+// weights of the two parts' normalised outputs: exp(lse_x - lse)
+__device__ __forceinline__ void pair_weights(float lse_a, float lse_b, float& wa, float& wb, float& lse) {
+  const float mx = fmaxf(lse_a, lse_b);
+  if (mx == -INFINITY) {
+    wa = wb = 0.f;
+    lse = -INFINITY;
+    return;
+  }
+  const float ea = __expf(lse_a - mx), eb = __expf(lse_b - mx), z = ea + eb;
+  wa = ea / z;
+  wb = eb / z;
+  lse = mx + __logf(z);
+}
+
 template <class C>
 __global__ void __launch_bounds__(C::NTHREADS, 1)
     decode_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUtensorMap lmap,
@@ -567,6 +621,7 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
   uint64_t* kv_empty_hi = reinterpret_cast<uint64_t*>(aux + 2592);  // [4] split stages: hi half + P^T free
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(aux + 256);
   int* range_s = reinterpret_cast<int*>(aux + 264);        // [4] cta tile range, #segments, overflow unit
+  float* woth_s = reinterpret_cast<float*>(aux + 2624);   // [NQ <= 64] swap-AB owner merge: weight of the other part
   int4* segtab = reinterpret_cast<int4*>(aux + 3072);      // [MAXSEG][2] (seg_to_entry)
   int* rowtab = reinterpret_cast<int*>(aux + 3072 + C::MAXSEG * 32);  // [T] pool row per tile row (cp path)
   int* vend_s = reinterpret_cast<int*>(aux + 320);         // [NQ] visible-key end per query column
@@ -584,7 +639,12 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
   if (GLAD_TRACE && p.trace && threadIdx.x == 0) p.trace[static_cast<size_t>(cta) * kTraceStride + 7] = globaltimer();
 
   // ------------------------------------------------------------- setup
+  // (PDL) barrier init, TMEM alloc and descriptor prefetch below may overlap
+  // the plan kernel; everything that reads global memory another kernel
+  // wrote (plan, Q, cache, block table) comes after griddep_wait()
   if (warp == 0) {
+    griddep_wait();
+    griddep_launch();  // the merge kernel may be scheduled as SMs free up
     // Work range of this CTA and its segment table, with warp-parallel loads
     // (a serial search over the plan would cost one L2 round trip per step).
     const int U = p.n_units;
@@ -670,6 +730,7 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
     if (p.q_tma) tma_prefetch_desc(&qmap);
   }
   if (warp == 2) { tmem_alloc(tmem_slot, C::TMEM_COLS); tmem_relinquish(); }
+  if (warp != 0) griddep_wait();
   if (warp == 3) {
     // While warp 0 searches the plan: touch the block table, Q and the plan
     // so this SM's address translations are warm when the producer and the
@@ -1754,7 +1815,9 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
     // 1/l lives in einv_s[seg % NOB] until then.
     float* einv_s = reinterpret_cast<float*>(aux + 3072 + C::MAXSEG * 32 + T * 4);  // [NOB][NQ]
     int e_blk = C::NBLK_O;  // next block of the pending epilogue (NBLK_O = none pending)
-    int e_seg = 0, e_j = 0, e_ncols = 0, e_j0 = 0, e_slot = 0;
+    int e_seg = 0, e_j = 0, e_ncols = 0, e_j0 = 0, e_slot = 0, e_pi = 0;
+    bool e_rel = false;                // pending segment is the second part of a two-part unit
+    const float* e_oth = nullptr;      // owner: the other part's o_part rows (column c0)
     bool e_whole = false;
     size_t e_row0 = 0;
     auto epi_block = [&]() {
@@ -1786,6 +1849,17 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
           for (int n = 0; n < CW; n += 4) {
             const float4 a = ld_shared_f4(inv_addr + n * 4);
             v[n] = o[n] * a.x; v[n + 1] = o[n + 1] * a.y; v[n + 2] = o[n + 2] * a.z; v[n + 3] = o[n + 3] * a.w;
+          }
+          if (e_oth) {  // owner of a two-part unit: + w_other * the other part's normalised O
+            const uint32_t w_addr = smem_u32(woth_s + c0);
+#pragma unroll
+            for (int n = 0; n < CW; n += 4) {
+              const float4 w = ld_shared_f4(w_addr + n * 4);
+              v[n] += w.x * __ldcg(e_oth + static_cast<size_t>(n) * C::D_V + d);
+              v[n + 1] += w.y * __ldcg(e_oth + static_cast<size_t>(n + 1) * C::D_V + d);
+              v[n + 2] += w.z * __ldcg(e_oth + static_cast<size_t>(n + 2) * C::D_V + d);
+              v[n + 3] += w.w * __ldcg(e_oth + static_cast<size_t>(n + 3) * C::D_V + d);
+            }
           }
           const bool odd = lane & 1;
 #pragma unroll
@@ -1830,6 +1904,11 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
         }
       }
       ++e_blk;
+      if (e_rel && e_blk == C::NBLK_O) {  // second part of a two-part unit written: release it (per WG)
+        __threadfence();
+        named_bar_sync(bar_id, 128);
+        if (r == 0) atomicAdd(p.fix_cnt + e_pi, 1);
+      }
     };
     int k = 0, u = 0, seg = 0, it = 0;
     Seg s;
@@ -2035,22 +2114,36 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
       const float cs = warp_col_reduce<HC, false, LANES>(l, lane);
       if ((lane & ((1 << col_shift<HC, LANES>()) - 1)) == 0)
         red[(wg * 4 + wq) * 32 + (cb - c0) + ((lane & (LANES - 1)) >> col_shift<HC, LANES>())] = cs;
+      const int role = pair_role(p, s);
+      if (role == 1 && r == 0) {  // owner: the second part (both its WGs) must be out
+        pair_wait(p, s.pi, 2);
+        if (atomicAdd(p.fix_cnt + s.pi, 1) == 3) p.fix_cnt[s.pi] = 0;  // both owner WGs past: reset for the next launch
+      }
       named_bar_sync(bar_id, 128);
       // partial slot: 2 per range — the range's first segment (2c) or its
       // last one (2c + 1); only those two can be cut by a range boundary
       const int slot = (2 * (cta / p.cl_n) + (seg == 0 ? 0 : 1)) * p.cl_n + cta % p.cl_n;
+      const size_t slot_oth = static_cast<size_t>(2 * (cta + 1));  // owner: the next CTA's first-segment slot
       if (r < CW) {  // fold the row sum into alpha_s as 1/l (reused below) and write lse
         const float* rr = red + wg * 128 + r;
         const float ls = (rr[0] + rr[32]) + (rr[64] + rr[96]);
         alpha_s[c0 + r] = ls > 0.f ? 1.f / ls : 0.f;
         if (c0 + r < s.nq) {
           const float lse = ls > 0.f ? (m_run[c0 + r] + __log2f(ls)) * 0.69314718055994531f : -INFINITY;
-          if (s.whole) {
-            const int ng = s.n0 + c0 + r, t = ng / p.g_q, h = s.head * p.g_q + (ng - t * p.g_q);
+          const int ng = s.n0 + c0 + r, t = ng / p.g_q, h = s.head * p.g_q + (ng - t * p.g_q);
+          if (role == 1) {
+            float wa, wb, lse_t;
+            pair_weights(lse, __ldcg(p.lse_part + slot_oth * NQ + c0 + r), wa, wb, lse_t);
+            p.lse[(static_cast<size_t>(s.b) * p.Lq + t) * p.H + h] = lse_t;
+            alpha_s[c0 + r] *= wa;
+            woth_s[c0 + r] = wb;
+          } else if (s.whole) {
             p.lse[(static_cast<size_t>(s.b) * p.Lq + t) * p.H + h] = lse;
           } else {
             p.lse_part[static_cast<size_t>(slot) * NQ + c0 + r] = lse;
           }
+        } else if (role == 1) {
+          woth_s[c0 + r] = 0.f;
         }
       }
       // pending epilogue of this segment: 1/l to einv_s, output addressing
@@ -2061,12 +2154,15 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
       e_blk = 0;
       e_seg = seg;
       e_j = it - 1;  // last tile of this segment
-      e_whole = s.whole;
+      e_whole = s.whole || role == 1;  // the owner writes the merged output like a whole unit
       e_slot = slot;
+      e_pi = s.pi;
+      e_rel = (role == 2);
+      e_oth = role == 1 ? p.o_part + (slot_oth * NQ + c0) * C::D_V : nullptr;
       e_ncols = min(CW, s.nq - c0);
       e_j0 = 0;
       e_row0 = 0;
-      if (s.whole) {
+      if (e_whole) {
         const int ng = s.n0 + c0, t = ng / p.g_q;
         e_j0 = ng - t * p.g_q;
         e_row0 = (static_cast<size_t>(s.b) * p.Lq + t) * p.H + s.head * p.g_q + e_j0;

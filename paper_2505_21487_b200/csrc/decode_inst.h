@@ -18,22 +18,28 @@ cudaError_t launch_one(const CUtensorMap& tmap, const CUtensorMap& lmap, const C
   using C = DecodeCfg<DV, DKN, DR, NQ, T, DS>;
   cudaError_t e = set_smem_attr<C>();
   if (e != cudaSuccess) return e;
-  if (p.cl_n <= 1) {
-    decode_kernel<C><<<grid, C::NTHREADS, C::SMEM_BYTES, stream>>>(tmap, lmap, qmap, p);
-    return cudaGetLastError();
-  }
+  // PDL: the prologue overlaps the plan kernel's tail (griddep_wait in the kernel)
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(C::NTHREADS);
   cfg.dynamicSmemBytes = C::SMEM_BYTES;
   cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = p.cl_n;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
+  cudaLaunchAttribute attr[2];
+  int na = 0;
+  if (GLAD_PDL) {
+    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  if (p.cl_n > 1) {
+    attr[na].id = cudaLaunchAttributeClusterDimension;
+    attr[na].val.clusterDim.x = p.cl_n;
+    attr[na].val.clusterDim.y = 1;
+    attr[na].val.clusterDim.z = 1;
+    ++na;
+  }
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = na;
   return cudaLaunchKernelEx(&cfg, decode_kernel<C>, tmap, lmap, qmap, p);
 }
 

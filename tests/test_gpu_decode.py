@@ -215,6 +215,26 @@ def test_small_page_producers(cfg, mask, tile):
     check(out, lse, o_ref, lse_ref, what=f"mask={mask} {cfg}")
 
 
+@pytest.mark.parametrize("mask", [7, 7 | 512], ids=["merge_kernel", "in_kernel_merge"])
+@pytest.mark.parametrize("cfg", [(3, 1, 128, 2, 256, 64, [1500, 777, 4096], 64, 7),     # GLA-2 swap-AB, 3-part units
+                                 (2, 1, 128, 1, 512, 64, [2048, 900], 64, 64),         # MLA, query-block groups
+                                 (3, 2, 128, 2, 256, 64, [3000, 129, 1025], 16, 5),    # rows mode (q_len 2)
+                                 (2, 1, 16, 2, 128, 32, [5000, 1], 1, 11),             # page 1, one tiny unit
+                                 (4, 1, 64, 2, 256, 64, [640, 640, 640, 640], 64, 0)])  # 148 CTAs, many cuts
+def test_split_merge_paths(cfg, mask, tile):
+    """Units cut by CTA range boundaries: every cut unit merged by the merge
+    kernel (default), and (phase-mask bit 512) two-part units merged inside
+    the decode kernel by their first CTA with longer ones left to the merge
+    kernel, against the oracle."""
+    B, Lq, H, h_c, d_c, d_R, lens, page, ctas = cfg
+    glad.debug_set_phase_mask(mask)
+    try:
+        out, lse, o_ref, lse_ref = run_latent(B, Lq, H, h_c, d_c, d_R, np.array(lens), page, ctas=ctas, seed=41)
+    finally:
+        glad.debug_set_phase_mask(7)
+    check(out, lse, o_ref, lse_ref, what=f"mask={mask} {cfg}")
+
+
 @pytest.mark.parametrize("mask", [7, 7 | 128], ids=["qb_groups", "qb_inner"])
 @pytest.mark.parametrize("cfg", [(4, 1, 128, 1, 512, 64, [900, 333, 1, 2048], 64, 64),   # MLA: 2 query blocks
                                  (3, 2, 128, 1, 512, 64, [700, 1500, 64], 16, 0),        # MLA q_len 2: 4 blocks
@@ -289,7 +309,9 @@ def run_gta(B, Lq, H, h_kv, seqlens, page, ctas=0, causal=True, seed=0):
 
 
 @pytest.mark.parametrize("cfg", [(2, 1, 64, 8, [700, 333], 64, 0), (2, 2, 64, 8, [700, 333], 16, 2),
-                                 (3, 1, 32, 2, [129, 1, 400], 1, 1), (1, 4, 64, 4, [1500], 64, 3)])
+                                 (3, 1, 32, 2, [129, 1, 400], 1, 1), (1, 4, 64, 4, [1500], 64, 3),
+                                 (2, 1, 64, 8, [700, 333], 4, 5),      # hybrid small-page producer
+                                 (2, 16, 64, 8, [900, 333], 2, 0)])    # rows mode (128 rows), page 2
 def test_gta(cfg, tile):
     B, Lq, H, h_kv, lens, page, ctas = cfg
     out, lse, o_ref, lse_ref = run_gta(B, Lq, H, h_kv, np.array(lens), page, ctas=ctas, seed=7)
