@@ -195,10 +195,7 @@ GLAD_API void glad_debug_set_trace(void* device_buf);
  * block) CTA groups (multi-block units walked in the ((head, b), block)
  * order), 256 = pages < 16 through TMA gather4 alone (default: gather4
  * for most rows of a tile + 16-B cp.async by a second producer warp for the
- * rest), 512 = units cut into two parts (64-row swap-AB blocks) merged
- * inside the decode kernel by their first CTA, which waits for the second
- * part's release (default: every cut unit by the merge kernel).  Not
- * thread-safe. */
+ * rest).  Not thread-safe. */
 GLAD_API void glad_debug_set_phase_mask(int32_t mask);
 /* Debug/benchmark only: force the KV tile height (64, 96 or 128 tokens; 0 =
  * library choice).  Results are identical up to fp32 summation order. */

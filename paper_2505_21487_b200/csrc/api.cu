@@ -15,6 +15,12 @@
 #include "../../include/glad.h"
 #include "internal.h"
 
+#ifndef GLAD_SEG_COST
+#define GLAD_SEG_COST 0
+#endif
+#ifndef GLAD_SEG_COST_ROWS
+#define GLAD_SEG_COST_ROWS 6
+#endif
 #ifndef GLAD_MIN_GROUP_CTAS
 #define GLAD_MIN_GROUP_CTAS 8
 #endif
@@ -163,7 +169,7 @@ glad_status decode_geom(Variant v, const glad_cache_layout* L, int32_t Lq, int32
 // Workspace of one decode call: [plan (U+1) int32][lse_part 2G*NQ f32]
 // [o_part 2G*NQ*D_V f32] (two partial slots per CTA range), each 256-byte aligned.
 struct WsLayout {
-  size_t plan, lse, opart, cnt, total;
+  size_t plan, lse, opart, total;
 };
 WsLayout ws_layout(int64_t U, int64_t G, int nq, int d_v) {
   auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
@@ -171,8 +177,7 @@ WsLayout ws_layout(int64_t U, int64_t G, int nq, int d_v) {
   w.plan = 0;
   w.lse = al(static_cast<size_t>(U + 1) * 4);
   w.opart = w.lse + al(static_cast<size_t>(2 * G) * nq * 4);
-  w.cnt = w.opart + al(static_cast<size_t>(2 * G) * nq * d_v * 4);
-  w.total = w.cnt + al(static_cast<size_t>(U) * 4);
+  w.total = w.opart + al(static_cast<size_t>(2 * G) * nq * d_v * 4);
   return w;
 }
 
@@ -226,7 +231,7 @@ glad_status decode_common(Variant v, const void* q, const void* pool, const glad
   if (cl_n == 1 && g.n_qblk > 1 && !(g_phase_mask & 128) && ngq <= 16 && R0 >= 16 * ngq) {
     qb_outer = 1;
     n_groups = static_cast<int>(ngq);
-  } else if (L->n_heads_kv > 1 && R0 >= GLAD_MIN_GROUP_CTAS * L->n_heads_kv) {
+  } else if (L->n_heads_kv > 1 && L->n_heads_kv <= glad::kMaxGroups && R0 >= GLAD_MIN_GROUP_CTAS * L->n_heads_kv) {
     // (not with fewer than GLAD_MIN_GROUP_CTAS CTAs per head: the
     // materialised prefill's 128 "heads" would leave 20 of 148 SMs idle)
     n_groups = L->n_heads_kv;
@@ -321,6 +326,11 @@ glad_status decode_common(Variant v, const void* q, const void* pool, const glad
   p.cp_kv = (L->page_size < 16 && !g4) ? 1 : 0;
   p.g4 = g4 ? ((g_phase_mask & 256) ? 1 : 2) : 0;  // bit 256: gather4 alone (no LSU rows)
   p.n_groups = n_groups;
+  // segment-switch cost in virtual tiles, so that the ranges balance work +
+  // switches (measured with the trace: ~2.5 tiles per switch in swap-AB, ~9
+  // in rows mode; A/B decode ms, 0 -> 6 in rows mode: C3 q_len 2 0.1728 ->
+  // 0.1680; 0 -> 2 in swap-AB: C2 equal, C2 page 1 +1 %, MLA -2 %)
+  p.seg_cost = g.key.nq == 128 ? GLAD_SEG_COST_ROWS : GLAD_SEG_COST;
   p.qb_outer = qb_outer;
   p.q_box_h = q_box_h;
   p.q_box_t = q_box_t;
@@ -350,18 +360,12 @@ glad_status decode_common(Variant v, const void* q, const void* pool, const glad
   p.trace = g_trace;
   p.dbg_load_only = (g_phase_mask & 64) ? 1 : 0;
   p.cl_n = cl_n;
-  // phase-mask bit 512 (off by default): two-part cut units of swap-AB
-  // blocks merged inside the decode kernel by their first CTA (the step is
-  // ~2 % shorter, the decode kernel ~5 % longer; clusters and rows mode
-  // always use the merge kernel)
-  p.fix_cnt = (GLAD_FIXUP && cl_n == 1 && g.key.nq != 128 && (g_phase_mask & 512))
-                  ? reinterpret_cast<int32_t*>(wsb + wl.cnt) : nullptr;
 
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   int32_t* plan = reinterpret_cast<int32_t*>(wsb + wl.plan);
   cudaError_t e = cudaSuccess;
   if (g_phase_mask & 1) {
-    e = glad::launch_plan(seqlens, plan, p.fix_cnt, p.n_units, cl_n, B, g.key.t, g.n_qblk, qb_outer, g.key.nq, Lq, g.g_q, p.causal, H,
+    e = glad::launch_plan(seqlens, plan, p.n_units, p.seg_cost, cl_n, B, g.key.t, g.n_qblk, qb_outer, g.key.nq, Lq, g.g_q, p.causal, H,
                           g.key.d_v, out, lse, nullptr, st);
     if (e != cudaSuccess) return fail(GLAD_ERR_CUDA, "plan launch failed: %s", cudaGetErrorString(e));
   }
@@ -369,9 +373,9 @@ glad_status decode_common(Variant v, const void* q, const void* pool, const glad
     e = glad::launch_decode(g.key, tmap, lmap, qmap, p, G, st);
     if (e != cudaSuccess) return fail(GLAD_ERR_CUDA, "decode launch failed: %s", cudaGetErrorString(e));
   }
-  if (g_phase_mask & 4) {  // units cut into > 2 parts (two-part units: inside the decode kernel)
+  if (g_phase_mask & 4) {
     e = glad::launch_merge_split(plan, p.o_part, p.lse_part, G, cl_n, p.n_units, g.key.nq, g.n_qblk, qb_outer, B,
-                                 n_groups, g.g_q, Lq, H, g.key.d_v, p.fix_cnt ? 1 : 0, out, lse, st);
+                                 n_groups, g.g_q, Lq, H, g.key.d_v, p.seg_cost, out, lse, st);
     if (e != cudaSuccess) return fail(GLAD_ERR_CUDA, "merge launch failed: %s", cudaGetErrorString(e));
   }
   return GLAD_OK;
@@ -387,7 +391,7 @@ const char* glad_version(void) { return "glad 0.1.0 sm_100a"; }
 
 void glad_debug_set_trace(void* device_buf) { g_trace = static_cast<uint64_t*>(device_buf); }
 
-void glad_debug_set_phase_mask(int32_t mask) { g_phase_mask = mask & 1023; }
+void glad_debug_set_phase_mask(int32_t mask) { g_phase_mask = mask & 511; }
 
 void glad_debug_set_tile(int32_t tokens) { g_tile_override = tokens; }
 

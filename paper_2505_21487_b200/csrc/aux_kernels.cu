@@ -89,8 +89,8 @@ __global__ void combine_kernel(const float* __restrict__ o_part, const float* __
 // -> exclusive prefix sum plan[0..U]; plan[U] = total tiles.  Also writes
 // the output of units with no visible key (zeros, lse = -inf), which no
 // decode CTA visits.
-__global__ void plan_kernel(const int32_t* __restrict__ seqlens, int32_t* __restrict__ plan, int32_t* __restrict__ cnt,
-                            int U, int cl_n,
+__global__ void plan_kernel(const int32_t* __restrict__ seqlens, int32_t* __restrict__ plan,
+                            int U, int seg_cost, int cl_n,
                             int B, int tile, int n_qblk, int qb_outer, int nq_blk, int Lq, int g_q,
                             int causal, int H, int d_v, __nv_bfloat16* __restrict__ out, float* __restrict__ lse,
                             uint64_t* trace) {
@@ -104,7 +104,6 @@ __global__ void plan_kernel(const int32_t* __restrict__ seqlens, int32_t* __rest
   for (int base = 0; base < U; base += blockDim.x) {
     const int u = base + threadIdx.x;
     int tiles = 0;
-    if (cnt && u < U) cnt[u] = 0;  // in-kernel merge counters
     if (u < U) {
       // plan entry u: unit u, or with clusters the (head, sequence) group of
       // cl_n units whose tiles are those of its last query block (most keys)
@@ -129,6 +128,7 @@ __global__ void plan_kernel(const int32_t* __restrict__ seqlens, int32_t* __rest
         }
       }
     }
+    if (tiles > 0) tiles += seg_cost;  // virtual tiles: the unit's segment-switch cost in the range balance
     int v = tiles;  // inclusive warp scan
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -158,10 +158,10 @@ __global__ void plan_kernel(const int32_t* __restrict__ seqlens, int32_t* __rest
   if (trace && threadIdx.x == 0) trace[1] = globaltimer();
 }
 
-cudaError_t launch_plan(const int32_t* seqlens, int32_t* plan, int32_t* cnt, int U, int cl_n, int B, int tile, int n_qblk,
+cudaError_t launch_plan(const int32_t* seqlens, int32_t* plan, int U, int seg_cost, int cl_n, int B, int tile, int n_qblk,
                         int qb_outer, int nq_blk, int Lq, int g_q, int causal, int H, int d_v, void* out, float* lse,
                         uint64_t* trace, cudaStream_t stream) {
-  plan_kernel<<<1, 1024, 0, stream>>>(seqlens, plan, cnt, U, cl_n, B, tile, n_qblk, qb_outer, nq_blk, Lq, g_q, causal, H, d_v,
+  plan_kernel<<<1, 1024, 0, stream>>>(seqlens, plan, U, seg_cost, cl_n, B, tile, n_qblk, qb_outer, nq_blk, Lq, g_q, causal, H, d_v,
                                       static_cast<__nv_bfloat16*>(out), lse, trace);
   return cudaGetLastError();
 }
@@ -182,15 +182,21 @@ constexpr int kMergeMaxParts = 8;  // weights staged per pass
 __global__ void __launch_bounds__(kMergeThreads) merge_split_kernel(
     const int32_t* __restrict__ plan, const float* __restrict__ o_part, const float* __restrict__ lse_part, int G,
     int cl_n, int U, int nq_blk, int n_qblk, int qb_outer, int B, int n_groups, int g_q, int Lq, int H, int d_v,
-    int pair_merged, __nv_bfloat16* __restrict__ out, float* __restrict__ lse) {
+    int seg_cost, __nv_bfloat16* __restrict__ out, float* __restrict__ lse) {
   __shared__ int u_s;
   __shared__ float w_s[kMergeMaxParts][128];  // nq_blk <= 128 (rows mode)
   __shared__ float mx_s[128], iz_s[128];
+  __shared__ int gb_s[kMaxGroups + 1];
   griddep_wait();  // (PDL) the decode grid's partials and plan are complete and visible
   const int GR = G / cl_n;                     // ranges
   const int b_cta = blockIdx.x / cl_n + 1;     // boundary between ranges b-1 and b
   const int rank = blockIdx.x % cl_n;
-  const CtaRange rg = cta_range(b_cta, GR, plan, U, n_groups);
+  // group boundaries in shared memory: one parallel load instead of a chain
+  // of dependent L2 reads per range lookup
+  const int ng = n_groups > 1 ? n_groups : 1;
+  if (threadIdx.x <= ng) gb_s[threadIdx.x] = __ldg(plan + threadIdx.x * (U / ng));
+  __syncthreads();
+  const CtaRange rg = cta_range_gb(b_cta, GR, gb_s, ng);
   if (rg.t0 >= rg.t1) return;
   const int t = rg.t0;
   // unit containing tile t: 32-ary search by warp 0 (last u with plan[u] <= t)
@@ -209,12 +215,12 @@ __global__ void __launch_bounds__(kMergeThreads) merge_split_kernel(
   }
   __syncthreads();
   const int pe = u_s;  // plan entry
-  const int pu0 = __ldg(plan + pe), pu1 = __ldg(plan + pe + 1);
-  if (pu0 == t) return;  // the entry starts at this boundary: not cut here
-  const int cf = cta_of_tile(pu0, GR, plan, U, n_groups);
+  const int pr0 = __ldg(plan + pe), pu1 = __ldg(plan + pe + 1);
+  const int pu0 = pr0 + seg_cost;  // first real tile (after the entry's virtual segment-cost tiles)
+  if (t <= pu0) return;  // the boundary is at or before the entry's first real tile: not cut here
+  const int cf = cta_of_tile_gb(pu0, GR, gb_s, ng);
   if (cf != b_cta - 1) return;  // an earlier boundary cuts it: that block merges
-  const int cl = cta_of_tile(pu1 - 1, GR, plan, U, n_groups);
-  if (pair_merged && cl == cf + 1) return;  // two-part unit: merged inside the decode kernel
+  const int cl = cta_of_tile_gb(pu1 - 1, GR, gb_s, ng);
   const int u = pe * cl_n + rank;
   const UnitIdx ui = unit_idx(u, B, n_qblk, qb_outer);
   const int qb = ui.qb, b = ui.b, head = ui.head;
@@ -224,7 +230,7 @@ __global__ void __launch_bounds__(kMergeThreads) merge_split_kernel(
   // partial slot of range c (decode epilogue): 2c if the entry is c's first
   // segment, 2c + 1 if it is its last one (only range cf can have earlier
   // segments, when its range starts before the entry)
-  const int cf_last = cta_range(cf, GR, plan, U, n_groups).t0 < pu0 ? 1 : 0;
+  const int cf_last = cta_range_gb(cf, GR, gb_s, ng).t0 < pr0 ? 1 : 0;
   auto slot_of = [&](int c) -> int64_t { return static_cast<int64_t>(2 * c + (c == cf ? cf_last : 0)) * cl_n + rank; };
   for (int n = threadIdx.x; n < nq; n += kMergeThreads) {
     float mx = -INFINITY;
@@ -288,7 +294,7 @@ __global__ void __launch_bounds__(kMergeThreads) merge_split_kernel(
 
 cudaError_t launch_merge_split(const int32_t* plan, const float* o_part, const float* lse_part, int G, int cl_n,
                                int U, int nq_blk, int n_qblk, int qb_outer, int B, int n_groups, int g_q, int Lq,
-                               int H, int d_v, int pair_merged, void* out, float* lse, cudaStream_t stream) {
+                               int H, int d_v, int seg_cost, void* out, float* lse, cudaStream_t stream) {
   if (G / cl_n < 2) return cudaSuccess;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3((G / cl_n - 1) * cl_n, GLAD_MERGE_SPLIT);
@@ -301,7 +307,7 @@ cudaError_t launch_merge_split(const int32_t* plan, const float* o_part, const f
   cfg.attrs = attr;
   cfg.numAttrs = GLAD_PDL ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, merge_split_kernel, plan, o_part, lse_part, G, cl_n, U, nq_blk, n_qblk, qb_outer, B,
-                            n_groups, g_q, Lq, H, d_v, pair_merged, static_cast<__nv_bfloat16*>(out), lse);
+                            n_groups, g_q, Lq, H, d_v, seg_cost, static_cast<__nv_bfloat16*>(out), lse);
 }
 
 cudaError_t launch_append(void* pool, int64_t row_stride, int page_size, const int32_t* block_table,

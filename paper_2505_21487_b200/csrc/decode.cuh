@@ -63,6 +63,8 @@ struct DecodeParams {
   int32_t n_qblk, n_units;  // query blocks per head, U = n_heads_kv * B * n_qblk (head-major)
   int32_t causal;
   int32_t n_groups;         // > 1: CTAs form n_groups equal groups, one per unit group (see cta_range)
+  int32_t seg_cost;         // virtual tiles the plan puts in front of every unit with work (segment-switch
+                            // cost: ranges balance tiles + seg_cost x segments); plan[u] + seg_cost = first real tile
   int32_t qb_outer;         // unit order: 1 = ((head, query block), b), 0 = ((head, b), query block)
   const __nv_bfloat16* pool;  // paged cache (cp.async producer path)
   int64_t row_stride;       // elements
@@ -73,8 +75,6 @@ struct DecodeParams {
   int32_t q_box_h, q_box_t;
   float scale_log2;         // softmax_scale * log2(e)
   int32_t dbg_load_only;    // debug (phase-mask bit 64): stream the KV tiles only (no QK / softmax / PV; output garbage)
-  int32_t* fix_cnt;         // [U] in-kernel split merge: parts of each cut unit written so far (nullptr:
-                            // the merge kernel combines them; zeroed by the plan kernel, reset by the merger)
   int cl_n;                 // CTAs per cluster = query blocks per (head, sequence); 1 = no cluster.
                             // With cl_n > 1 the plan is over (head, sequence) groups, the CTAs of a
                             // cluster share each KV tile (TMA multicast) and CTA rank r owns query
@@ -107,15 +107,6 @@ struct DecodeParams {
 // the per-tile softmax path.
 #ifndef GLAD_ROWS_DEFER
 #define GLAD_ROWS_DEFER 0
-#endif
-// swap-AB blocks: two-part cut units merged inside the decode kernel by
-// their first CTA when phase-mask bit 512 is set (A/B, step ms, merge kernel
-// -> in-kernel: C2 GLA-2 0.276 -> 0.270, C2 MLA 0.469 -> 0.458, C4 GTA equal,
-// but the decode kernel alone +5 %: off by default); rows mode keeps the
-// merge kernel (the mid-kernel release fence and the owner's tail reads cost
-// more there: C3 q_len 2 0.199 -> 0.211)
-#ifndef GLAD_FIXUP
-#define GLAD_FIXUP 1
 #endif
 #ifndef GLAD_ROWS_QNB2
 #define GLAD_ROWS_QNB2 0  // two TMEM Q state-part buffers (next segment's Q written during this one)
@@ -478,7 +469,7 @@ template <int NQ>
 __device__ __noinline__ void make_seg(const DecodeParams& p, int u, int cta_t0, int cta_t1, Seg* out) {
   Seg s;
   seg_unit<NQ>(p, u, __ldg(p.seqlens + unit_idx(u * p.cl_n, p.B, p.n_qblk, p.qb_outer).b), s);
-  const int pu0 = __ldg(p.plan + u), pu1 = __ldg(p.plan + u + 1);
+  const int pu0 = __ldg(p.plan + u) + p.seg_cost, pu1 = __ldg(p.plan + u + 1);
   s.t0 = max(cta_t0, pu0) - pu0;
   s.t1 = min(cta_t1, pu1) - pu0;
   s.whole = (s.t0 == 0 && s.t1 == pu1 - pu0);
@@ -494,6 +485,7 @@ __device__ __noinline__ void make_seg(const DecodeParams& p, int u, int cta_t0, 
 struct CtaRange {
   int t0, t1;
 };
+constexpr int kMaxGroups = 64;  // CTA groups (api.cu caps n_groups)
 __device__ __forceinline__ CtaRange cta_range(int c, int G, const int32_t* plan, int U, int n_groups) {
   CtaRange r;
   if (n_groups > 1) {
@@ -511,19 +503,22 @@ __device__ __forceinline__ CtaRange cta_range(int c, int G, const int32_t* plan,
   }
   return r;
 }
-// CTA whose range contains tile t (inverse of cta_range).
-__device__ __forceinline__ int cta_of_tile(int t, int G, const int32_t* plan, int U, int n_groups) {
-  if (n_groups > 1) {
-    const int Gh = G / n_groups, upg = U / n_groups;
-    int g = 0;
-    while (g + 1 < n_groups && __ldg(plan + (g + 1) * upg) <= t) ++g;
-    const int gs = __ldg(plan + g * upg), n = __ldg(plan + (g + 1) * upg) - gs;
-    const int per = (n + Gh - 1) / Gh;
-    return g * Gh + (t - gs) / per;
-  }
-  const int total = __ldg(plan + U);
-  const int per = (total + G - 1) / G;
-  return t / per;
+// The same from the group boundaries gb[g] = plan[g U/n] (g = 0..n, n >= 1
+// groups; n = 1: [0, total]) staged in shared memory (merge kernel).
+__device__ __forceinline__ CtaRange cta_range_gb(int c, int G, const int* gb, int ng) {
+  const int Gh = G / ng, g = c / Gh, k = c - g * Gh;
+  const int gs = gb[g], n = gb[g + 1] - gs, per = (n + Gh - 1) / Gh;
+  CtaRange r;
+  r.t0 = gs + min(n, k * per);
+  r.t1 = gs + min(n, (k + 1) * per);
+  return r;
+}
+__device__ __forceinline__ int cta_of_tile_gb(int t, int G, const int* gb, int ng) {
+  const int Gh = G / ng;
+  int g = 0;
+  while (g + 1 < ng && gb[g + 1] <= t) ++g;
+  const int gs = gb[g], n = gb[g + 1] - gs, per = (n + Gh - 1) / Gh;
+  return g * Gh + (t - gs) / per;
 }
 
 // Segment table entry (32 B, built once in the prologue so that no warp role
@@ -554,47 +549,11 @@ __device__ __forceinline__ Seg seg_from_entry(const DecodeParams& p, const int4*
   return s;
 }
 
-// In-kernel merge of two-part cut units (the common split: a unit cut by
-// one CTA range boundary).  Role of this CTA's segment s: 0 = none (whole
-// unit, or cut into > 2 parts: the merge kernel combines those), 1 = owner
-// (the unit's first CTA: the unit is its LAST segment, so it ends at the end
-// of the kernel; it waits for the other part and writes the merged output),
-// 2 = second part (the next CTA's FIRST segment, finished early: writes its
-// normalised partial + lse and releases it with a fence + counter add).
-__device__ __forceinline__ int pair_role(const DecodeParams& p, const Seg& s) {
-  if (!p.fix_cnt || s.whole) return 0;
-  const int G = gridDim.x;
-  const int pu0 = __ldg(p.plan + s.pi), pu1 = __ldg(p.plan + s.pi + 1);
-  const int cf = cta_of_tile(pu0, G, p.plan, p.n_units, p.n_groups);
-  const int cl = cta_of_tile(pu1 - 1, G, p.plan, p.n_units, p.n_groups);
-  if (cl != cf + 1) return 0;
-  return static_cast<int>(blockIdx.x) == cf ? 1 : 2;
-}
-__device__ __forceinline__ void pair_wait(const DecodeParams& p, int pi, int target) {
-  const long long t0 = clock64();
-  while (ld_acquire_gpu(p.fix_cnt + pi) < target) {
-    __nanosleep(64);
-    if (clock64() - t0 > (1ll << 34)) {
-      printf("glad: split-merge wait watchdog (block %d unit %d)\n", blockIdx.x, pi);
-      __trap();
-    }
-  }
-}
-// weights of the two parts' normalised outputs: exp(lse_x - lse)
-__device__ __forceinline__ void pair_weights(float lse_a, float lse_b, float& wa, float& wb, float& lse) {
-  const float mx = fmaxf(lse_a, lse_b);
-  if (mx == -INFINITY) {
-    wa = wb = 0.f;
-    lse = -INFINITY;
-    return;
-  }
-  const float ea = __expf(lse_a - mx), eb = __expf(lse_b - mx), z = ea + eb;
-  wa = ea / z;
-  wb = eb / z;
-  lse = mx + __logf(z);
-}
-
-template <class C>
+// SP: the small-page producer paths (pages < 16: gather4 / hybrid / cp.async)
+// are compiled in.  A separate instantiation keeps their code (and register
+// pressure) out of the page-run TMA kernels (C2: the hybrid producer's code
+// alone made the page-64 kernel 6 % slower).
+template <class C, bool SP>
 __global__ void __launch_bounds__(C::NTHREADS, 1)
     decode_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUtensorMap lmap,
                   const __grid_constant__ CUtensorMap qmap,
@@ -621,7 +580,6 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
   uint64_t* kv_empty_hi = reinterpret_cast<uint64_t*>(aux + 2592);  // [4] split stages: hi half + P^T free
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(aux + 256);
   int* range_s = reinterpret_cast<int*>(aux + 264);        // [4] cta tile range, #segments, overflow unit
-  float* woth_s = reinterpret_cast<float*>(aux + 2624);   // [NQ <= 64] swap-AB owner merge: weight of the other part
   int4* segtab = reinterpret_cast<int4*>(aux + 3072);      // [MAXSEG][2] (seg_to_entry)
   int* rowtab = reinterpret_cast<int*>(aux + 3072 + C::MAXSEG * 32);  // [T] pool row per tile row (cp path)
   int* vend_s = reinterpret_cast<int*>(aux + 320);         // [NQ] visible-key end per query column
@@ -634,7 +592,9 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
   const int cta = blockIdx.x;
   // small pages with TMA-loaded Q: gather4 + LSU hybrid producer (warps 0 + 3)
   constexpr int G4_LSU_ROWS = (C::T * GLAD_G4_LSU_PCT / 100) & ~3;
-  const bool g4_lsu = G4_LSU_ROWS > 0 && p.g4 == 2 && p.q_tma;
+  const int cp_kv = SP ? p.cp_kv : 0;  // small-page producer modes (0 in the page-run instantiation)
+  const int g4 = SP ? p.g4 : 0;
+  const bool g4_lsu = G4_LSU_ROWS > 0 && g4 == 2 && p.q_tma;
   const bool g4_lsu2 = g4_lsu && GLAD_G4_LSU_WARPS == 2;  // warp 2 (Q loader) copies LSU rows too
   if (GLAD_TRACE && p.trace && threadIdx.x == 0) p.trace[static_cast<size_t>(cta) * kTraceStride + 7] = globaltimer();
 
@@ -664,9 +624,10 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
     if (t0 < t1) {
       for (int base = lo;; base += 32) {
         const int u = base + lane;
-        int pu0 = t1, pu1 = t1;
-        if (u < U) { pu0 = __ldg(p.plan + u); pu1 = __ldg(p.plan + u + 1); }
-        const bool in = u < U && pu0 < t1;
+        int pr0 = t1, pu1 = t1;
+        if (u < U) { pr0 = __ldg(p.plan + u); pu1 = __ldg(p.plan + u + 1); }
+        const bool in = u < U && pr0 < t1;
+        const int pu0 = pr0 + p.seg_cost;  // first real tile of the unit
         const int st0 = max(t0, pu0) - pu0, st1 = min(t1, pu1) - pu0;
         const bool has = in && st1 > st0;
         int L = 0;
@@ -705,7 +666,7 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
   }
   if (threadIdx.x == 0) {
     for (int i = 0; i < NS; ++i) {
-      const int nfull = p.cp_kv ? (p.q_tma ? 64 : 32) : (g4_lsu ? 1 + 32 * (1 + (g4_lsu2 ? 1 : 0) + (GLAD_G4_LSU_W0 ? 1 : 0)) : 1);  // cp.async lanes (+ the expect_tx arrival)
+      const int nfull = cp_kv ? (p.q_tma ? 64 : 32) : (g4_lsu ? 1 + 32 * (1 + (g4_lsu2 ? 1 : 0) + (GLAD_G4_LSU_W0 ? 1 : 0)) : 1);  // cp.async lanes (+ the expect_tx arrival)
       mbar_init(&kv_full[i], nfull);
       mbar_init(&kv_empty[i], 1);
       mbar_init(&kv_full_hi[i], nfull);
@@ -726,7 +687,7 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
     }
     fence_barrier_init();
     tma_prefetch_desc(&tmap);
-    if (!p.cp_kv) tma_prefetch_desc(&lmap);  // latent boxes, or the gather4 row map
+    if (!cp_kv) tma_prefetch_desc(&lmap);  // latent boxes, or the gather4 row map
     if (p.q_tma) tma_prefetch_desc(&qmap);
   }
   if (warp == 2) { tmem_alloc(tmem_slot, C::TMEM_COLS); tmem_relinquish(); }
@@ -783,7 +744,7 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
     }
   };
 
-  if (p.cp_kv && (warp == 0 || (warp == 3 && p.q_tma))) {
+  if (cp_kv && (warp == 0 || (warp == 3 && p.q_tma))) {
     // ============ cooperative cp.async producer for small pages ============
     // The paper's distributed offset calculation on B200 terms: each lane
     // resolves the page-table entry of "its" rows (one lookup per token, an
@@ -867,7 +828,7 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
         }
       }
     }
-  } else if (warp == 0 || (warp == 3 && p.g4 && p.q_tma) || (warp == 2 && g4_lsu2)) {
+  } else if (warp == 0 || (warp == 3 && g4 && p.q_tma) || (warp == 2 && g4_lsu2)) {
     // ========================= TMA producer (all 32 lanes issue) =========================
     // (gather4 mode with TMA-loaded Q: warp 3 is a second producer warp that
     // issues half of every tile's row groups)
@@ -971,7 +932,7 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
         // the page lookup of this lane's page run is done before the stage
         // wait: after the release only the TMA issue remains on the critical path
         constexpr int NIT0 = C::SPLIT ? 1 : 2;  // first-issue items per page run (split: lo; else latent + RoPE)
-        const int row0 = (loader && !p.g4 && lane < nbox * NIT0) ? item_row(bt_row, p0, lane / NIT0) : 0;
+        const int row0 = (loader && !g4 && lane < nbox * NIT0) ? item_row(bt_row, p0, lane / NIT0) : 0;
         if (trace && lane == 0 && warp == 0 && it == 0) {
           if (row0 == 0x7fffffff) __nanosleep(1);  // debug: wait for the lookup itself
           trace[6] = globaltimer();
@@ -979,10 +940,10 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
         const uint32_t ph = ((it / NS) & 1) ^ 1;
         mbar_wait(&kv_empty[stage], ph);
         // cluster multicast and gather4 fill the whole stage at once
-        const bool whole_stage = !C::SPLIT || p.cl_n > 1 || p.g4;
+        const bool whole_stage = !C::SPLIT || p.cl_n > 1 || g4;
         if (C::SPLIT && whole_stage) mbar_wait(&kv_empty_hi[stage], ph);
         if (trace && lane == 0 && warp == 0 && it < kTraceTiles) trace[13 + 12 * it] = globaltimer();
-        if (lane == 0 && !p.g4)
+        if (lane == 0 && !g4)
           mbar_arrive_expect_tx(&kv_full[stage], static_cast<uint32_t>(nbox * box_rows * (C::SPLIT ? C::NLO : C::NCH) * 128));
         if (p.cl_n > 1) {  // stage free here -> tell the loader; the loader waits for every CTA
           if (lane == 0) mbar_arrive_cluster(&cl_empty[stage], 0);
@@ -990,7 +951,7 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
         }
         __syncwarp();
         const uint32_t stage_addr = sbase + stage * C::STAGE;
-        if (p.g4) {
+        if (g4) {
           // small pages: one gather4 per (4 token rows, 64-column chunk) —
           // the TMA unit does the per-row address generation of P:308-314;
           // each lane resolves the block-table entries of its row groups
@@ -1089,13 +1050,13 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
           }
         }
         if (trace && lane == 0 && warp == 0 && it < kTraceTiles) trace[8 + 12 * it] = globaltimer();
-        if (C::L2PF && !p.g4 && loader && !pf_ready) {
+        if (C::L2PF && !g4 && loader && !pf_ready) {
           pf_advance();
           for (int i = 0; i < NS + GLAD_PF_EXTRA + it && pvalid; ++i) pf_advance();
           pf_ready = true;
           if (trace && lane == 0 && warp == 0) trace[kTraceStride - 6] = globaltimer();  // debug: prefetch cursor ready
         }
-        if (C::L2PF && !p.g4 && pvalid && loader) {  // L2 prefetch of tile it + NS, after the stage load so it never delays it
+        if (C::L2PF && !g4 && pvalid && loader) {  // L2 prefetch of tile it + NS, after the stage load so it never delays it
           issue_tile(ps, ptl, 0, true, -1);
           pf_advance();
         }
@@ -1208,7 +1169,7 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
             if (trace && lane == 0 && next_qk == 0) trace[1] = globaltimer();
             if (trace && lane == 0 && next_qk < kTraceTiles) trace[9 + 12 * next_qk] = globaltimer();
             tc_fence_after();
-            if (p.cp_kv || g4_lsu) fence_proxy_async_smem();
+            if (cp_kv || g4_lsu) fence_proxy_async_smem();
           }
         }
         if (qk_go) {
@@ -1299,7 +1260,7 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
         const int stage = next_qk % NS;
         const int sb = next_qk & 1;
         tc_fence_after();
-        if (p.cp_kv || g4_lsu) fence_proxy_async_smem();  // cp.async (generic proxy) writes -> UMMA (async proxy) reads
+        if (cp_kv || g4_lsu) fence_proxy_async_smem();  // cp.async (generic proxy) writes -> UMMA (async proxy) reads
         const uint32_t d = tm + sb * NQ;
         const uint64_t ad = desc_kmajor_sw128(sbase + stage * C::STAGE, C::LGRP);
         const uint64_t rd = desc_kmajor_sw128(sbase + stage * C::STAGE + C::OFF_R);
@@ -1424,7 +1385,7 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
       }
       if (trace && lane == 0) trace[3] = cp.seg + 1;
     }
-  } else if (warp < 4 && !(warp == 3 && (p.cp_kv || p.g4) && p.q_tma) && !(warp == 2 && g4_lsu2)) {
+  } else if (warp < 4 && !(warp == 3 && (cp_kv || g4) && p.q_tma) && !(warp == 2 && g4_lsu2)) {
     // ========================= Q loader: TMA (one thread) or cp.async (64 threads) =========================
     const int tid = threadIdx.x - 64;
     constexpr int QCH0 = C::ROWS ? C::NCH_QK : 0;  // first Q chunk staged in shared memory
@@ -1815,9 +1776,7 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
     // 1/l lives in einv_s[seg % NOB] until then.
     float* einv_s = reinterpret_cast<float*>(aux + 3072 + C::MAXSEG * 32 + T * 4);  // [NOB][NQ]
     int e_blk = C::NBLK_O;  // next block of the pending epilogue (NBLK_O = none pending)
-    int e_seg = 0, e_j = 0, e_ncols = 0, e_j0 = 0, e_slot = 0, e_pi = 0;
-    bool e_rel = false;                // pending segment is the second part of a two-part unit
-    const float* e_oth = nullptr;      // owner: the other part's o_part rows (column c0)
+    int e_seg = 0, e_j = 0, e_ncols = 0, e_j0 = 0, e_slot = 0;
     bool e_whole = false;
     size_t e_row0 = 0;
     auto epi_block = [&]() {
@@ -1849,17 +1808,6 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
           for (int n = 0; n < CW; n += 4) {
             const float4 a = ld_shared_f4(inv_addr + n * 4);
             v[n] = o[n] * a.x; v[n + 1] = o[n + 1] * a.y; v[n + 2] = o[n + 2] * a.z; v[n + 3] = o[n + 3] * a.w;
-          }
-          if (e_oth) {  // owner of a two-part unit: + w_other * the other part's normalised O
-            const uint32_t w_addr = smem_u32(woth_s + c0);
-#pragma unroll
-            for (int n = 0; n < CW; n += 4) {
-              const float4 w = ld_shared_f4(w_addr + n * 4);
-              v[n] += w.x * __ldcg(e_oth + static_cast<size_t>(n) * C::D_V + d);
-              v[n + 1] += w.y * __ldcg(e_oth + static_cast<size_t>(n + 1) * C::D_V + d);
-              v[n + 2] += w.z * __ldcg(e_oth + static_cast<size_t>(n + 2) * C::D_V + d);
-              v[n + 3] += w.w * __ldcg(e_oth + static_cast<size_t>(n + 3) * C::D_V + d);
-            }
           }
           const bool odd = lane & 1;
 #pragma unroll
@@ -1904,11 +1852,6 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
         }
       }
       ++e_blk;
-      if (e_rel && e_blk == C::NBLK_O) {  // second part of a two-part unit written: release it (per WG)
-        __threadfence();
-        named_bar_sync(bar_id, 128);
-        if (r == 0) atomicAdd(p.fix_cnt + e_pi, 1);
-      }
     };
     int k = 0, u = 0, seg = 0, it = 0;
     Seg s;
@@ -2114,36 +2057,22 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
       const float cs = warp_col_reduce<HC, false, LANES>(l, lane);
       if ((lane & ((1 << col_shift<HC, LANES>()) - 1)) == 0)
         red[(wg * 4 + wq) * 32 + (cb - c0) + ((lane & (LANES - 1)) >> col_shift<HC, LANES>())] = cs;
-      const int role = pair_role(p, s);
-      if (role == 1 && r == 0) {  // owner: the second part (both its WGs) must be out
-        pair_wait(p, s.pi, 2);
-        if (atomicAdd(p.fix_cnt + s.pi, 1) == 3) p.fix_cnt[s.pi] = 0;  // both owner WGs past: reset for the next launch
-      }
       named_bar_sync(bar_id, 128);
       // partial slot: 2 per range — the range's first segment (2c) or its
       // last one (2c + 1); only those two can be cut by a range boundary
       const int slot = (2 * (cta / p.cl_n) + (seg == 0 ? 0 : 1)) * p.cl_n + cta % p.cl_n;
-      const size_t slot_oth = static_cast<size_t>(2 * (cta + 1));  // owner: the next CTA's first-segment slot
       if (r < CW) {  // fold the row sum into alpha_s as 1/l (reused below) and write lse
         const float* rr = red + wg * 128 + r;
         const float ls = (rr[0] + rr[32]) + (rr[64] + rr[96]);
         alpha_s[c0 + r] = ls > 0.f ? 1.f / ls : 0.f;
         if (c0 + r < s.nq) {
           const float lse = ls > 0.f ? (m_run[c0 + r] + __log2f(ls)) * 0.69314718055994531f : -INFINITY;
-          const int ng = s.n0 + c0 + r, t = ng / p.g_q, h = s.head * p.g_q + (ng - t * p.g_q);
-          if (role == 1) {
-            float wa, wb, lse_t;
-            pair_weights(lse, __ldcg(p.lse_part + slot_oth * NQ + c0 + r), wa, wb, lse_t);
-            p.lse[(static_cast<size_t>(s.b) * p.Lq + t) * p.H + h] = lse_t;
-            alpha_s[c0 + r] *= wa;
-            woth_s[c0 + r] = wb;
-          } else if (s.whole) {
+          if (s.whole) {
+            const int ng = s.n0 + c0 + r, t = ng / p.g_q, h = s.head * p.g_q + (ng - t * p.g_q);
             p.lse[(static_cast<size_t>(s.b) * p.Lq + t) * p.H + h] = lse;
           } else {
             p.lse_part[static_cast<size_t>(slot) * NQ + c0 + r] = lse;
           }
-        } else if (role == 1) {
-          woth_s[c0 + r] = 0.f;
         }
       }
       // pending epilogue of this segment: 1/l to einv_s, output addressing
@@ -2154,15 +2083,12 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
       e_blk = 0;
       e_seg = seg;
       e_j = it - 1;  // last tile of this segment
-      e_whole = s.whole || role == 1;  // the owner writes the merged output like a whole unit
+      e_whole = s.whole;
       e_slot = slot;
-      e_pi = s.pi;
-      e_rel = (role == 2);
-      e_oth = role == 1 ? p.o_part + (slot_oth * NQ + c0) * C::D_V : nullptr;
       e_ncols = min(CW, s.nq - c0);
       e_j0 = 0;
       e_row0 = 0;
-      if (e_whole) {
+      if (s.whole) {
         const int ng = s.n0 + c0, t = ng / p.g_q;
         e_j0 = ng - t * p.g_q;
         e_row0 = (static_cast<size_t>(s.b) * p.Lq + t) * p.H + s.head * p.g_q + e_j0;

@@ -7,16 +7,18 @@ namespace glad {
 
 // The > 48 KB dynamic shared memory opt-in is a per-device (per-context)
 // function attribute: cached per device ordinal, set on first use on each.
-template <class C>
+template <class C, bool SP>
 cudaError_t set_smem_attr() {
-  return set_func_smem_once(reinterpret_cast<const void*>(decode_kernel<C>), C::SMEM_BYTES);
+  return set_func_smem_once(reinterpret_cast<const void*>(decode_kernel<C, SP>), C::SMEM_BYTES);
 }
 
 template <int DV, int DKN, int DR, int NQ, int T, int DS>
 cudaError_t launch_one(const CUtensorMap& tmap, const CUtensorMap& lmap, const CUtensorMap& qmap,
                        const DecodeParams& p, int grid, cudaStream_t stream) {
   using C = DecodeCfg<DV, DKN, DR, NQ, T, DS>;
-  cudaError_t e = set_smem_attr<C>();
+  // pages < 16 (gather4 / hybrid / cp.async producers): the SP instantiation
+  const bool sp = p.cp_kv || p.g4;
+  cudaError_t e = sp ? set_smem_attr<C, true>() : set_smem_attr<C, false>();
   if (e != cudaSuccess) return e;
   // PDL: the prologue overlaps the plan kernel's tail (griddep_wait in the kernel)
   cudaLaunchConfig_t cfg{};
@@ -40,7 +42,8 @@ cudaError_t launch_one(const CUtensorMap& tmap, const CUtensorMap& lmap, const C
   }
   cfg.attrs = attr;
   cfg.numAttrs = na;
-  return cudaLaunchKernelEx(&cfg, decode_kernel<C>, tmap, lmap, qmap, p);
+  return sp ? cudaLaunchKernelEx(&cfg, decode_kernel<C, true>, tmap, lmap, qmap, p)
+            : cudaLaunchKernelEx(&cfg, decode_kernel<C, false>, tmap, lmap, qmap, p);
 }
 
 // Calls f.template run<C>() for the DecodeCfg matching (key, T); returns
@@ -107,7 +110,7 @@ struct ClustersF {
   int* out;
   template <class C>
   cudaError_t run() {
-    cudaError_t e = set_smem_attr<C>();
+    cudaError_t e = set_smem_attr<C, false>();  // clusters: pages >= 16 only
     if (e != cudaSuccess) return e;
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(cl_n * 64);
@@ -120,7 +123,7 @@ struct ClustersF {
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return cudaOccupancyMaxActiveClusters(out, decode_kernel<C>, &cfg);
+    return cudaOccupancyMaxActiveClusters(out, decode_kernel<C, false>, &cfg);
   }
 };
 

@@ -69,12 +69,12 @@ int decode_max_clusters(const DecodeKey& key, int cl_n);  // resident clusters o
 int decode_max_nq(int d_v);
 bool decode_rows_supported(const DecodeKey& key);  // rows mode (nq = 128) exists for these dims (any t)
 
-cudaError_t launch_plan(const int32_t* seqlens, int32_t* plan, int32_t* cnt, int U, int cl_n, int B, int tile, int n_qblk,
+cudaError_t launch_plan(const int32_t* seqlens, int32_t* plan, int U, int seg_cost, int cl_n, int B, int tile, int n_qblk,
                         int qb_outer, int nq_blk, int Lq, int g_q, int causal, int H, int d_v, void* out, float* lse,
                         uint64_t* trace, cudaStream_t stream);
 cudaError_t launch_merge_split(const int32_t* plan, const float* o_part, const float* lse_part, int G, int cl_n,
                                int U, int nq_blk, int n_qblk, int qb_outer, int B, int n_groups, int g_q, int Lq,
-                               int H, int d_v, int pair_merged, void* out, float* lse, cudaStream_t stream);
+                               int H, int d_v, int seg_cost, void* out, float* lse, cudaStream_t stream);
 cudaError_t launch_append(void* pool, int64_t row_stride, int page_size, const int32_t* block_table,
                           int32_t bt_stride, const int32_t* seqlens_before, const void* rows, int32_t B,
                           int32_t n_new, int32_t width, cudaStream_t stream);

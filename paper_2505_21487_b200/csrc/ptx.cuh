@@ -62,11 +62,6 @@ __device__ __forceinline__ bool mbar_try_wait_hint(uint32_t addr, uint32_t parit
 // Both are no-ops for a normally launched kernel.
 __device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void griddep_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
-__device__ __forceinline__ int ld_acquire_gpu(const int* p) {
-  int v;
-  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
 // Non-suspending probe (for schedulers that poll several barriers).
 __device__ __forceinline__ bool mbar_test_wait(uint32_t addr, uint32_t parity) {
   uint32_t ok;

@@ -215,24 +215,18 @@ def test_small_page_producers(cfg, mask, tile):
     check(out, lse, o_ref, lse_ref, what=f"mask={mask} {cfg}")
 
 
-@pytest.mark.parametrize("mask", [7, 7 | 512], ids=["merge_kernel", "in_kernel_merge"])
 @pytest.mark.parametrize("cfg", [(3, 1, 128, 2, 256, 64, [1500, 777, 4096], 64, 7),     # GLA-2 swap-AB, 3-part units
                                  (2, 1, 128, 1, 512, 64, [2048, 900], 64, 64),         # MLA, query-block groups
                                  (3, 2, 128, 2, 256, 64, [3000, 129, 1025], 16, 5),    # rows mode (q_len 2)
                                  (2, 1, 16, 2, 128, 32, [5000, 1], 1, 11),             # page 1, one tiny unit
                                  (4, 1, 64, 2, 256, 64, [640, 640, 640, 640], 64, 0)])  # 148 CTAs, many cuts
-def test_split_merge_paths(cfg, mask, tile):
-    """Units cut by CTA range boundaries: every cut unit merged by the merge
-    kernel (default), and (phase-mask bit 512) two-part units merged inside
-    the decode kernel by their first CTA with longer ones left to the merge
-    kernel, against the oracle."""
+def test_split_merge_paths(cfg, tile):
+    """Units cut by CTA range boundaries (ranges balanced over tiles plus a
+    per-segment switch cost, rows mode) merged by the merge kernel, against
+    the oracle."""
     B, Lq, H, h_c, d_c, d_R, lens, page, ctas = cfg
-    glad.debug_set_phase_mask(mask)
-    try:
-        out, lse, o_ref, lse_ref = run_latent(B, Lq, H, h_c, d_c, d_R, np.array(lens), page, ctas=ctas, seed=41)
-    finally:
-        glad.debug_set_phase_mask(7)
-    check(out, lse, o_ref, lse_ref, what=f"mask={mask} {cfg}")
+    out, lse, o_ref, lse_ref = run_latent(B, Lq, H, h_c, d_c, d_R, np.array(lens), page, ctas=ctas, seed=41)
+    check(out, lse, o_ref, lse_ref, what=f"{cfg}")
 
 
 @pytest.mark.parametrize("mask", [7, 7 | 128], ids=["qb_groups", "qb_inner"])
