@@ -19,7 +19,10 @@
 #define GLAD_SEG_COST 0
 #endif
 #ifndef GLAD_SEG_COST_ROWS
-#define GLAD_SEG_COST_ROWS 6
+#define GLAD_SEG_COST_ROWS 12  // rows mode, d_v >= 256
+#endif
+#ifndef GLAD_SEG_COST_ROWS128
+#define GLAD_SEG_COST_ROWS128 4  // rows mode, d_v = 128
 #endif
 #ifndef GLAD_MIN_GROUP_CTAS
 #define GLAD_MIN_GROUP_CTAS 8
@@ -327,10 +330,13 @@ glad_status decode_common(Variant v, const void* q, const void* pool, const glad
   p.g4 = g4 ? ((g_phase_mask & 256) ? 1 : 2) : 0;  // bit 256: gather4 alone (no LSU rows)
   p.n_groups = n_groups;
   // segment-switch cost in virtual tiles, so that the ranges balance work +
-  // switches (measured with the trace: ~2.5 tiles per switch in swap-AB, ~9
-  // in rows mode; A/B decode ms, 0 -> 6 in rows mode: C3 q_len 2 0.1728 ->
-  // 0.1680; 0 -> 2 in swap-AB: C2 equal, C2 page 1 +1 %, MLA -2 %)
-  p.seg_cost = g.key.nq == 128 ? GLAD_SEG_COST_ROWS : GLAD_SEG_COST;
+  // switches (trace: ~2.5 tiles per switch in swap-AB, ~9 in rows mode at
+  // d_v = 256).  A/B decode ms over rows-mode costs 0 / 4 / 6 / 9 / 12: C3
+  // q_len 2 0.173 / 0.172 / 0.172 / 0.170 / 0.170, absorbed prefill (d_v 256)
+  // - / 3.25 / 2.84 / 2.49 / 2.46, GTA prefill (d_v 128, cheaper tiles and
+  // switches) - / 0.819 / 0.843 / 0.878 / 0.907, materialised prefill flat;
+  // swap-AB 0 / 2 / 3: C2 equal, C5 TP8 shard -2 % at 2, C2 page 1 +1 %.
+  p.seg_cost = g.key.nq != 128 ? GLAD_SEG_COST : (g.key.d_v >= 256 ? GLAD_SEG_COST_ROWS : GLAD_SEG_COST_ROWS128);
   p.qb_outer = qb_outer;
   p.q_box_h = q_box_h;
   p.q_box_t = q_box_t;
