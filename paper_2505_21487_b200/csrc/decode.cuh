@@ -549,11 +549,13 @@ __device__ __forceinline__ Seg seg_from_entry(const DecodeParams& p, const int4*
   return s;
 }
 
-// SP: the small-page producer paths (pages < 16: gather4 / hybrid / cp.async)
-// are compiled in.  A separate instantiation keeps their code (and register
-// pressure) out of the page-run TMA kernels (C2: the hybrid producer's code
-// alone made the page-64 kernel 6 % slower).
-template <class C, bool SP>
+// SP: producer paths compiled in — 0: page-run TMA boxes only; 1: + pages <
+// 16 through gather4 / the hybrid gather4 + LSU producer; 2: + the
+// cooperative cp.async producer (phase-mask bit 32).  Separate
+// instantiations keep their code (and register pressure) out of each other:
+// the hybrid producer's code alone made the page-64 kernel 6 % slower, the
+// cp.async producer's added 98 B of spills to the hybrid one.
+template <class C, int SP>
 __global__ void __launch_bounds__(C::NTHREADS, 1)
     decode_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUtensorMap lmap,
                   const __grid_constant__ CUtensorMap qmap,
@@ -592,8 +594,8 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
   const int cta = blockIdx.x;
   // small pages with TMA-loaded Q: gather4 + LSU hybrid producer (warps 0 + 3)
   constexpr int G4_LSU_ROWS = (C::T * GLAD_G4_LSU_PCT / 100) & ~3;
-  const int cp_kv = SP ? p.cp_kv : 0;  // small-page producer modes (0 in the page-run instantiation)
-  const int g4 = SP ? p.g4 : 0;
+  const int cp_kv = SP == 2 ? p.cp_kv : 0;  // small-page producer modes (0 in the page-run instantiation)
+  const int g4 = SP == 1 ? p.g4 : 0;
   const bool g4_lsu = G4_LSU_ROWS > 0 && g4 == 2 && p.q_tma;
   const bool g4_lsu2 = g4_lsu && GLAD_G4_LSU_WARPS == 2;  // warp 2 (Q loader) copies LSU rows too
   if (GLAD_TRACE && p.trace && threadIdx.x == 0) p.trace[static_cast<size_t>(cta) * kTraceStride + 7] = globaltimer();

@@ -7,7 +7,7 @@ namespace glad {
 
 // The > 48 KB dynamic shared memory opt-in is a per-device (per-context)
 // function attribute: cached per device ordinal, set on first use on each.
-template <class C, bool SP>
+template <class C, int SP>
 cudaError_t set_smem_attr() {
   return set_func_smem_once(reinterpret_cast<const void*>(decode_kernel<C, SP>), C::SMEM_BYTES);
 }
@@ -16,9 +16,9 @@ template <int DV, int DKN, int DR, int NQ, int T, int DS>
 cudaError_t launch_one(const CUtensorMap& tmap, const CUtensorMap& lmap, const CUtensorMap& qmap,
                        const DecodeParams& p, int grid, cudaStream_t stream) {
   using C = DecodeCfg<DV, DKN, DR, NQ, T, DS>;
-  // pages < 16 (gather4 / hybrid / cp.async producers): the SP instantiation
-  const bool sp = p.cp_kv || p.g4;
-  cudaError_t e = sp ? set_smem_attr<C, true>() : set_smem_attr<C, false>();
+  // pages < 16: the gather4 / hybrid (SP 1) or cp.async (SP 2) instantiation
+  const int sp = p.cp_kv ? 2 : (p.g4 ? 1 : 0);
+  cudaError_t e = sp == 2 ? set_smem_attr<C, 2>() : sp == 1 ? set_smem_attr<C, 1>() : set_smem_attr<C, 0>();
   if (e != cudaSuccess) return e;
   // PDL: the prologue overlaps the plan kernel's tail (griddep_wait in the kernel)
   cudaLaunchConfig_t cfg{};
@@ -42,8 +42,9 @@ cudaError_t launch_one(const CUtensorMap& tmap, const CUtensorMap& lmap, const C
   }
   cfg.attrs = attr;
   cfg.numAttrs = na;
-  return sp ? cudaLaunchKernelEx(&cfg, decode_kernel<C, true>, tmap, lmap, qmap, p)
-            : cudaLaunchKernelEx(&cfg, decode_kernel<C, false>, tmap, lmap, qmap, p);
+  return sp == 2   ? cudaLaunchKernelEx(&cfg, decode_kernel<C, 2>, tmap, lmap, qmap, p)
+         : sp == 1 ? cudaLaunchKernelEx(&cfg, decode_kernel<C, 1>, tmap, lmap, qmap, p)
+                   : cudaLaunchKernelEx(&cfg, decode_kernel<C, 0>, tmap, lmap, qmap, p);
 }
 
 // Calls f.template run<C>() for the DecodeCfg matching (key, T); returns
@@ -110,7 +111,7 @@ struct ClustersF {
   int* out;
   template <class C>
   cudaError_t run() {
-    cudaError_t e = set_smem_attr<C, false>();  // clusters: pages >= 16 only
+    cudaError_t e = set_smem_attr<C, 0>();  // clusters: pages >= 16 only
     if (e != cudaSuccess) return e;
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(cl_n * 64);
@@ -123,7 +124,7 @@ struct ClustersF {
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return cudaOccupancyMaxActiveClusters(out, decode_kernel<C, false>, &cfg);
+    return cudaOccupancyMaxActiveClusters(out, decode_kernel<C, 0>, &cfg);
   }
 };
 
