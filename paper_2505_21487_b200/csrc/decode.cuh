@@ -129,6 +129,9 @@ struct DecodeParams {
 #ifndef GLAD_NS_CAP
 #define GLAD_NS_CAP 4
 #endif
+#ifndef GLAD_PF_MIN_BOX
+#define GLAD_PF_MIN_BOX 64
+#endif
 #ifndef GLAD_PF_BULK
 #define GLAD_PF_BULK 0  // L2 prefetch: 0 = TMA tensor prefetch of the tile's boxes, 1 = bulk page runs, 2 = bulk, head-0 CTAs only
 #endif
@@ -1052,13 +1055,17 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
           }
         }
         if (trace && lane == 0 && warp == 0 && it < kTraceTiles) trace[8 + 12 * it] = globaltimer();
-        if (C::L2PF && !g4 && loader && !pf_ready) {
+        // (page runs shorter than GLAD_PF_MIN_BOX rows: no L2 prefetch — its
+        // TMA ops per tile grow with the run count; C2 page 16 soaked decode
+        // 0.323 -> 0.276 ms without it, page 64 within noise)
+        const bool l2pf = C::L2PF && !g4 && box_rows >= GLAD_PF_MIN_BOX;
+        if (l2pf && loader && !pf_ready) {
           pf_advance();
           for (int i = 0; i < NS + GLAD_PF_EXTRA + it && pvalid; ++i) pf_advance();
           pf_ready = true;
           if (trace && lane == 0 && warp == 0) trace[kTraceStride - 6] = globaltimer();  // debug: prefetch cursor ready
         }
-        if (C::L2PF && !g4 && pvalid && loader) {  // L2 prefetch of tile it + NS, after the stage load so it never delays it
+        if (l2pf && pvalid && loader) {  // L2 prefetch of tile it + NS, after the stage load so it never delays it
           issue_tile(ps, ptl, 0, true, -1);
           pf_advance();
         }
