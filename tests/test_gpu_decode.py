@@ -229,6 +229,19 @@ def test_split_merge_paths(cfg, tile):
     check(out, lse, o_ref, lse_ref, what=f"{cfg}")
 
 
+@pytest.mark.parametrize("cfg", [(8, 2, 128, 2, 256, 64, [1, 2, 63, 64, 65, 130, 700, 3], 16, 37),  # rows, tiny units
+                                 (6, 4, 128, 2, 256, 64, [5, 900, 1, 64, 2000, 129], 64, 148),   # rows, 2 blocks
+                                 (5, 2, 128, 2, 256, 64, [3000, 7, 2, 640, 1], 1, 9)])            # rows, page 1
+def test_segment_cost_ranges(cfg, tile):
+    """Rows mode plans a few virtual tiles per unit (segment-switch cost), so
+    CTA ranges can start or end inside a unit's virtual prefix and cover no
+    real tile of it: such units must be neither decoded twice nor merged
+    from an empty part.  Many tiny units and odd CTA counts, vs the oracle."""
+    B, Lq, H, h_c, d_c, d_R, lens, page, ctas = cfg
+    out, lse, o_ref, lse_ref = run_latent(B, Lq, H, h_c, d_c, d_R, np.array(lens), page, ctas=ctas, seed=43)
+    check(out, lse, o_ref, lse_ref, what=f"{cfg}")
+
+
 @pytest.mark.parametrize("mask", [7, 7 | 128], ids=["qb_groups", "qb_inner"])
 @pytest.mark.parametrize("cfg", [(4, 1, 128, 1, 512, 64, [900, 333, 1, 2048], 64, 64),   # MLA: 2 query blocks
                                  (3, 2, 128, 1, 512, 64, [700, 1500, 64], 16, 0),        # MLA q_len 2: 4 blocks
