@@ -117,6 +117,9 @@ struct DecodeParams {
 #ifndef GLAD_ROWS_NS_CAP
 #define GLAD_ROWS_NS_CAP 4
 #endif
+#ifndef GLAD_POLY_GTA_ROWS
+#define GLAD_POLY_GTA_ROWS 4  // GTA rows mode (A/B, GTA prefill: 0.815 -> 0.798 ms at 4, 0.853 at 2)
+#endif
 #ifndef GLAD_POLY_EVERY
 #define GLAD_POLY_EVERY 0  // every k-th pair of exponentials via exp2_poly2 (0: all on MUFU)
 #endif
@@ -1464,6 +1467,9 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
     constexpr int DH = C::D_V / NWGR;    // O columns per thread
     constexpr uint32_t kTrig = 0x4380u;  // bf16 bits of 2^TAU = 256
     static_assert(TAU == 8.f, "kTrig encodes 2^TAU");
+    // every POLY-th pair of exponentials on the FMA pipe: only the GTA rows
+    // shape (d_v 128, key 64: the least tensor work per exponential) gains
+    constexpr int POLY = (C::D_V == 128 && C::D_KN == 64) ? GLAD_POLY_GTA_ROWS : GLAD_POLY_EVERY;
     static_assert(TH % 16 == 0 && NP % 8 == 0 && DH % 32 == 0, "rows mode tile split");
     const int wg = (warp - 4) >> 2;
     const int wq = warp & 3;
@@ -1583,7 +1589,7 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
 #pragma unroll
           for (int j = 0; j < TH; j += 2) {
             const float2 e = ffma2(make_float2(x[j], x[j + 1]), make_float2(sl2, sl2), make_float2(nm, nm));
-            if (GLAD_POLY_EVERY && ((j / 2) % GLAD_POLY_EVERY) == GLAD_POLY_EVERY - 1) {
+            if (POLY && ((j / 2) % POLY) == POLY - 1) {
               const float2 y = exp2_poly2(e);  // part of the exponentials on the FMA pipe
               pk[j / 2] = pack_bf16x2(y.x, y.y);
             } else {
